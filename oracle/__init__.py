@@ -1,0 +1,160 @@
+"""CPU oracle for the factorization-based DPP sampler -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product package
+``paper_1905_00165_b200`` never imports it and shares no code with it.
+
+Thin ctypes marshalling over ``dpp_oracle.c`` (plain C, fp64, one thread, no
+BLAS), which follows Listing 1 of arXiv 1905.00165 step by
+step; see the header of that file for the readings R1-R8 it implements.
+
+Pinned by ``tests/test_oracle_*.py`` (-m "not gpu"):
+  * Philox:    KAT against curand's ``curand_Philox4x32_10`` (library routine).
+  * decisions: K = diag(p) closed form; K = 0, K = I.
+  * law:       brute-force subset frequencies vs |det(K - 1_{S^c})|.
+  * structure: projection cardinality = rank, UST spanning
+               trees with loglik -ln tau(G), Aztec tilings with
+               loglik -d(d+1)/2 ln 2.
+  * factor:    L D L^H = K - 1_{Y^c}, L U = K - 1_{Y^c}; loglik = ln|det| (slogdet).
+  * prefix:    decisions on K[:m,:m] = first m decisions on K (loop invariant,
+               PAPER.md:402-405).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "dpp_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+HERM_D, HERM_Z, LU_Z = 0, 1, 2
+TIE_TOL = 1e-9
+RANGE_TOL = 1e-8
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [
+        ("n_kept", ctypes.c_int32),
+        ("n_ties", ctypes.c_int32),
+        ("first_tie", ctypes.c_int32),
+        ("n_out_of_range", ctypes.c_int32),
+        ("min_abs_pivot", ctypes.c_double),
+        ("max_abs_imag_pivot", ctypes.c_double),
+    ]
+
+
+@dataclass
+class OracleResult:
+    mask: np.ndarray          # uint8[n], 1 = kept
+    loglik: float
+    factor: np.ndarray        # in-place factor of K - 1_{Y^c} (column-major semantics)
+    n_kept: int
+    n_ties: int
+    first_tie: int
+    n_out_of_range: int
+    min_abs_pivot: float
+    max_abs_imag_pivot: float
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (gcc -O2 -ffp-contract=off, one thread, no BLAS)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-std=c11", "-shared", "-fPIC",
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        P = ctypes.c_void_p
+        for name in ("oracle_sample_herm_d", "oracle_sample_herm_z", "oracle_sample_lu_z"):
+            f = getattr(_lib, name)
+            f.restype = ctypes.c_int
+            f.argtypes = [ctypes.c_int64, P, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, P,
+                          ctypes.c_double, ctypes.c_double, P, P, P]
+        _lib.oracle_uniform.restype = ctypes.c_double
+        _lib.oracle_uniform.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64]
+        _lib.oracle_philox4x32_10.restype = None
+        _lib.oracle_philox4x32_10.argtypes = [P, P, P]
+        _lib.oracle_sample_many.restype = ctypes.c_int
+        _lib.oracle_sample_many.argtypes = [ctypes.c_int, ctypes.c_int64, P, ctypes.c_int64,
+                                            ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, P, P]
+    return _lib
+
+
+def philox4x32_10(ctr, key) -> tuple:
+    c = (ctypes.c_uint32 * 4)(*[int(v) & 0xFFFFFFFF for v in ctr])
+    k = (ctypes.c_uint32 * 2)(*[int(v) & 0xFFFFFFFF for v in key])
+    o = (ctypes.c_uint32 * 4)()
+    lib().oracle_philox4x32_10(c, k, o)
+    return tuple(int(v) for v in o)
+
+
+def uniform(seed: int, j: int, b: int = 0) -> float:
+    return float(lib().oracle_uniform(seed, j, b))
+
+
+def _as_colmajor(K: np.ndarray, kind: int) -> np.ndarray:
+    dt = np.float64 if kind == HERM_D else np.complex128
+    return np.array(K, dtype=dt, order="F", copy=True)
+
+
+def sample(kind: int, K: np.ndarray, seed: int = 0, b: int = 0, forced=None,
+           tie_tol: float = TIE_TOL, range_tol: float = RANGE_TOL) -> OracleResult:
+    """One sample of DPP(K) by Listing 1 (kind = HERM_D | HERM_Z | LU_Z)."""
+    A = _as_colmajor(K, kind)
+    n = A.shape[0]
+    assert A.shape == (n, n)
+    mask = np.zeros(max(n, 1), dtype=np.uint8)
+    ll = ctypes.c_double(0.0)
+    info = _Info()
+    fptr = None
+    if forced is not None:
+        forced = np.ascontiguousarray(np.asarray(forced, dtype=np.uint8))
+        assert forced.shape == (n,)
+        fptr = forced.ctypes.data
+    fn = {HERM_D: lib().oracle_sample_herm_d, HERM_Z: lib().oracle_sample_herm_z,
+          LU_Z: lib().oracle_sample_lu_z}[kind]
+    rc = fn(n, A.ctypes.data, max(n, 1), seed, b, fptr, tie_tol, range_tol,
+            mask.ctypes.data, ctypes.byref(ll), ctypes.byref(info))
+    if rc != 0:
+        raise RuntimeError(f"oracle returned {rc}")
+    return OracleResult(mask[:n].copy(), ll.value, A, info.n_kept, info.n_ties, info.first_tie,
+                        info.n_out_of_range, info.min_abs_pivot, info.max_abs_imag_pivot)
+
+
+def sample_herm_d(K, seed=0, b=0, forced=None, **kw):
+    return sample(HERM_D, K, seed, b, forced, **kw)
+
+
+def sample_herm_z(K, seed=0, b=0, forced=None, **kw):
+    return sample(HERM_Z, K, seed, b, forced, **kw)
+
+
+def sample_lu_z(K, seed=0, b=0, forced=None, **kw):
+    return sample(LU_Z, K, seed, b, forced, **kw)
+
+
+def sample_many(kind: int, K: np.ndarray, seed: int, b0: int, batch: int):
+    """Masks (batch x n, uint8) and logliks (batch) of samples b0..b0+batch-1."""
+    A = _as_colmajor(K, kind)
+    n = A.shape[0]
+    masks = np.zeros((batch, max(n, 1)), dtype=np.uint8)
+    lls = np.zeros(batch, dtype=np.float64)
+    rc = lib().oracle_sample_many(kind, n, A.ctypes.data, max(n, 1), seed, b0, batch,
+                                  masks.ctypes.data, lls.ctypes.data)
+    if rc != 0:
+        raise RuntimeError(f"oracle returned {rc}")
+    return masks[:, :n], lls

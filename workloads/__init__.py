@@ -1,0 +1,246 @@
+"""Seeded synthetic marginal kernels shaped like the paper's workloads.
+
+This module holds NONE of the sampler's arithmetic (no pivot decisions, no
+Schur updates, no Philox).  It only builds input kernels K and validates the
+combinatorial structure of samples.  Both the CPU oracle (``oracle/``) and the
+CUDA product path consume its outputs; neither is imported here.
+
+Recipes:
+  * ``haar_kernel``    K = Q diag(lam) Q^H, Q from QR of an i.i.d. Gaussian with
+                       the Haar sign fix Q <- Q sign(diag R); lam ~ U(0,1) or
+                       Beta(1/2,1/2); exactly symmetrised (BASELINE.json configs
+                       0, 3, 4; Macchi's criterion PAPER.md:202-204 makes it
+                       admissible).
+  * ``ust_kernel``     transfer-current kernel K = B^T (B B^T)^{-1} B of a grid
+                       graph with vertex 0 grounded (configs 1; PAPER.md:49-52,
+                       81-83, 1159-1161).
+  * ``aztec_kernel``   Kenyon's kernel M_ij = Kast(b_i,w_i) Kast^{-1}(w_i,b_j) of
+                       the Aztec diamond (config 2).
+  * ``similarity``     D^{-1} K D, a non-Hermitian kernel with the same DPP
+                       (Prop. 2).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = [
+    "haar_kernel", "haar_kernel_torch", "projection_kernel", "ust_kernel", "grid_edges",
+    "aztec_edges", "aztec_kernel", "similarity", "is_spanning_tree", "is_aztec_tiling",
+    "log_num_spanning_trees_grid",
+]
+
+
+# --------------------------------------------------------------------------- Haar
+def _haar_q(rng: np.random.Generator, n: int, complex_: bool) -> np.ndarray:
+    if complex_:
+        G = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(2.0)
+    else:
+        G = rng.standard_normal((n, n))
+    Q, R = np.linalg.qr(G)
+    d = np.diagonal(R)
+    ph = d / np.abs(d)
+    return Q * ph[None, :]
+
+
+def _spectrum(rng: np.random.Generator, n: int, spectrum: str) -> np.ndarray:
+    if spectrum == "uniform":
+        return rng.uniform(0.0, 1.0, n)
+    if spectrum == "beta":
+        return rng.beta(0.5, 0.5, n)
+    if spectrum.startswith("projection:"):
+        r = int(spectrum.split(":")[1])
+        lam = np.zeros(n)
+        lam[:r] = 1.0
+        return lam
+    raise ValueError(spectrum)
+
+
+def haar_kernel(n: int, seed: int = 0, spectrum: str = "uniform", complex_: bool = False) -> np.ndarray:
+    """K = Q diag(lam) Q^H (numpy, host).  G is drawn first, then lam."""
+    rng = np.random.default_rng(seed)
+    Q = _haar_q(rng, n, complex_)
+    lam = _spectrum(rng, n, spectrum)
+    K = (Q * lam[None, :]) @ Q.conj().T
+    K = 0.5 * (K + K.conj().T)
+    if complex_:
+        K[np.diag_indices(n)] = K.diagonal().real
+    return np.asfortranarray(K)
+
+
+def projection_kernel(n: int, rank: int, seed: int = 0, complex_: bool = False) -> np.ndarray:
+    return haar_kernel(n, seed, f"projection:{rank}", complex_)
+
+
+def haar_kernel_torch(n: int, seed: int = 0, spectrum: str = "uniform", complex_: bool = False,
+                      device: str = "cuda"):
+    """Same recipe on the GPU with torch (harness code for n >= 4096; untimed).
+
+    Returns a torch tensor holding K in column-major order (i.e. a C-contiguous
+    tensor T with T[l, i] = K[i, l]; K is symmetric/Hermitian so T = conj(K))."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    dt = torch.complex128 if complex_ else torch.float64
+    if complex_:
+        G = torch.complex(torch.randn(n, n, generator=g, device=device, dtype=torch.float64),
+                          torch.randn(n, n, generator=g, device=device, dtype=torch.float64)) / np.sqrt(2.0)
+    else:
+        G = torch.randn(n, n, generator=g, device=device, dtype=torch.float64)
+    Q, R = torch.linalg.qr(G)
+    del G
+    d = torch.diagonal(R)
+    Q = Q * (d / d.abs())[None, :]
+    del R
+    if spectrum == "uniform":
+        lam = torch.rand(n, generator=g, device=device, dtype=torch.float64)
+    elif spectrum == "beta":
+        # Beta(1/2, 1/2) by inverse CDF: x = sin^2(pi u / 2)
+        u = torch.rand(n, generator=g, device=device, dtype=torch.float64)
+        lam = torch.sin(0.5 * np.pi * u) ** 2
+    else:
+        raise ValueError(spectrum)
+    K = (Q * lam.to(dt)[None, :]) @ Q.conj().T
+    del Q
+    K = 0.5 * (K + K.conj().T)
+    if complex_:
+        K.diagonal().imag.zero_()
+    # column-major storage of K == row-major storage of K^T; for Hermitian K, K^T = conj(K)
+    return K.T.contiguous()
+
+
+# --------------------------------------------------------------------------- UST
+def grid_edges(rows: int, cols: int):
+    """Edges of a rows x cols grid graph; vertex id = y*cols + x.  Horizontal
+    edges in row-major order, then vertical edges (reading #14)."""
+    edges = []
+    for y in range(rows):
+        for x in range(cols - 1):
+            edges.append((y * cols + x, y * cols + x + 1))
+    for y in range(rows - 1):
+        for x in range(cols):
+            edges.append((y * cols + x, (y + 1) * cols + x))
+    return edges
+
+
+def ust_kernel(rows: int, cols: int) -> np.ndarray:
+    """Transfer-current kernel K = B^T (B B^T)^{-1} B, B = reduced incidence
+    matrix (vertex 0 grounded); +1 at the lower vertex id, -1 at the higher."""
+    import scipy.linalg as sla
+    edges = grid_edges(rows, cols)
+    V, E = rows * cols, len(edges)
+    B = np.zeros((V, E))
+    for e, (a, b) in enumerate(edges):
+        B[a, e] = 1.0
+        B[b, e] = -1.0
+    B = B[1:, :]
+    L = B @ B.T
+    c = sla.cho_factor(L, lower=True)
+    X = sla.cho_solve(c, B)
+    K = B.T @ X
+    K = 0.5 * (K + K.T)
+    return np.asfortranarray(K)
+
+
+def is_spanning_tree(V: int, edges, kept: np.ndarray) -> bool:
+    sel = [edges[e] for e in np.flatnonzero(kept)]
+    if len(sel) != V - 1:
+        return False
+    parent = list(range(V))
+
+    def find(a):
+        while parent[a] != a:
+            parent[a] = parent[parent[a]]
+            a = parent[a]
+        return a
+
+    for a, b in sel:
+        ra, rb = find(a), find(b)
+        if ra == rb:
+            return False
+        parent[ra] = rb
+    return True
+
+
+def log_num_spanning_trees_grid(rows: int, cols: int) -> float:
+    """ln tau(P_rows x P_cols) from the Laplacian eigenvalue product (Kirchhoff):
+    tau = (1/V) prod_{(j,k) != (0,0)} (4 - 2cos(pi j/rows) - 2cos(pi k/cols))."""
+    s = 0.0
+    for j in range(rows):
+        for k in range(cols):
+            if j == 0 and k == 0:
+                continue
+            s += np.log(4.0 - 2.0 * np.cos(np.pi * j / rows) - 2.0 * np.cos(np.pi * k / cols))
+    return s - np.log(rows * cols)
+
+
+# --------------------------------------------------------------------------- Aztec
+def aztec_squares(d: int):
+    """Unit squares (lower-left corner (x, y)) of the order-d Aztec diamond."""
+    sq = []
+    for x in range(-d, d):
+        for y in range(-d, d):
+            if abs(x + 0.5) + abs(y + 0.5) <= d:
+                sq.append((x, y))
+    return sq
+
+
+def aztec_edges(d: int):
+    """Ground set: adjacent (black, white) square pairs; black iff x+y even.
+    Black squares sorted by (x, y); neighbours in order E, W, N, S (reading #15).
+    Returns (edges, blacks, whites) with edges = [(bi, wi, vertical: bool)]."""
+    sq = aztec_squares(d)
+    sset = set(sq)
+    blacks = sorted([s for s in sq if (s[0] + s[1]) % 2 == 0])
+    whites = sorted([s for s in sq if (s[0] + s[1]) % 2 != 0])
+    widx = {w: i for i, w in enumerate(whites)}
+    edges = []
+    for bi, (x, y) in enumerate(blacks):
+        for dx, dy, vert in ((1, 0, False), (-1, 0, False), (0, 1, True), (0, -1, True)):
+            nb = (x + dx, y + dy)
+            if nb in sset:
+                edges.append((bi, widx[nb], vert))
+    return edges, blacks, whites
+
+
+def aztec_kernel(d: int) -> np.ndarray:
+    """Kenyon's kernel M_ij = Kast(b_i, w_i) Kast^{-1}(w_i, b_j) (plain gauge).
+
+    The plain gauge is fine in fp64 up to d ~ 20;
+    larger d needs the balanced gauge (not built in round 1)."""
+    edges, blacks, whites = aztec_edges(d)
+    nb = len(blacks)
+    Kast = np.zeros((nb, len(whites)), dtype=np.complex128)
+    for bi, wi, vert in edges:
+        Kast[bi, wi] = 1j if vert else 1.0
+    Kinv = np.linalg.inv(Kast)
+    n = len(edges)
+    bidx = np.array([e[0] for e in edges])
+    widx = np.array([e[1] for e in edges])
+    kv = np.array([1j if e[2] else 1.0 for e in edges])
+    M = kv[:, None] * Kinv[widx][:, bidx]
+    assert M.shape == (n, n)
+    return np.asfortranarray(M)
+
+
+def is_aztec_tiling(d: int, kept: np.ndarray) -> bool:
+    edges, blacks, whites = aztec_edges(d)
+    sel = np.flatnonzero(kept)
+    if len(sel) != d * (d + 1):
+        return False
+    bc = np.zeros(len(blacks), dtype=int)
+    wc = np.zeros(len(whites), dtype=int)
+    for e in sel:
+        bc[edges[e][0]] += 1
+        wc[edges[e][1]] += 1
+    return bool(np.all(bc == 1) and np.all(wc == 1))
+
+
+# --------------------------------------------------------------------------- Prop. 2
+def similarity(K: np.ndarray, seed: int = 0, lo: float = 0.5, hi: float = 2.0) -> np.ndarray:
+    """D^{-1} K D with a random complex diagonal D, |D| in [lo, hi] (Prop. 2)."""
+    rng = np.random.default_rng(seed + 7919)
+    n = K.shape[0]
+    mag = rng.uniform(lo, hi, n)
+    ph = np.exp(2j * np.pi * rng.uniform(0, 1, n))
+    D = mag * ph
+    return np.asfortranarray((1.0 / D)[:, None] * K.astype(np.complex128) * D[None, :])
