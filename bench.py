@@ -1,0 +1,333 @@
+"""Benchmark of the B200 DPP sampler (BASELINE.json metric) -- one JSON line on rank 0.
+
+Workload (config.workload): BASELINE.json configs[3] -- the dense real-symmetric fp64 kernel
+n = 16384, K = Q diag(lam) Q^T with Haar-like Q and lam ~ Beta(1/2, 1/2), sampled by the blocked
+modified LDL^T with nb = 128 and depth-1 lookahead.  This is the configuration the north_star
+target ("n=16384 fp64 Hermitian sampler ... >= 60% of B200 FP64 peak on the trailing update") is
+stated on; configs[0] (n = 256) is the small parity case the oracle finishes in seconds.
+
+A step = one complete sample (all SURVEY §8(a) stages) of the kernel resident in HBM, through
+the public C ABI (dpp_sample_herm_d_batched, batch 1: the call copies K into its workspace and
+factors the copy; sample index b differs every step).  value = model GFLOP/s (n^3/3 per sample,
+the paper's convention) of the whole job; the input (2.1 GB) is larger than L2.
+
+--gpus N (torchrun, one process per GPU): independent samples per rank (b = rank*(W+K) + i), no
+data-path collective ("scaling": "weak"); time = max over ranks.
+--impl reference: the CPU oracle (oracle/, plain C, unblocked Listing 1) on this host's cores,
+each step one bounded sample (the leading m x m block of the same kernel).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N = 16384
+NB = 128
+SEED = 0
+KSEED = 0
+METRIC = "DPP sampler FP64 GFLOP/s (n^3/3 LDL^H, 2n^3/3 LU), samples/s, % FP64 peak"
+UNIT = "GFLOP/s"
+# Measured FP64 DMMA.8x8x4 peak of this pool's B200 (tools/fp64_peak.cu, profiles/r01_fp64_peak.jsonl);
+# MEASURED_PEAKS.json has no FP64 entry.  For reference: bf16 measured 1647.4 x nominal ratio
+# (37.2 / 2250) = 27.2 TF/s would be a LOWER (more flattering) denominator; we use the measured 37.1.
+FP64_PEAK_TFLOPS = 37.1
+PEAK_SOURCE = "measured DMMA.8x8x4 loop, profiles/r01_fp64_peak.jsonl (MEASURED_PEAKS.json has no fp64 entry)"
+
+
+def model_flops(n: int) -> float:
+    return n ** 3 / 3.0
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.path = f"/tmp/dpp_clocks_{os.getpid()}.csv"
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.close()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        pw = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None, "samples": len(rows), "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------------------- oracle (CPU)
+def _oracle_worker(args):
+    import numpy as np
+    import oracle
+    Kpre, b = args
+    t0 = time.perf_counter()
+    oracle.sample_herm_d(Kpre, SEED, b)
+    return time.perf_counter() - t0
+
+
+def oracle_leg(Kpre, reps: int, cores: int):
+    """Times the oracle (as it stands) on `cores` host processes, each sampling Kpre once per rep."""
+    import multiprocessing as mp
+    import oracle
+    oracle.build()
+    m = Kpre.shape[0]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        t0 = time.perf_counter()
+        for r in range(reps):
+            pool.map(_oracle_worker, [(Kpre, r * cores + c) for c in range(cores)])
+        wall = time.perf_counter() - t0
+    flops = model_flops(m) * reps * cores
+    return flops / wall / 1e9, wall
+
+
+def pick_prefix(Kfull_prefix_fn, target_s: float, cores: int):
+    """Choose m so one oracle sample of the leading m x m block takes about target_s seconds."""
+    import oracle
+    oracle.build()
+    m0 = 768
+    K0 = Kfull_prefix_fn(m0)
+    t0 = time.perf_counter()
+    oracle.sample_herm_d(K0, SEED, 0)
+    dt = max(time.perf_counter() - t0, 1e-3)
+    m = int(m0 * (target_s / dt) ** (1.0 / 3.0))
+    return max(256, min(m - m % 16, 4096))
+
+
+# --------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n = args.n
+
+    import numpy as np
+    import torch
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        return reference_arm(args, n)
+
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    import paper_1905_00165_b200 as dpp
+    import workloads as W
+
+    Kc = W.haar_kernel_torch(n, seed=KSEED, spectrum="beta")  # column-major storage (symmetric)
+    torch.cuda.synchronize()
+    opts = dpp.make_opts(nb=NB, lookahead=1)
+    op = dpp.DPP_OP_HERM_D | dpp.DPP_OP_BATCHED
+    work = torch.empty(dpp.dpp_workspace_bytes(op, 1, n, opts), dtype=torch.uint8, device="cuda")
+    mask = torch.empty((1, n), dtype=torch.uint8, device="cuda")
+    ll = torch.empty(1, dtype=torch.float64, device="cuda")
+    info = torch.empty((1, 32), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    b_base = rank * (args.warmup + args.steps)
+
+    def step(i):
+        dpp.dpp_sample_herm_d_batched(1, n, Kc, n, 0, SEED, b_base + i, mask, ll, info, opts, work, stream=stream)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+
+    # ---- timed region: barrier + sync on both sides, CUDA events on the launching stream
+    clk = ClockSampler(local_rank)
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dpp.dpp_profile_begin()
+    e0.record(stream)
+    for i in range(args.steps):
+        step(args.warmup + i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    prof = dpp.dpp_profile_end()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    kept = int(mask.sum())
+    total_flops = model_flops(n) * args.steps * world
+    value = total_flops / (ms_max / 1e3) / 1e9
+    samples_per_s = args.steps * world / (ms_max / 1e3)
+    launches = sum(v["launches"] for v in prof.values())
+
+    # roofline of the dominant kernel: the trailing update (b), stage 3, on its own stream
+    up = prof["update_trailing"]
+    achieved_tf = up["flops"] / (up["ms"] / 1e3) / 1e12 if up["ms"] > 0 else 0.0
+    stage_share = {k: round(v["ms"] / max(ms, 1e-9), 4) for k, v in prof.items()}
+
+    # ---- end-to-end through the host-buffer C-ABI call (H2D of K + D2H of mask/loglik inside)
+    e2e = None
+    if not args.no_e2e:
+        Kh = Kc.cpu().pin_memory()
+        mh = torch.empty((1, n), dtype=torch.uint8).pin_memory()
+        lh = torch.empty(1, dtype=torch.float64).pin_memory()
+        ih = torch.empty((1, 32), dtype=torch.uint8).pin_memory()
+        opw = dpp.DPP_OP_HERM_D | dpp.DPP_OP_HOST
+        work_h = torch.empty(dpp.dpp_workspace_bytes(opw, 1, n, opts), dtype=torch.uint8, device="cuda")
+        del work
+        torch.cuda.empty_cache()
+
+        def hstep(i):
+            dpp.dpp_sample_herm_d_host(1, n, Kh, n, 0, SEED, b_base + i, mh, lh, ih, opts, work_h, stream=stream)
+        hstep(0)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        for i in range(args.steps):
+            hstep(args.warmup + i)
+        h1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(total_flops / (float(te.item()) / 1e3) / 1e9, 2), "unit": UNIT,
+               "h2d_bytes_per_step": int(Kh.numel() * Kh.element_size()),
+               "d2h_bytes_per_step": int(mh.numel() + lh.numel() * 8 + ih.numel()),
+               "samples_per_s": round(args.steps * world / (float(te.item()) / 1e3), 3)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = min(16, len(os.sched_getaffinity(0)))
+
+        def prefix(m):
+            return Kc[:m, :m].cpu().numpy().T.copy()
+        m = pick_prefix(prefix, 8.0, cores)
+        gf, wall = oracle_leg(prefix(m), 1, cores)
+        cpu = {"value": round(gf, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{cores} concurrent oracle samples (one per host core, b = 0..{cores - 1}) of the "
+                         f"leading {m}x{m} block of the same n={n} kernel (same flop convention m^3/3), "
+                         f"{wall:.1f} s wall"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"BASELINE configs[3]: dense real-symmetric fp64 K=Q diag(lam) Q^T, "
+                                   f"lam~Beta(1/2,1/2), n={n}, one sample per step per GPU",
+                       "n": n, "nb": NB, "lookahead": 1, "global_batch": world, "seq_len": None,
+                       "parallelism": f"dp{world} (independent samples)" if world > 1 else "single GPU",
+                       "l2": "inputs (K, 2.1 GB) larger than L2; no flush needed",
+                       "api": "dpp_sample_herm_d_batched(batch=1): K copied into the workspace each step"},
+            "samples_per_s": round(samples_per_s, 3),
+            "pct_fp64_peak": round(100.0 * value / 1e3 / (FP64_PEAK_TFLOPS * world), 2),
+            "kept_last_sample": kept,
+            "roofline": {"bound": "tensor", "kernel": "update_kernel<real,herm> (stage 3, trailing region)",
+                         "achieved": round(achieved_tf, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": round(achieved_tf / FP64_PEAK_TFLOPS, 4), "traffic": None,
+                         "peak_source": PEAK_SOURCE,
+                         "per_launch_flops": round(up["flops"] / max(up["launches"], 1)),
+                         "avg_launch_ms": round(up["ms"] / max(up["launches"], 1), 4)},
+            "stages": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                           "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3)} for k, v in prof.items()},
+            "stage_time_share": stage_share,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "impl": "ours",
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def reference_arm(args, n):
+    """The CPU oracle, as it stands, on this host's cores; same metric/unit/config."""
+    import torch
+    import workloads as W
+    cores = min(16, len(os.sched_getaffinity(0)))
+    if torch.cuda.is_available():
+        Kc = W.haar_kernel_torch(n, seed=KSEED, spectrum="beta")
+
+        def prefix(m):
+            return Kc[:m, :m].cpu().numpy().T.copy()
+        workload = f"leading m x m block of the config[3] kernel (n={n}, Beta(1/2,1/2), GPU-generated)"
+    else:
+        def prefix(m):
+            return W.haar_kernel(m, seed=KSEED, spectrum="beta")
+        workload = "numpy Haar kernel with the config[3] recipe (no GPU to generate the n=16384 kernel)"
+    # each step must be bounded so the whole --steps K --warmup W run ends within a few minutes
+    per_step_s = max(2.0, min(10.0, 150.0 / max(args.steps + args.warmup, 1)))
+    m = pick_prefix(prefix, per_step_s, cores)
+    Kpre = prefix(m)
+    for _ in range(args.warmup):
+        oracle_leg(Kpre, 1, cores)
+    t0 = time.perf_counter()
+    gf, wall = oracle_leg(Kpre, args.steps, cores)
+    ms = (time.perf_counter() - t0) * 1e3
+    line = {
+        "metric": METRIC, "value": round(gf, 3), "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"BASELINE configs[3] (n={n}) -- oracle sample: {workload}, m={m}",
+                   "n": n, "m_sample": m, "global_batch": cores, "seq_len": None, "parallelism": f"{cores} host processes"},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(gf, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"per step {cores} concurrent unblocked oracle samples of the leading {m}x{m} block"},
+        "e2e": {"value": round(gf, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

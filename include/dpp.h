@@ -1,0 +1,198 @@
+/*
+ * dpp.h -- C ABI of the B200-native factorization-based DPP sampler.
+ *
+ * Implements the method of arXiv 1905.00165 ("High-performance sampling of
+ * generic Determinantal Point Processes"): an exact sample of DPP(K) from its
+ * marginal kernel K by a randomly modified, unpivoted, right-looking
+ * factorization (Theorem "Factorization-based DPP sampling", PAPER.md:389-423;
+ * Listing 1), blocked as in Listing 3/4.
+ * At pivot j the item is kept with probability Re A(j,j) (u_j <= Re A(j,j));
+ * otherwise A(j,j) -= 1; then the usual Schur-complement update.  The result is
+ * the kept set (mask), its log-likelihood sum_j ln|final pivot_j|
+ * (PAPER.md:395-396), and, in place, the factor of K - 1_{Y^c}
+ * (Listing 1 caption).
+ *
+ * Conventions (every entry point):
+ *  - Matrices are column-major with leading dimension ld >= max(1, n).
+ *    Complex matrices are interleaved (re, im) pairs of doubles (dpp_complex_t).
+ *  - Unless the name ends in _host, ALL pointers (K, mask, loglik, info, work,
+ *    opts->forced) are DEVICE pointers and the call is stream-ordered and
+ *    asynchronous: results are valid once `stream` has been synchronised.
+ *    `stream` is a cudaStream_t (NULL = legacy default stream).
+ *  - The caller owns every buffer.  The library never allocates device memory
+ *    on the sampling path: it uses `work` (>= dpp_workspace_bytes(...) bytes,
+ *    256-byte aligned).
+ *  - Uniforms: u_j = Philox4x32-10 with key (lo32 seed, hi32 seed) and counter
+ *    (lo32 j, hi32 j, lo32 b, hi32 b), x = (r.y << 32) | r.x,
+ *    u = (2 (x >> 12) + 1) 2^-53 -- j is the GLOBAL pivot index, b the sample
+ *    index.  Results are therefore independent of nb, lookahead, chunking and
+ *    GPU count (reading R2).
+ *  - Hermitian entry points read and write the LOWER triangle only (strict
+ *    lower = L with implicit unit diagonal, diagonal = real D); the strict
+ *    upper triangle is never touched; Im of a diagonal entry is treated as 0.
+ *    The LU entry point overwrites all of K (strict lower = L, diag+upper = U).
+ *  - Return codes: 0 = OK; negative = error (dpp_strerror).  Numerical
+ *    anomalies are NOT errors: ties (|u_j - d_j| <= tie_tol), out-of-range
+ *    pivots (d_j outside [-range_tol, 1+range_tol]) and non-real LU pivots are
+ *    counted in dpp_info_t.  A zero pivot cannot occur: |final pivot| >=
+ *    min(u, 1-u) >= 2^-53 for any real pivot value (reading R7).
+ *    Asynchronous CUDA faults surface at the caller's synchronisation.
+ *  - n = 0 is valid: loglik = 0, info zeroed (first_tie = -1), mask untouched.
+ *  - Thread safety: calls are reentrant; calls from several host threads on
+ *    the same device are serialised internally while being enqueued.
+ */
+#ifndef DPP_B200_H_
+#define DPP_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DPP_OK 0
+#define DPP_EINVAL (-1)      /* bad size, ld, nb, batch or NULL required pointer */
+#define DPP_EWORKSPACE (-2)  /* work == NULL or work_bytes too small or misaligned */
+#define DPP_ECUDA (-3)       /* CUDA launch / configuration error */
+#define DPP_ENCCL (-4)       /* NCCL error (distributed entry points) */
+#define DPP_EUNSUPPORTED (-5)/* device is not sm_100 */
+
+typedef struct { double re, im; } dpp_complex_t;
+typedef struct CUstream_st* dpp_stream_t; /* == cudaStream_t */
+
+/* Options; pass NULL for the defaults. */
+typedef struct {
+  int32_t nb;            /* block size: 32, 64 or 128 (0 = default: 128 real, 64 complex) */
+  int32_t lookahead;     /* 0 = single stream, 1 = depth-1 lookahead on two streams (default) */
+  double tie_tol;        /* default 1e-9 */
+  double range_tol;      /* default 1e-8 */
+  const uint8_t* forced; /* DEVICE, nullable: forced decisions (replay / likelihood of a
+                            given set, SPEC log_likelihood_of); batch x n bytes, row b at
+                            forced + b*n; decision j is forced[j] != 0 */
+  int64_t batch_chunk;   /* batched: samples factored concurrently (0 = whole batch) */
+} dpp_opts_t;
+
+/* Per-sample diagnostics (DEVICE memory unless the call is _host). */
+typedef struct {
+  int32_t n_kept;             /* |Y| */
+  int32_t n_ties;             /* pivots with |u_j - Re p_j| <= tie_tol */
+  int32_t first_tie;          /* first such pivot, -1 if none */
+  int32_t n_out_of_range;     /* pivots with Re p_j outside [-range_tol, 1 + range_tol] */
+  double min_abs_pivot;       /* min_j |final pivot_j| (+inf if n = 0) */
+  double max_abs_imag_pivot;  /* LU only: max_j |Im p_j| before the decision */
+} dpp_info_t;
+
+/* Operation codes for dpp_workspace_bytes. */
+#define DPP_OP_HERM_D 0
+#define DPP_OP_HERM_Z 1
+#define DPP_OP_LU_Z 2
+#define DPP_OP_BATCHED 0x10 /* OR-ed: batched entry point (K copied into work) */
+#define DPP_OP_HOST 0x20    /* OR-ed: _host entry point (implies a K copy in work) */
+
+/* Bytes of device workspace needed by the call (op, batch, n, opts). */
+size_t dpp_workspace_bytes(int op, int64_t batch, int64_t n, const dpp_opts_t* opts);
+
+/* ---- single sample (sample index b = 0), K overwritten in place ----------
+ * n:      order of K (>= 0)
+ * K:      DEVICE, n x n column-major, ld >= max(1, n); OVERWRITTEN by the factor
+ * seed:   Philox key
+ * mask:   DEVICE uint8[n]; 1 = item kept
+ * loglik: DEVICE double[1]; sum_j ln|final pivot_j| in pivot order
+ * info:   DEVICE dpp_info_t[1] or NULL
+ * Cites: Listing 1 blocked per Listing 3/4;
+ * Hermitian specialisation PAPER.md:396-398, 626-628. */
+int dpp_sample_herm_d(int64_t n, double* K, int64_t ld, uint64_t seed, uint8_t* mask,
+                      double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
+                      size_t work_bytes, dpp_stream_t stream);
+int dpp_sample_herm_z(int64_t n, dpp_complex_t* K, int64_t ld, uint64_t seed, uint8_t* mask,
+                      double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
+                      size_t work_bytes, dpp_stream_t stream);
+int dpp_sample_lu_z(int64_t n, dpp_complex_t* K, int64_t ld, uint64_t seed, uint8_t* mask,
+                    double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
+                    size_t work_bytes, dpp_stream_t stream);
+
+/* ---- batched independent samples b = b0 .. b0+batch-1 ----------------------
+ * K is READ-ONLY: strideK == 0 -> one kernel shared by every sample; else
+ * sample s reads the kernel at K + s*strideK (elements).  Each sample is
+ * factored in its own copy inside `work`.  mask: batch x n (row s at mask +
+ * s*n); loglik: batch; info: batch or NULL. */
+int dpp_sample_herm_d_batched(int64_t batch, int64_t n, const double* K, int64_t ld,
+                              int64_t strideK, uint64_t seed, uint64_t b0, uint8_t* mask,
+                              double* loglik, dpp_info_t* info, const dpp_opts_t* opts,
+                              void* work, size_t work_bytes, dpp_stream_t stream);
+int dpp_sample_herm_z_batched(int64_t batch, int64_t n, const dpp_complex_t* K, int64_t ld,
+                              int64_t strideK, uint64_t seed, uint64_t b0, uint8_t* mask,
+                              double* loglik, dpp_info_t* info, const dpp_opts_t* opts,
+                              void* work, size_t work_bytes, dpp_stream_t stream);
+int dpp_sample_lu_z_batched(int64_t batch, int64_t n, const dpp_complex_t* K, int64_t ld,
+                            int64_t strideK, uint64_t seed, uint64_t b0, uint8_t* mask,
+                            double* loglik, dpp_info_t* info, const dpp_opts_t* opts,
+                            void* work, size_t work_bytes, dpp_stream_t stream);
+
+/* ---- host-buffer entry points (end-to-end: H2D copy, sample, D2H copy) ----
+ * Same as *_batched but K, mask, loglik and info are HOST pointers (pinned
+ * memory gives the fastest copies).  `work` is DEVICE memory of at least
+ * dpp_workspace_bytes(op | DPP_OP_HOST, batch, n, opts) bytes.  Synchronous:
+ * results are valid on return. */
+int dpp_sample_herm_d_host(int64_t batch, int64_t n, const double* K, int64_t ld,
+                           int64_t strideK, uint64_t seed, uint64_t b0, uint8_t* mask,
+                           double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
+                           size_t work_bytes, dpp_stream_t stream);
+int dpp_sample_herm_z_host(int64_t batch, int64_t n, const dpp_complex_t* K, int64_t ld,
+                           int64_t strideK, uint64_t seed, uint64_t b0, uint8_t* mask,
+                           double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
+                           size_t work_bytes, dpp_stream_t stream);
+int dpp_sample_lu_z_host(int64_t batch, int64_t n, const dpp_complex_t* K, int64_t ld,
+                         int64_t strideK, uint64_t seed, uint64_t b0, uint8_t* mask,
+                         double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
+                         size_t work_bytes, dpp_stream_t stream);
+
+/* ---- device Philox uniforms (the generator the sampler uses) ---------------
+ * u[i] = u(seed, j0 + i, b) for i < count, written to DEVICE u.  Exposed so the
+ * generator can be checked against curand and the oracle (reading R2). */
+int dpp_philox_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, double* u,
+                        dpp_stream_t stream);
+
+/* ---- distributed 1D block-column-cyclic factorization (one sample) ---------
+ * Rank r of P owns block columns c = r, r+P, r+2P, ... (block width nb), stored
+ * contiguously as an n x ncols_local column-major array K_local with leading
+ * dimension ld_local >= n (ncols_local = dpp_bcc_local_cols(n, nb, P, r)).
+ * Per block step the owner factors its diagonal tile and panel and broadcasts
+ * [panel | pivots | decisions | partial loglik] with NCCL; every rank then
+ * updates its local trailing columns.  On return every rank holds the full
+ * mask (n bytes) and loglik; K_local holds the local columns of the factor.
+ * comm wraps an ncclComm_t created from a 128-byte ncclUniqueId. */
+typedef struct dpp_comm_s* dpp_comm_t;
+int dpp_comm_init(const void* nccl_unique_id, int nranks, int rank, dpp_comm_t* comm);
+int dpp_comm_destroy(dpp_comm_t comm);
+int64_t dpp_bcc_local_cols(int64_t n, int32_t nb, int nranks, int rank);
+size_t dpp_dist_workspace_bytes(int op, int64_t n, int nranks, const dpp_opts_t* opts);
+int dpp_sample_herm_d_dist(dpp_comm_t comm, int64_t n, double* K_local, int64_t ld_local,
+                           uint64_t seed, uint8_t* mask, double* loglik, dpp_info_t* info,
+                           const dpp_opts_t* opts, void* work, size_t work_bytes,
+                           dpp_stream_t stream);
+
+/* ---- stage profiling (diagnostics; used by bench.py for the roofline) ------
+ * Between dpp_profile_begin() and dpp_profile_end() every stage launch made by
+ * this thread's calls on the current device is bracketed by CUDA events ON THE
+ * STREAM IT IS LAUNCHED ON.  dpp_profile_end() synchronises those events and
+ * returns, per stage (0 = diag tile, 1 = panel, 2 = lookahead update (a),
+ * 3 = trailing update (b)), the number of launches, the summed event time and
+ * the ALGORITHMIC flops (paper convention: real flops; a complex multiply-add
+ * counts 8, i.e. 4x the real count).  Not reentrant across host threads. */
+typedef struct {
+  int64_t launches[4];
+  double ms[4];
+  double flops[4];
+} dpp_profile_t;
+int dpp_profile_begin(void);
+int dpp_profile_end(dpp_profile_t* out);
+
+const char* dpp_strerror(int code);
+const char* dpp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DPP_B200_H_ */

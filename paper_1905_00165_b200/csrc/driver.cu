@@ -1,0 +1,430 @@
+// driver.cu -- host driver of the blocked sampler and the C ABI of include/dpp.h.
+//
+// Blocked, right-looking DPP sampling = Listing 3's loop with line 583
+// replaced by the unblocked sampler (Listing 4):
+//   for j0 in 0, nb, 2nb, ...:   stage 1 diag(j0) -> stage 2 panel(j0) -> stage 3 update(j0)
+// With lookahead (the GPU analogue of the paper's tile-dependency task
+// scheduling) the update of step k is split into
+//   (a) the next block column (and, for LU, the next block row), on the high-priority stream S1,
+//       immediately followed by diag(k+1) and panel(k+1), and
+//   (b) the rest of the trailing matrix, on stream S2,
+// so the sequential diag/panel chain of step k+1 runs under the big update of step k.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace dpp;
+
+namespace {
+
+constexpr size_t ALIGN = 256;
+inline size_t align_up(size_t x, size_t a = ALIGN) { return (x + a - 1) / a * a; }
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+struct Opts {
+  int nb;
+  int lookahead;
+  double tie_tol, range_tol;
+  const uint8_t* forced;
+  int64_t batch_chunk;
+};
+
+int resolve_opts(Kind kind, const dpp_opts_t* o, Opts* r) {
+  r->nb = (o && o->nb) ? o->nb : (kind == HERM_D ? 128 : 64);
+  r->lookahead = o ? o->lookahead : 1;
+  r->tie_tol = (o && o->tie_tol > 0) ? o->tie_tol : 1e-9;
+  r->range_tol = (o && o->range_tol > 0) ? o->range_tol : 1e-8;
+  r->forced = o ? o->forced : nullptr;
+  r->batch_chunk = o ? o->batch_chunk : 0;
+  if (r->nb != 32 && r->nb != 64 && r->nb != 128) return DPP_EINVAL;
+  if (kind != HERM_D && r->nb > 64) return DPP_EINVAL;  // complex tile must fit shared memory
+  if (r->lookahead < 0 || r->lookahead > 1) return DPP_EINVAL;
+  if (r->batch_chunk < 0) return DPP_EINVAL;
+  return DPP_OK;
+}
+
+size_t esize(Kind k) { return k == HERM_D ? 8 : 16; }
+
+// Workspace layout (all regions 256-byte aligned):
+//   [SampleState x chunk][W21 double buffer: 2 x chunk x ldw x nb (Hermitian)]
+//   [K copies: chunk x ldk x n (batched / host)][host staging: mask, loglik, info (host)]
+struct WsLayout {
+  size_t state_off, w_off, k_off, mask_off, ll_off, info_off, total;
+  int64_t ldw, ldk, strideW, strideK;
+};
+
+WsLayout layout(Kind kind, int64_t chunk, int64_t n, int nb, bool copies, bool host) {
+  WsLayout L{};
+  const size_t es = esize(kind);
+  L.ldw = std::max<int64_t>(round_up(n, 16), 16);
+  L.ldk = std::max<int64_t>(round_up(n, 16), 16);
+  L.strideW = L.ldw * std::max<int64_t>(std::min<int64_t>(nb, n), 1);  // W21 is at most min(nb, n) wide
+  L.strideK = L.ldk * std::max<int64_t>(n, 1);
+  size_t off = 0;
+  L.state_off = off; off = align_up(off + sizeof(SampleState) * (size_t)chunk);
+  L.w_off = off;
+  if (kind != LU_Z) off = align_up(off + 2 * (size_t)chunk * (size_t)L.strideW * es);
+  L.k_off = off;
+  if (copies) off = align_up(off + (size_t)chunk * (size_t)L.strideK * es);
+  L.mask_off = off;
+  if (host) off = align_up(off + (size_t)chunk * (size_t)std::max<int64_t>(n, 1));
+  L.ll_off = off;
+  if (host) off = align_up(off + 8 * (size_t)chunk);
+  L.info_off = off;
+  if (host) off = align_up(off + sizeof(dpp_info_t) * (size_t)chunk);
+  L.total = off;
+  return L;
+}
+
+// ---------------------------------------------------------------- stream pair per device
+struct DeviceStreams {
+  cudaStream_t s1 = nullptr, s2 = nullptr;
+  cudaEvent_t ev_start, ev_panel, ev_rest, ev_done1, ev_done2;
+  std::mutex mu;
+  bool init = false;
+};
+DeviceStreams g_streams[64];
+std::mutex g_streams_mu;
+
+int get_streams(DeviceStreams** out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return DPP_ECUDA;
+  DeviceStreams& d = g_streams[dev];
+  std::lock_guard<std::mutex> lk(g_streams_mu);
+  if (!d.init) {
+    int lo = 0, hi = 0;
+    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return DPP_ECUDA;
+    if (cudaStreamCreateWithPriority(&d.s1, cudaStreamNonBlocking, hi) != cudaSuccess) return DPP_ECUDA;
+    if (cudaStreamCreateWithPriority(&d.s2, cudaStreamNonBlocking, lo) != cudaSuccess) return DPP_ECUDA;
+    for (cudaEvent_t* e : {&d.ev_start, &d.ev_panel, &d.ev_rest, &d.ev_done1, &d.ev_done2})
+      if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return DPP_ECUDA;
+    d.init = true;
+  }
+  *out = &d;
+  return DPP_OK;
+}
+
+int check_device() {
+  int dev = 0, major = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return DPP_ECUDA;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return DPP_ECUDA;
+  return major == 10 ? DPP_OK : DPP_EUNSUPPORTED;
+}
+
+#define CK(x) do { if ((x) != cudaSuccess) return DPP_ECUDA; } while (0)
+
+// ---------------------------------------------------------------- stage profiling
+struct ProfRec { int stage; double flops; cudaEvent_t e0, e1; };
+struct Profiler {
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  cudaEvent_t get() {
+    if (used == pool.size()) { cudaEvent_t e; cudaEventCreate(&e); pool.push_back(e); }
+    return pool[used++];
+  }
+};
+thread_local Profiler g_prof;
+
+struct ProfScope {  // brackets one launch with events on its stream
+  int stage; double flops; cudaStream_t s; cudaEvent_t e1 = nullptr;
+  ProfScope(int st, double fl, cudaStream_t str) : stage(st), flops(fl), s(str) {
+    if (g_prof.on) {
+      cudaEvent_t e0 = g_prof.get();
+      e1 = g_prof.get();
+      cudaEventRecord(e0, s);
+      g_prof.recs.push_back({stage, flops, e0, e1});
+    }
+  }
+  ~ProfScope() { if (e1) cudaEventRecord(e1, s); }
+};
+
+double cplx_mult(Kind k) { return k == HERM_D ? 1.0 : 4.0; }
+// algorithmic flops of a Hermitian update region (lower elements only) or an LU rectangle
+double region_flops(Kind kind, int64_t row0, int64_t col0, int64_t rows, int64_t cols, int K) {
+  double elems;
+  if (kind == LU_Z) {
+    elems = (double)rows * (double)cols;
+  } else {
+    elems = 0;  // count (i, j) with i >= j, i in [row0, row0+rows), j in [col0, col0+cols)
+    for (int64_t j = col0; j < col0 + cols; ++j) {
+      const int64_t lo = std::max(j, row0), hi = row0 + rows;
+      if (hi > lo) elems += (double)(hi - lo);
+    }
+  }
+  return elems * 2.0 * K * cplx_mult(kind);
+}
+
+// ---------------------------------------------------------------- the blocked factorization
+// Factors `batch` matrices A + s*strideA (in place), samples b0 + s.
+int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_t strideA, int batch,
+                uint64_t seed, uint64_t b0, uint8_t* mask, const uint8_t* forced, double* loglik,
+                dpp_info_t* info, void* state, void* W, int64_t ldw, int64_t strideW, cudaStream_t caller) {
+  if (n == 0) { CK(launch_zero_state(state, loglik, info, batch, caller)); return DPP_OK; }
+  DeviceStreams* ds = nullptr;
+  int rc = get_streams(&ds);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(ds->mu);
+  const int nb = o.nb;
+  const bool la = o.lookahead > 0;
+  cudaStream_t s1 = la ? ds->s1 : caller, s2 = la ? ds->s2 : caller;
+  if (la) {
+    CK(cudaEventRecord(ds->ev_start, caller));
+    CK(cudaStreamWaitEvent(s1, ds->ev_start, 0));
+    CK(cudaStreamWaitEvent(s2, ds->ev_start, 0));
+  }
+  const size_t es = esize(kind);
+  char* Ab = reinterpret_cast<char*>(A);
+  const bool vec = kind != HERM_D ||
+                   ((ld % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (ldw % 2 == 0));
+  int step = 0;
+  bool have_rest = false;
+  for (int64_t j0 = 0; j0 < n; j0 += nb, ++step) {
+    const int jb = (int)std::min<int64_t>(nb, n - j0);
+    const int64_t j1 = j0 + jb, m2 = n - j1;
+    DiagArgs d{};
+    d.A = A; d.ld = ld; d.strideA = strideA; d.n = n; d.j0 = j0; d.tcol = j0; d.jb = jb; d.seed = seed; d.b0 = b0;
+    d.mask = mask; d.forced = forced; d.state = state; d.loglik = loglik; d.info = info;
+    d.tie_tol = o.tie_tol; d.range_tol = o.range_tol; d.batch = batch;
+    {
+      const double fl = (kind == LU_Z ? 2.0 : 1.0) * jb * (double)jb * jb / 3.0 * cplx_mult(kind) * batch;
+      ProfScope ps(0, fl, s1);
+      CK(launch_diag(kind, nb, d, s1));
+    }
+    if (m2 <= 0) break;
+    void* Wk = W ? reinterpret_cast<char*>(W) + (size_t)(step & 1) * (size_t)batch * (size_t)strideW * es : nullptr;
+    PanelArgs p{};
+    p.A = A; p.ld = ld; p.strideA = strideA; p.n = n; p.j0 = j0; p.tcol = j0; p.jb = jb; p.W = Wk; p.ldw = ldw;
+    p.strideW = strideW; p.batch = batch;
+    {
+      const double fl = (kind == LU_Z ? 2.0 : 1.0) * (double)m2 * jb * jb * cplx_mult(kind) * batch;
+      ProfScope ps(1, fl, s1);
+      CK(launch_panel(kind, nb, p, s1));
+    }
+
+    UpdateArgs u{};
+    u.Aop = Ab + (size_t)(j1 + j0 * ld) * es;  // L21
+    u.lda = ld; u.strideA = strideA;
+    if (kind == LU_Z) { u.Bop = Ab + (size_t)(j0 + j1 * ld) * es; u.ldb = ld; u.strideB = strideA; }  // U12
+    else { u.Bop = Wk; u.ldb = ldw; u.strideB = strideW; }
+    u.C = Ab + (size_t)(j1 + j1 * ld) * es; u.ldc = ld; u.strideC = strideA;
+    u.m_total = (int)m2; u.K = jb; u.batch = batch; u.vec = vec ? 1 : 0;
+    const int jn = (int)std::min<int64_t>(nb, m2);  // width of the next block
+    if (!la) {
+      u.row0 = 0; u.col0 = 0; u.rows = (int)m2; u.cols = (int)m2; u.tri = (kind != LU_Z);
+      ProfScope ps(3, region_flops(kind, 0, 0, m2, m2, jb) * batch, s1);
+      CK(launch_update(kind, u, s1));
+      continue;
+    }
+    CK(cudaEventRecord(ds->ev_panel, s1));
+    // (a) next block column [0, jn) x rows [0, m2)  (+ LU: next block row [0, jn) x cols [jn, m2))
+    if (have_rest) CK(cudaStreamWaitEvent(s1, ds->ev_rest, 0));
+    {
+      UpdateArgs ua = u;
+      ua.row0 = 0; ua.col0 = 0; ua.rows = (int)m2; ua.cols = jn; ua.tri = 0;
+      double fl = region_flops(kind, 0, 0, m2, jn, jb);
+      if (kind == LU_Z && m2 > jn) fl += region_flops(kind, 0, jn, jn, m2 - jn, jb);
+      ProfScope ps(2, fl * batch, s1);
+      CK(launch_update(kind, ua, s1));
+      if (kind == LU_Z && m2 > jn) {
+        UpdateArgs ur = u;
+        ur.row0 = 0; ur.col0 = jn; ur.rows = jn; ur.cols = (int)(m2 - jn); ur.tri = 0;
+        CK(launch_update(kind, ur, s1));
+      }
+    }
+    // (b) the rest [jn, m2)^2 on S2
+    if (m2 > jn) {
+      CK(cudaStreamWaitEvent(s2, ds->ev_panel, 0));
+      UpdateArgs ub = u;
+      ub.row0 = jn; ub.col0 = jn; ub.rows = (int)(m2 - jn); ub.cols = (int)(m2 - jn);
+      ub.tri = (kind != LU_Z);
+      {
+        ProfScope ps(3, region_flops(kind, jn, jn, m2 - jn, m2 - jn, jb) * batch, s2);
+        CK(launch_update(kind, ub, s2));
+      }
+      CK(cudaEventRecord(ds->ev_rest, s2));
+      have_rest = true;
+    }
+  }
+  if (la) {
+    CK(cudaEventRecord(ds->ev_done1, s1));
+    CK(cudaEventRecord(ds->ev_done2, s2));
+    CK(cudaStreamWaitEvent(caller, ds->ev_done1, 0));
+    CK(cudaStreamWaitEvent(caller, ds->ev_done2, 0));
+  }
+  return DPP_OK;
+}
+
+int validate(int64_t n, int64_t ld, const void* K, const uint8_t* mask, const double* loglik) {
+  if (n < 0 || ld < std::max<int64_t>(1, n)) return DPP_EINVAL;
+  if (n > (int64_t)1 << 30) return DPP_EINVAL;
+  if (n > 0 && (!K || !mask)) return DPP_EINVAL;
+  if (!loglik) return DPP_EINVAL;
+  return DPP_OK;
+}
+
+int sample_inplace(Kind kind, int64_t n, void* K, int64_t ld, uint64_t seed, uint8_t* mask, double* loglik,
+                   dpp_info_t* info, const dpp_opts_t* opts, void* work, size_t work_bytes, cudaStream_t st) {
+  Opts o;
+  int rc = resolve_opts(kind, opts, &o);
+  if (rc) return rc;
+  if ((rc = validate(n, ld, K, mask, loglik))) return rc;
+  if ((rc = check_device())) return rc;
+  WsLayout L = layout(kind, 1, n, o.nb, false, false);
+  if (!work || work_bytes < L.total || reinterpret_cast<uintptr_t>(work) % ALIGN) return DPP_EWORKSPACE;
+  if (kind != HERM_D && reinterpret_cast<uintptr_t>(K) % 16) return DPP_EINVAL;
+  char* w = reinterpret_cast<char*>(work);
+  return run_blocked(kind, o, n, K, ld, 0, 1, seed, 0, mask, o.forced, loglik, info, w + L.state_off,
+                     kind != LU_Z ? w + L.w_off : nullptr, L.ldw, L.strideW, st);
+}
+
+int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t ld, int64_t strideK, uint64_t seed,
+                   uint64_t b0, uint8_t* mask, double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
+                   size_t work_bytes, cudaStream_t st, bool host) {
+  Opts o;
+  int rc = resolve_opts(kind, opts, &o);
+  if (rc) return rc;
+  if (batch < 0 || strideK < 0) return DPP_EINVAL;
+  if (batch == 0) return DPP_OK;
+  if ((rc = validate(n, ld, K, mask, loglik))) return rc;
+  if (strideK > 0 && strideK < ld * std::max<int64_t>(n, 1)) return DPP_EINVAL;
+  if ((rc = check_device())) return rc;
+  const int64_t chunk = o.batch_chunk > 0 ? std::min(o.batch_chunk, batch) : batch;
+  if (chunk > 65535) return DPP_EINVAL;
+  WsLayout L = layout(kind, chunk, n, o.nb, true, host);
+  if (!work || work_bytes < L.total || reinterpret_cast<uintptr_t>(work) % ALIGN) return DPP_EWORKSPACE;
+  char* w = reinterpret_cast<char*>(work);
+  const size_t es = esize(kind);
+  const cudaMemcpyKind ck = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  char* Kc = w + L.k_off;
+  for (int64_t c0 = 0; c0 < batch; c0 += chunk) {
+    const int cb = (int)std::min<int64_t>(chunk, batch - c0);
+    if (n > 0) {
+      if (strideK == 0 && host) {
+        // one host->device transfer of the shared kernel, then device-side replication
+        CK(cudaMemcpy2DAsync(Kc, (size_t)L.ldk * es, K, (size_t)ld * es, (size_t)n * es, (size_t)n, ck, st));
+        for (int s = 1; s < cb; ++s)
+          CK(cudaMemcpyAsync(Kc + (size_t)s * L.strideK * es, Kc, (size_t)L.strideK * es, cudaMemcpyDeviceToDevice, st));
+      } else {
+        for (int s = 0; s < cb; ++s) {
+          const char* src = reinterpret_cast<const char*>(K) + (size_t)(strideK * (c0 + s)) * es;
+          CK(cudaMemcpy2DAsync(Kc + (size_t)s * L.strideK * es, (size_t)L.ldk * es, src, (size_t)ld * es,
+                               (size_t)n * es, (size_t)n, ck, st));
+        }
+      }
+    }
+    uint8_t* mk = host ? reinterpret_cast<uint8_t*>(w + L.mask_off) : mask + c0 * n;
+    double* llk = host ? reinterpret_cast<double*>(w + L.ll_off) : loglik + c0;
+    dpp_info_t* ifo = host ? (info ? reinterpret_cast<dpp_info_t*>(w + L.info_off) : nullptr) : (info ? info + c0 : nullptr);
+    const uint8_t* fz = o.forced ? o.forced + c0 * n : nullptr;
+    rc = run_blocked(kind, o, n, Kc, L.ldk, L.strideK, cb, seed, b0 + (uint64_t)c0, mk, fz, llk, ifo,
+                     w + L.state_off, kind != LU_Z ? w + L.w_off : nullptr, L.ldw, L.strideW, st);
+    if (rc) return rc;
+    if (host) {
+      if (n > 0) CK(cudaMemcpyAsync(mask + c0 * n, mk, (size_t)cb * n, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(loglik + c0, llk, 8 * (size_t)cb, cudaMemcpyDeviceToHost, st));
+      if (info) CK(cudaMemcpyAsync(info + c0, ifo, sizeof(dpp_info_t) * (size_t)cb, cudaMemcpyDeviceToHost, st));
+    }
+  }
+  if (host) CK(cudaStreamSynchronize(st));
+  return DPP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t dpp_workspace_bytes(int op, int64_t batch, int64_t n, const dpp_opts_t* opts) {
+  const Kind kind = (Kind)(op & 0x3);
+  if ((op & 0x3) == 3 || n < 0 || batch < 0) return 0;
+  Opts o;
+  if (resolve_opts(kind, opts, &o)) return 0;
+  const bool batched = (op & (DPP_OP_BATCHED | DPP_OP_HOST)) != 0;
+  const bool host = (op & DPP_OP_HOST) != 0;
+  int64_t chunk = batched ? batch : 1;
+  if (batched && o.batch_chunk > 0) chunk = std::min(chunk, o.batch_chunk);
+  chunk = std::max<int64_t>(chunk, 1);
+  return layout(kind, chunk, n, o.nb, batched, host).total;
+}
+
+int dpp_sample_herm_d(int64_t n, double* K, int64_t ld, uint64_t seed, uint8_t* mask, double* loglik,
+                      dpp_info_t* info, const dpp_opts_t* opts, void* work, size_t work_bytes, dpp_stream_t stream) {
+  return sample_inplace(HERM_D, n, K, ld, seed, mask, loglik, info, opts, work, work_bytes, (cudaStream_t)stream);
+}
+int dpp_sample_herm_z(int64_t n, dpp_complex_t* K, int64_t ld, uint64_t seed, uint8_t* mask, double* loglik,
+                      dpp_info_t* info, const dpp_opts_t* opts, void* work, size_t work_bytes, dpp_stream_t stream) {
+  return sample_inplace(HERM_Z, n, K, ld, seed, mask, loglik, info, opts, work, work_bytes, (cudaStream_t)stream);
+}
+int dpp_sample_lu_z(int64_t n, dpp_complex_t* K, int64_t ld, uint64_t seed, uint8_t* mask, double* loglik,
+                    dpp_info_t* info, const dpp_opts_t* opts, void* work, size_t work_bytes, dpp_stream_t stream) {
+  return sample_inplace(LU_Z, n, K, ld, seed, mask, loglik, info, opts, work, work_bytes, (cudaStream_t)stream);
+}
+
+#define BATCHED(name, kind, T, host)                                                                          \
+  int name(int64_t batch, int64_t n, const T* K, int64_t ld, int64_t strideK, uint64_t seed, uint64_t b0,     \
+           uint8_t* mask, double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,                 \
+           size_t work_bytes, dpp_stream_t stream) {                                                           \
+    return sample_batched(kind, batch, n, K, ld, strideK, seed, b0, mask, loglik, info, opts, work, work_bytes, \
+                          (cudaStream_t)stream, host);                                                         \
+  }
+BATCHED(dpp_sample_herm_d_batched, HERM_D, double, false)
+BATCHED(dpp_sample_herm_z_batched, HERM_Z, dpp_complex_t, false)
+BATCHED(dpp_sample_lu_z_batched, LU_Z, dpp_complex_t, false)
+BATCHED(dpp_sample_herm_d_host, HERM_D, double, true)
+BATCHED(dpp_sample_herm_z_host, HERM_Z, dpp_complex_t, true)
+BATCHED(dpp_sample_lu_z_host, LU_Z, dpp_complex_t, true)
+#undef BATCHED
+
+int dpp_philox_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, double* u, dpp_stream_t stream) {
+  if (count < 0 || (count > 0 && !u)) return DPP_EINVAL;
+  return launch_uniforms(seed, j0, b, count, u, (cudaStream_t)stream) == cudaSuccess ? DPP_OK : DPP_ECUDA;
+}
+
+int dpp_profile_begin(void) {
+  for (auto& r : g_prof.recs) (void)r;
+  g_prof.recs.clear();
+  g_prof.used = 0;
+  g_prof.on = true;
+  return DPP_OK;
+}
+
+int dpp_profile_end(dpp_profile_t* out) {
+  g_prof.on = false;
+  if (!out) return DPP_EINVAL;
+  std::memset(out, 0, sizeof(*out));
+  for (auto& r : g_prof.recs) {
+    if (cudaEventSynchronize(r.e1) != cudaSuccess) return DPP_ECUDA;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.e0, r.e1) != cudaSuccess) return DPP_ECUDA;
+    out->launches[r.stage] += 1;
+    out->ms[r.stage] += ms;
+    out->flops[r.stage] += r.flops;
+  }
+  g_prof.recs.clear();
+  g_prof.used = 0;
+  return DPP_OK;
+}
+
+const char* dpp_strerror(int code) {
+  switch (code) {
+    case DPP_OK: return "ok";
+    case DPP_EINVAL: return "invalid argument";
+    case DPP_EWORKSPACE: return "workspace missing, too small or misaligned";
+    case DPP_ECUDA: return "CUDA error";
+    case DPP_ENCCL: return "NCCL error";
+    case DPP_EUNSUPPORTED: return "unsupported device (needs sm_100)";
+  }
+  return "unknown error";
+}
+
+const char* dpp_version(void) { return "dpp-b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"
