@@ -8,10 +8,16 @@
 // Prop. 5 ("the subtraction of 1 from each eliminated pivot commutes with the
 // outer product updates") makes taking these decisions tile-locally exact.
 //
-// Design (B200): one CTA per (tile, sample); the whole jb x jb tile lives in shared memory
-// (real nb=128: 128 KB); 8 warps; warps own trailing columns round-robin, lanes own rows.
-// One __syncthreads per pivot: the scaled column k (and pivot) are written back at the start
-// of step k+1 (nobody reads column k during step k+1), so the pivot step needs no second barrier.
+// Design (B200, latency-bound: jb dependent pivot steps):
+//  * one CTA of 256 threads per (tile, sample); the tile lives in REGISTERS, distributed 2-D
+//    cyclically over a 16 x 16 thread grid (thread (tr, tc) owns rows tr + 16a, cols tc + 16b);
+//  * per pivot only the pivot column (and, for LU, the pivot row) goes through shared memory,
+//    double-buffered, so each pivot step costs exactly one __syncthreads;
+//  * the rank-1 update skips, warp-uniformly, the 16-row/16-column blocks already eliminated
+//    (and, Hermitian, the blocks strictly above the diagonal);
+//  * column k keeps its unscaled values after step k; the scaling L = w * (1/p) and the final
+//    pivots are applied once at the end (reading R17), and the log-likelihood / tie / range
+//    bookkeeping is done in parallel after the loop and summed by one thread IN PIVOT ORDER.
 // The Hermitian path reads/writes the lower triangle only.
 #include <cuda_runtime.h>
 
@@ -21,105 +27,148 @@
 
 namespace dpp {
 
-template <typename T, bool HERM, int NB, int NT>
-__global__ void __launch_bounds__(NT) diag_kernel(const DiagArgs a) {
-  constexpr int NW = NT / 32;
-  constexpr int RC = (NB + 31) / 32;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* S = reinterpret_cast<T*>(smem_raw);               // S(i,l) at l*NB + i
-  double* U = reinterpret_cast<double*>(S + NB * NB);  // uniforms of the tile's pivots
-  uint8_t* keepv = reinterpret_cast<uint8_t*>(U + NB);
+template <typename T, bool HERM, int NB>
+__global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
+  constexpr int TR = 16, TC = 16, RA = NB / TR, CB = NB / TC;
+  __shared__ T colbuf[2][NB];
+  __shared__ T rowbuf[HERM ? 1 : 2][HERM ? 1 : NB];
+  __shared__ T pv[NB], rv[NB];
+  __shared__ double U[NB], dv[NB], imv[NB], lg[NB];
+  __shared__ uint8_t keepv[NB];
 
   const int s = blockIdx.y;
   const int jb = a.jb;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
+  const int tr = tid % TR, tc = tid / TR;
   T* A = reinterpret_cast<T*>(a.A) + (int64_t)s * a.strideA + a.j0 + a.tcol * a.ld;
   SampleState* st = reinterpret_cast<SampleState*>(a.state) + s;
   const uint64_t b = a.b0 + (uint64_t)s;
 
-  // ---- stage the tile (Hermitian: lower triangle only) and this tile's uniforms
-  for (int l = warp; l < jb; l += NW)
-    for (int i = lane; i < jb; i += 32)
-      if (!HERM || i >= l) S[l * NB + i] = A[(int64_t)l * a.ld + i];
-  for (int k = tid; k < jb; k += NT) {
+  // ---- stage: registers (Hermitian: lower triangle only), uniforms, forced decisions
+  T R[RA][CB];
+#pragma unroll
+  for (int ia = 0; ia < RA; ++ia)
+#pragma unroll
+    for (int ib = 0; ib < CB; ++ib) {
+      const int i = tr + TR * ia, l = tc + TC * ib;
+      R[ia][ib] = (i < jb && l < jb && (!HERM || i >= l)) ? A[(int64_t)l * a.ld + i] : zero<T>();
+    }
+  for (int k = tid; k < jb; k += 256) {
     U[k] = uniform_u(a.seed, (uint64_t)(a.j0 + k), b);
     if (a.forced) keepv[k] = a.forced[(int64_t)s * a.n + a.j0 + k] != 0;
   }
-
-  // thread 0 carries the running per-sample state in pivot order
-  double ll = 0.0, minabs = INFINITY, maximag = 0.0;
-  int nkept = 0, nties = 0, firsttie = -1, noor = 0;
-  if (tid == 0 && a.j0 > 0) {
-    ll = st->loglik; minabs = st->min_abs_pivot; maximag = st->max_abs_imag_pivot;
-    nkept = st->n_kept; nties = st->n_ties; firsttie = st->first_tie; noor = st->n_out_of_range;
+  // publish pivot column 0 (and row 0)
+  if (tc == 0) {
+#pragma unroll
+    for (int ia = 0; ia < RA; ++ia) colbuf[0][tr + TR * ia] = R[ia][0];
+  }
+  if (!HERM && tr == 0) {
+#pragma unroll
+    for (int ib = 0; ib < CB; ++ib) rowbuf[0][tc + TC * ib] = R[0][ib];
   }
   __syncthreads();
-
-  T Lprev[RC];
-  T pprev = zero<T>();
-#pragma unroll
-  for (int c = 0; c < RC; ++c) Lprev[c] = zero<T>();
 
   for (int k = 0; k < jb; ++k) {
-    // deferred write-back of step k-1: scaled column k-1 and its final pivot
-    if (k > 0 && warp == (k - 1) % NW) {
-#pragma unroll
-      for (int c = 0; c < RC; ++c) {
-        const int i = lane + 32 * c;
-        if (i > k - 1 && i < jb) S[(k - 1) * NB + i] = Lprev[c];
-      }
-      if (lane == 0) S[(k - 1) * NB + (k - 1)] = pprev;
-    }
-    T p = S[k * NB + k];
+    const int cur = k & 1, nxt = cur ^ 1;
+    T p = colbuf[cur][k];
     if (HERM) p = make_real(re(p), p);
     const double d = re(p);
-    const double u = U[k];
-    const bool keep = a.forced ? (keepv[k] != 0) : (u <= d);
-    if (!keep) p = sub_one(p);  // Listing 1: A_j -= 1
+    const bool keep = a.forced ? (keepv[k] != 0) : (U[k] <= d);
+    if (!keep) p = sub_one(p);  // Listing 1
+    const T r = recip(p);
     if (tid == 0) {
-      if (fabs(u - d) <= a.tie_tol) { if (nties == 0) firsttie = (int)(a.j0 + k); ++nties; }
-      if (d < -a.range_tol || d > 1.0 + a.range_tol) ++noor;
-      if (!HERM) maximag = fmax(maximag, fabs(im(S[k * NB + k])));
-      const double ap = absval(p);
-      ll += log(ap);
-      minabs = fmin(minabs, ap);
-      nkept += keep ? 1 : 0;
+      pv[k] = p; rv[k] = r; dv[k] = d; imv[k] = im(colbuf[cur][k]);
       if (!a.forced) keepv[k] = keep ? 1 : 0;
     }
-    const T r = recip(p);
-    // line 438: L(i,k) = A(i,k) / p for this lane's rows
-    T Lk[RC];
+    // multipliers: L(i,k) = w_i / p (line 438) for my rows, conj(w_l) or U(k,l) for my columns
+    T Li[RA], Wl[CB];
 #pragma unroll
-    for (int c = 0; c < RC; ++c) {
-      const int i = lane + 32 * c;
-      Lk[c] = (i > k && i < jb) ? mul(S[k * NB + i], r) : zero<T>();
+    for (int ia = 0; ia < RA; ++ia) {
+      const int i = tr + TR * ia;
+      Li[ia] = (i > k && i < jb) ? mul(colbuf[cur][i], r) : zero<T>();
     }
-    // line 439: rank-1 update of the trailing part of the tile
-    for (int l = k + 1 + warp; l < jb; l += NW) {
-      const T bl = HERM ? cj(S[k * NB + l]) : S[l * NB + k];  // conj(w_l) or U(k,l)
-      T* col = S + l * NB;
 #pragma unroll
-      for (int c = 0; c < RC; ++c) {
-        const int i = lane + 32 * c;
-        if ((HERM ? (i >= l) : (i > k)) && i < jb) col[i] = fms(col[i], Lk[c], bl);
+    for (int ib = 0; ib < CB; ++ib) {
+      const int l = tc + TC * ib;
+      Wl[ib] = (l > k && l < jb) ? (HERM ? cj(colbuf[cur][l]) : rowbuf[HERM ? 0 : cur][l]) : zero<T>();
+    }
+    // rank-1 update (line 439) on the live blocks
+#pragma unroll
+    for (int ia = 0; ia < RA; ++ia) {
+      if (TR * ia + TR - 1 <= k) continue;  // warp-uniform: all rows of block ia eliminated
+#pragma unroll
+      for (int ib = 0; ib < CB; ++ib) {
+        if (HERM && ib > ia) continue;       // strictly above the diagonal
+        if (TC * ib + TC - 1 <= k) continue;
+        R[ia][ib] = fms(R[ia][ib], Li[ia], Wl[ib]);
       }
     }
+    // publish pivot column k+1 (and row k+1) for the next step
+    // (the owning register is selected with compile-time indices only: a runtime index into R
+    //  would demote the tile to local memory)
+    const int kn = k + 1;
+    if (kn < jb) {
 #pragma unroll
-    for (int c = 0; c < RC; ++c) Lprev[c] = Lk[c];
-    pprev = p;
+      for (int ib = 0; ib < CB; ++ib) {
+        if (tc + TC * ib == kn) {
+#pragma unroll
+          for (int ia = 0; ia < RA; ++ia) {
+            const int i = tr + TR * ia;
+            if (i >= kn) colbuf[nxt][i] = R[ia][ib];
+          }
+        }
+      }
+      if (!HERM) {
+#pragma unroll
+        for (int ia = 0; ia < RA; ++ia) {
+          if (tr + TR * ia == kn) {
+#pragma unroll
+            for (int ib = 0; ib < CB; ++ib) {
+              const int l = tc + TC * ib;
+              if (l > kn) rowbuf[HERM ? 0 : nxt][l] = R[ia][ib];
+            }
+          }
+        }
+      }
+    }
     __syncthreads();
   }
-  if (jb > 0 && warp == (jb - 1) % NW) {
-    if (lane == 0) S[(jb - 1) * NB + (jb - 1)] = pprev;
+
+  // ---- finalize the factor: L = (unscaled column) * (1/p), diagonal = final pivot
+#pragma unroll
+  for (int ia = 0; ia < RA; ++ia)
+#pragma unroll
+    for (int ib = 0; ib < CB; ++ib) {
+      const int i = tr + TR * ia, l = tc + TC * ib;
+      if (i < jb && l < jb && (!HERM || i >= l)) {
+        T v = R[ia][ib];
+        if (i > l) v = mul(v, rv[l]);
+        else if (i == l) v = pv[l];
+        A[(int64_t)l * a.ld + i] = v;
+      }
+    }
+  // ---- decisions, likelihood terms and diagnostics, in parallel; summed in pivot order
+  for (int k = tid; k < jb; k += 256) {
+    a.mask[(int64_t)s * a.n + a.j0 + k] = keepv[k];
+    lg[k] = log(absval(pv[k]));
   }
   __syncthreads();
-
-  // ---- write the factored tile, decisions and state back
-  for (int l = warp; l < jb; l += NW)
-    for (int i = lane; i < jb; i += 32)
-      if (!HERM || i >= l) A[(int64_t)l * a.ld + i] = S[l * NB + i];
-  for (int k = tid; k < jb; k += NT) a.mask[(int64_t)s * a.n + a.j0 + k] = keepv[k];
   if (tid == 0) {
+    double ll = 0.0, minabs = INFINITY, maximag = 0.0;
+    int nkept = 0, nties = 0, firsttie = -1, noor = 0;
+    if (a.j0 > 0) {
+      ll = st->loglik; minabs = st->min_abs_pivot; maximag = st->max_abs_imag_pivot;
+      nkept = st->n_kept; nties = st->n_ties; firsttie = st->first_tie; noor = st->n_out_of_range;
+    }
+    for (int k = 0; k < jb; ++k) {
+      const double d = dv[k], u = U[k];
+      if (fabs(u - d) <= a.tie_tol) { if (nties == 0) firsttie = (int)(a.j0 + k); ++nties; }
+      if (d < -a.range_tol || d > 1.0 + a.range_tol) ++noor;
+      if (!HERM) maximag = fmax(maximag, fabs(imv[k]));
+      ll += lg[k];
+      minabs = fmin(minabs, absval(pv[k]));
+      nkept += keepv[k];
+    }
     st->loglik = ll; st->min_abs_pivot = minabs; st->max_abs_imag_pivot = maximag;
     st->n_kept = nkept; st->n_ties = nties; st->first_tie = firsttie; st->n_out_of_range = noor;
     if (a.j0 + jb == a.n && a.loglik) {
@@ -135,18 +184,13 @@ __global__ void __launch_bounds__(NT) diag_kernel(const DiagArgs a) {
 
 template <typename T, bool HERM, int NB>
 static cudaError_t launch_diag_t(const DiagArgs& a, cudaStream_t s) {
-  constexpr int NT = 256;
-  const size_t smem = (size_t)NB * NB * sizeof(T) + NB * sizeof(double) + NB;
-  auto* fn = diag_kernel<T, HERM, NB, NT>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
   dim3 grid(1, a.batch);
-  fn<<<grid, NT, smem, s>>>(a);
+  diag_kernel<T, HERM, NB><<<grid, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 size_t diag_smem_bytes(Kind kind, int nb) {
-  return (size_t)nb * nb * (kind == HERM_D ? 8 : 16) + nb * 9;
+  return (size_t)nb * (kind == HERM_D ? 8 : 16) * 6 + nb * 33;
 }
 
 cudaError_t launch_diag(Kind kind, int nb, const DiagArgs& a, cudaStream_t s) {

@@ -22,9 +22,9 @@
 namespace dpp {
 
 template <bool CPLX> struct Cfg;
-// real: CTA 128x128, 8 warps as 2(M) x 4(N), warp tile 64x32, K chunk 16, 4 stages
+// real: CTA 128x128, 8 warps as 2(M) x 4(N), warp tile 64x32, K chunk 8, 4 stages
 template <> struct Cfg<false> {
-  static constexpr int BM = 128, BN = 128, WM = 2, WN = 4, KC = 16, STAGES = 4;
+  static constexpr int BM = 128, BN = 128, WM = 2, WN = 4, KC = 8, STAGES = 4;
 };
 // complex: CTA 64x64, 8 warps as 2 x 4, warp tile 32x16, K chunk 8, 4 stages
 template <> struct Cfg<true> {
@@ -44,7 +44,13 @@ struct Layout {
   static constexpr int A_ELEMS = C::KC * LDA;
   static constexpr int B_ELEMS = BLU ? C::BN * LDBN : C::KC * LDBK;
   static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
-  static constexpr size_t SMEM = (size_t)STAGE_ELEMS * C::STAGES * ES;
+  static constexpr size_t RING = (size_t)STAGE_ELEMS * C::STAGES * ES;
+  // C tile staged in shared memory, column j at j*LDC: LDC = 130 (real) / 65 (complex) keeps
+  // the accumulator-fragment access pattern (8 rows x 4 column pairs per warp) conflict-free
+  // and every column 16-byte aligned for the bulk (TMA) copies.
+  static constexpr int LDC = CPLX ? C::BM + 1 : C::BM + 2;
+  static constexpr size_t CTILE = (size_t)C::BN * LDC * ES;
+  static constexpr size_t SMEM = RING + CTILE;
 };
 
 template <bool CPLX> struct Elem { using T = double; };
@@ -148,18 +154,23 @@ update_kernel(const UpdateArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp % C::WM, wn = warp / C::WM;
 
-  // ---- prefetch this CTA's C tile into L2 (one bulk prefetch per column segment)
-  {
-    const int nrows = min(C::BM, a.m_total - grow0);
-    for (int c = tid; c < C::BN; c += NT) {
-      const int gc = gcol0 + c;
-      if (gc < col_end) {
-        const T* p = Cg + grow0 + (gc - cshift) * a.ldc;
-        const uintptr_t lo = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
-        const uintptr_t hi = (reinterpret_cast<uintptr_t>(p + nrows) + 15) & ~uintptr_t(15);
-        prefetch_l2_bulk(reinterpret_cast<const void*>(lo), (unsigned)(hi - lo));
-      }
-    }
+  // ---- C tile -> shared memory with TMA bulk copies, issued now, awaited in the epilogue
+  __shared__ __align__(8) uint64_t cbar;
+  T* Cs = reinterpret_cast<T*>(smem_raw + LY::RING);
+  const int nrows = min(C::BM, row_end - grow0);         // rows of this tile inside the region
+  const int ncols = min(C::BN, col_end - gcol0);
+  const bool diag_tile = !BLU && (gcol0 + ncols - 1 > grow0);  // some element above the diagonal
+  const bool bulk = VEC && ((nrows * (int)sizeof(T)) % 16 == 0);
+  if (tid == 0) {
+    mbar_init(&cbar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (bulk && warp == 0) {
+    if (lane == 0) mbar_arrive_expect_tx(&cbar, (uint32_t)(ncols * nrows * (int)sizeof(T)));
+    __syncwarp();
+    for (int c = lane; c < ncols; c += 32)
+      bulk_g2s(Cs + c * LY::LDC, Cg + grow0 + (gcol0 + c - cshift) * a.ldc, (uint32_t)(nrows * sizeof(T)), &cbar);
   }
 
   // ---- accumulators
@@ -235,18 +246,27 @@ update_kernel(const UpdateArgs a) {
   }
   cp_async_wait<0>();
 
-  // ---- epilogue: C -= acc  (Hermitian: only on/below the global diagonal)
+  // ---- epilogue: C -= acc in shared memory, then write the tile back
+  if (bulk) {
+    mbar_wait(&cbar, 0);
+  } else {
+    // unaligned / odd-row tiles: cooperative loads (the slow path; ragged tails only)
+    for (int idx = tid; idx < ncols * nrows; idx += NT) {
+      const int c = idx / nrows, r = idx % nrows;
+      Cs[c * LY::LDC + r] = Cg[grow0 + r + (gcol0 + c - cshift) * a.ldc];
+    }
+    __syncthreads();
+  }
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
-    const int gr = grow0 + wm * TM + i * 8 + (lane >> 2);
+    const int r = wm * TM + i * 8 + (lane >> 2);
 #pragma unroll
     for (int j = 0; j < NI; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int gc = gcol0 + wn * TN + j * 8 + 2 * (lane & 3) + e;
-        const bool ok = gr < row_end && gc < col_end && (BLU || gr >= gc);
-        if (ok) {
-          T* p = Cg + gr + (gc - cshift) * a.ldc;
+        const int c = wn * TN + j * 8 + 2 * (lane & 3) + e;
+        if (r < nrows && c < ncols && (BLU || grow0 + r >= gcol0 + c)) {
+          T* p = Cs + c * LY::LDC + r;
           if constexpr (!CPLX) {
             *p = *p - acc[i][j][e];
           } else {
@@ -257,6 +277,23 @@ update_kernel(const UpdateArgs a) {
           }
         }
       }
+    }
+  }
+  if (bulk && !diag_tile) {
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (warp == 0) {
+      for (int c = lane; c < ncols; c += 32)
+        bulk_s2g(Cg + grow0 + (gcol0 + c - cshift) * a.ldc, Cs + c * LY::LDC, (uint32_t)(nrows * sizeof(T)));
+      bulk_commit();
+      bulk_wait_read0();
+    }
+  } else {
+    __syncthreads();
+    // element stores; Hermitian diagonal tiles never write the strict upper triangle
+    for (int idx = tid; idx < ncols * nrows; idx += NT) {
+      const int c = idx / nrows, r = idx % nrows;
+      if (BLU || grow0 + r >= gcol0 + c) Cg[grow0 + r + (gcol0 + c - cshift) * a.ldc] = Cs[c * LY::LDC + r];
     }
   }
 }
