@@ -13,8 +13,8 @@
 //    cyclically over a 16 x 16 thread grid (thread (tr, tc) owns rows tr + 16a, cols tc + 16b);
 //  * per pivot only the pivot column (and, for LU, the pivot row) goes through shared memory,
 //    double-buffered, so each pivot step costs exactly one __syncthreads;
-//  * the rank-1 update skips, warp-uniformly, the 16-row/16-column blocks already eliminated
-//    (and, Hermitian, the blocks strictly above the diagonal);
+//  * the rank-1 update is branch-free (eliminated rows/columns carry zero multipliers; Hermitian
+//    blocks strictly above the diagonal are skipped at compile time);
 //  * column k keeps its unscaled values after step k; the scaling L = w * (1/p) and the final
 //    pivots are applied once at the end (reading R17), and the log-likelihood / tie / range
 //    bookkeeping is done in parallel after the loop and summed by one thread IN PIVOT ORDER.
@@ -92,17 +92,13 @@ __global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
       const int l = tc + TC * ib;
       Wl[ib] = (l > k && l < jb) ? (HERM ? cj(colbuf[cur][l]) : rowbuf[HERM ? 0 : cur][l]) : zero<T>();
     }
-    // rank-1 update (line 439) on the live blocks
+    // rank-1 update (line 439); eliminated rows/columns have zero multipliers, so the update is
+    // branch-free (Hermitian: blocks strictly above the diagonal are skipped statically)
 #pragma unroll
-    for (int ia = 0; ia < RA; ++ia) {
-      if (TR * ia + TR - 1 <= k) continue;  // warp-uniform: all rows of block ia eliminated
+    for (int ia = 0; ia < RA; ++ia)
 #pragma unroll
-      for (int ib = 0; ib < CB; ++ib) {
-        if (HERM && ib > ia) continue;       // strictly above the diagonal
-        if (TC * ib + TC - 1 <= k) continue;
-        R[ia][ib] = fms(R[ia][ib], Li[ia], Wl[ib]);
-      }
-    }
+      for (int ib = 0; ib < CB; ++ib)
+        if (!HERM || ib <= ia) R[ia][ib] = fms(R[ia][ib], Li[ia], Wl[ib]);
     // publish pivot column k+1 (and row k+1) for the next step
     // (the owning register is selected with compile-time indices only: a runtime index into R
     //  would demote the tile to local memory)

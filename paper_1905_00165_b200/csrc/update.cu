@@ -16,6 +16,8 @@
 // (no 3M trick: keeps the rounding of the textbook product and the paper's flop count).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -319,13 +321,26 @@ static cudaError_t launch_update_t(UpdateArgs a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <bool CPLX, bool BLU> cudaError_t launch_update_ws_t(UpdateArgs a, cudaStream_t s);
+
+// Fast path (update_ws.cu: persistent, warp-specialized, TMA-fed) for 16-byte-aligned operands;
+// the cp.async kernel above handles unaligned real matrices (odd ld) and forced fallback.
+static int g_force_generic = -1;
 cudaError_t launch_update(Kind kind, UpdateArgs a, cudaStream_t s) {
+  if (g_force_generic < 0) {
+    const char* e = getenv("DPP_UPDATE_GENERIC");  // test hook: exercise the generic kernel
+    g_force_generic = (e && e[0] == '1') ? 1 : 0;
+  }
+  const bool ws = a.vec && !g_force_generic;
   switch (kind) {
     case HERM_D:
+      if (ws) return launch_update_ws_t<false, false>(a, s);
       return a.vec ? launch_update_t<false, false, true>(a, s) : launch_update_t<false, false, false>(a, s);
     case HERM_Z:
+      if (ws) return launch_update_ws_t<true, false>(a, s);
       return launch_update_t<true, false, true>(a, s);
     case LU_Z:
+      if (ws) return launch_update_ws_t<true, true>(a, s);
       return launch_update_t<true, true, true>(a, s);
   }
   return cudaErrorInvalidValue;
