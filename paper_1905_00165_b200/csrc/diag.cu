@@ -1,4 +1,5 @@
-// diag.cu -- Stage 1: sequential sample-and-factor of one diagonal tile.
+// diag.cu -- Stage 1: sequential sample-and-factor of one diagonal tile,
+// plus the tile operators that turn stage 2 into tensor-core GEMMs.
 //
 // Listing 4 replaces the diagonal-block LU of Listing 3 (line 583) by the
 // unblocked sampler of Listing 1 applied to A_J1:
@@ -17,7 +18,11 @@
 //    blocks strictly above the diagonal are skipped at compile time);
 //  * column k keeps its unscaled values after step k; the scaling L = w * (1/p) and the final
 //    pivots are applied once at the end (reading R17), and the log-likelihood / tie / range
-//    bookkeeping is done in parallel after the loop and summed by one thread IN PIVOT ORDER.
+//    bookkeeping is done in parallel after the loop and summed by one thread IN PIVOT ORDER;
+//  * then (if a trailing matrix remains) the inverses of the unit-lower L11 (and, LU, of U11) are
+//    formed by a 16x16-blocked triangular inversion in shared memory, and written as the small
+//    right/left operators of the stage-2 GEMMs (L21 = A21 L11^-H D1^-1, U12 = L11^-1 A12,
+//    L21 = A21 U11^-1) -- Listing 3 lines 584-585 as products with inverses.
 // The Hermitian path reads/writes the lower triangle only.
 #include <cuda_runtime.h>
 
@@ -27,14 +32,89 @@
 
 namespace dpp {
 
+__device__ __forceinline__ double madd(double c, double a, double b) { return fma(a, b, c); }
+__device__ __forceinline__ double2 madd(double2 c, double2 a, double2 b) {
+  double rx = fma(a.x, b.x, c.x);
+  rx = fma(-a.y, b.y, rx);
+  double ry = fma(a.x, b.y, c.y);
+  ry = fma(a.y, b.x, ry);
+  return make_double2(rx, ry);
+}
+__device__ __forceinline__ double neg(double a) { return -a; }
+__device__ __forceinline__ double2 neg(double2 a) { return make_double2(-a.x, -a.y); }
+
+// block-packed lower-triangular storage: 16x16 blocks (I >= J), column-major inside a block
+__device__ __forceinline__ int bp(int i, int k) {
+  const int I = i >> 4, J = k >> 4;
+  return ((I * (I + 1) / 2 + J) << 8) + (i & 15) + ((k & 15) << 4);
+}
+
+// X = L^{-1} for a lower-triangular L (unit or not) of order 16*nblk, both block-packed in smem.
+// Tb: scratch for (nblk - 1) 16x16 blocks.  All 256 threads participate.
+template <typename T, bool UNIT>
+__device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // diagonal blocks: warp w inverts block w (lane c < 16 forms column c by forward substitution)
+  for (int I = warp; I < nblk; I += 8) {
+    if (lane < 16) {
+      const int c = lane;
+      const T* Lblk = Lb + ((I * (I + 1) / 2 + I) << 8);
+      T x[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        T s = (i == c) ? make_real(1.0, zero<T>()) : zero<T>();
+#pragma unroll
+        for (int l = 0; l < i; ++l) s = fms(s, Lblk[i + (l << 4)], x[l]);
+        x[i] = UNIT ? s : mul(s, recip(Lblk[i + (i << 4)]));
+      }
+      T* Xblk = Xb + ((I * (I + 1) / 2 + I) << 8);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) Xblk[i + (c << 4)] = x[i];
+    }
+  }
+  const int r = tid & 15, c = tid >> 4;
+  for (int d = 1; d < nblk; ++d) {
+    __syncthreads();
+    // T_q = sum_{K=J}^{I-1} L_{IK} X_{KJ}   for (I, J) = (d + q, q)
+    for (int q = 0; q + d < nblk; ++q) {
+      const int I = d + q, J = q;
+      T s = zero<T>();
+      for (int K = J; K < I; ++K) {
+        const T* Lblk = Lb + ((I * (I + 1) / 2 + K) << 8);
+        const T* Xblk = Xb + ((K * (K + 1) / 2 + J) << 8);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) s = madd(s, Lblk[r + (k << 4)], Xblk[k + (c << 4)]);
+      }
+      Tb[(q << 8) + r + (c << 4)] = s;
+    }
+    __syncthreads();
+    // X_{IJ} = -X_{II} T_q
+    for (int q = 0; q + d < nblk; ++q) {
+      const int I = d + q, J = q;
+      const T* Xii = Xb + ((I * (I + 1) / 2 + I) << 8);
+      T s = zero<T>();
+#pragma unroll
+      for (int l = 0; l < 16; ++l) s = madd(s, Xii[r + (l << 4)], Tb[(q << 8) + l + (c << 4)]);
+      Xb[((I * (I + 1) / 2 + J) << 8) + r + (c << 4)] = neg(s);
+    }
+  }
+  __syncthreads();
+}
+
 template <typename T, bool HERM, int NB>
 __global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
   constexpr int TR = 16, TC = 16, RA = NB / TR, CB = NB / TC;
+  constexpr int NBLK = NB / 16, NPB = NBLK * (NBLK + 1) / 2;  // packed 16x16 blocks
   __shared__ T colbuf[2][NB];
   __shared__ T rowbuf[HERM ? 1 : 2][HERM ? 1 : NB];
   __shared__ T pv[NB], rv[NB];
   __shared__ double U[NB], dv[NB], imv[NB], lg[NB];
   __shared__ uint8_t keepv[NB];
+  extern __shared__ __align__(16) unsigned char dsm[];
+  T* Lb = reinterpret_cast<T*>(dsm);          // block-packed L11 (unit lower)
+  T* Ub = Lb + NPB * 256;                      // LU: block-packed U11^T (lower, non-unit)
+  T* Xb = Ub + (HERM ? 0 : NPB * 256);         // inverse
+  T* Tb = Xb + NPB * 256;                      // scratch (NBLK - 1 blocks)
 
   const int s = blockIdx.y;
   const int jb = a.jb;
@@ -92,16 +172,14 @@ __global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
       const int l = tc + TC * ib;
       Wl[ib] = (l > k && l < jb) ? (HERM ? cj(colbuf[cur][l]) : rowbuf[HERM ? 0 : cur][l]) : zero<T>();
     }
-    // rank-1 update (line 439); eliminated rows/columns have zero multipliers, so the update is
-    // branch-free (Hermitian: blocks strictly above the diagonal are skipped statically)
+    // rank-1 update (line 439), branch-free
 #pragma unroll
     for (int ia = 0; ia < RA; ++ia)
 #pragma unroll
       for (int ib = 0; ib < CB; ++ib)
         if (!HERM || ib <= ia) R[ia][ib] = fms(R[ia][ib], Li[ia], Wl[ib]);
-    // publish pivot column k+1 (and row k+1) for the next step
-    // (the owning register is selected with compile-time indices only: a runtime index into R
-    //  would demote the tile to local memory)
+    // publish pivot column k+1 (and row k+1); the owning register is selected with compile-time
+    // indices only (a runtime index into R would demote the tile to local memory)
     const int kn = k + 1;
     if (kn < jb) {
 #pragma unroll
@@ -130,17 +208,23 @@ __global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
     __syncthreads();
   }
 
-  // ---- finalize the factor: L = (unscaled column) * (1/p), diagonal = final pivot
+  // ---- finalize the factor: L = (unscaled column) * (1/p), diagonal = final pivot; also stage
+  //      the triangular factors block-packed for the inversion (identity beyond jb)
+  const bool ops = a.need_ops != 0;
 #pragma unroll
   for (int ia = 0; ia < RA; ++ia)
 #pragma unroll
     for (int ib = 0; ib < CB; ++ib) {
       const int i = tr + TR * ia, l = tc + TC * ib;
-      if (i < jb && l < jb && (!HERM || i >= l)) {
-        T v = R[ia][ib];
-        if (i > l) v = mul(v, rv[l]);
-        else if (i == l) v = pv[l];
-        A[(int64_t)l * a.ld + i] = v;
+      T v = R[ia][ib];
+      if (i > l) v = mul(v, rv[l < jb ? l : 0]);
+      else if (i == l) v = pv[i < jb ? i : 0];
+      const bool in = i < jb && l < jb;
+      if (in && (!HERM || i >= l)) A[(int64_t)l * a.ld + i] = v;
+      if (ops) {
+        const T one = make_real(1.0, zero<T>());
+        if (i >= l) Lb[bp(i, l)] = (i == l) ? one : (in ? v : zero<T>());
+        if (!HERM && i <= l) Ub[bp(l, i)] = in ? v : (i == l ? one : zero<T>());  // U^T(l, i) = U(i, l)
       }
     }
   // ---- decisions, likelihood terms and diagnostics, in parallel; summed in pivot order
@@ -176,17 +260,59 @@ __global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
       }
     }
   }
+  if (!ops) return;
+
+  // ---- stage-2 operators from the inverses of the tile's triangular factors
+  const int nblk = (jb + 15) >> 4;
+  T* Bm = reinterpret_cast<T*>(a.Bm) + (int64_t)s * a.strideM;
+  tri_inverse_lower<T, true>(Lb, Xb, Tb, nblk);  // Xb = L11^{-1}
+  if (HERM) {
+    double* dvec = a.dvec + (int64_t)s * a.ldm;  // D1 of sample s (stride nb)
+    for (int k = tid; k < jb; k += 256) dvec[k] = re(pv[k]);
+    // Bm(j,k) = delta_jk - conj(Linv(j,k)) / D(j)  (j >= k), 0 above
+    for (int idx = tid; idx < jb * jb; idx += 256) {
+      const int k = idx / jb, j = idx % jb;
+      T v = zero<T>();
+      if (j >= k) {
+        v = neg(mul(cj(Xb[bp(j, k)]), make_real(re(rv[j]), zero<T>())));
+        if (j == k) v = make_real(re(v) + 1.0, v);
+      }
+      Bm[j + (int64_t)k * a.ldm] = v;
+    }
+  } else {
+    // Am(i,k) = -Linv(i,k) (i > k), else 0
+    T* Am = reinterpret_cast<T*>(a.Am) + (int64_t)s * a.strideM;
+    for (int idx = tid; idx < jb * jb; idx += 256) {
+      const int k = idx / jb, i = idx % jb;
+      Am[i + (int64_t)k * a.ldm] = (i > k) ? neg(Xb[bp(i, k)]) : zero<T>();
+    }
+    __syncthreads();
+    tri_inverse_lower<T, false>(Ub, Xb, Tb, nblk);  // Xb = (U11^T)^{-1} = (U11^{-1})^T
+    // Bm(j,k) = delta_jk - Uinv(k,j) = delta_jk - Xb(j,k)  (j >= k), 0 above
+    for (int idx = tid; idx < jb * jb; idx += 256) {
+      const int k = idx / jb, j = idx % jb;
+      T v = zero<T>();
+      if (j >= k) {
+        v = neg(Xb[bp(j, k)]);
+        if (j == k) v = make_real(re(v) + 1.0, v);
+      }
+      Bm[j + (int64_t)k * a.ldm] = v;
+    }
+  }
 }
 
 template <typename T, bool HERM, int NB>
 static cudaError_t launch_diag_t(const DiagArgs& a, cudaStream_t s) {
+  constexpr int NBLK = NB / 16, NPB = NBLK * (NBLK + 1) / 2;
+  const size_t smem = a.need_ops ? (size_t)((HERM ? 2 : 3) * NPB * 256 + (NBLK - 1) * 256) * sizeof(T) : 0;
+  auto* fn = diag_kernel<T, HERM, NB>;
+  if (smem > 0) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   dim3 grid(1, a.batch);
-  diag_kernel<T, HERM, NB><<<grid, 256, 0, s>>>(a);
+  fn<<<grid, 256, smem, s>>>(a);
   return cudaGetLastError();
-}
-
-size_t diag_smem_bytes(Kind kind, int nb) {
-  return (size_t)nb * (kind == HERM_D ? 8 : 16) * 6 + nb * 33;
 }
 
 cudaError_t launch_diag(Kind kind, int nb, const DiagArgs& a, cudaStream_t s) {

@@ -3,11 +3,12 @@
 // One sample of DPP(K) for a Hermitian real K too large (or too slow) for one GPU.  Rank r of P
 // owns block columns c = r, r+P, ... (width nb) of the lower triangle, stored contiguously.  Block
 // step k of Listing 3/4:
-//   owner(k) = k mod P:  stage 1 diag tile (decisions + D1), stage 2 panel (W21 = A21 L11^{-T},
-//                        L21 in place), pack [state | D1 | mask bits | W21] into the message;
+//   owner(k) = k mod P:  stage 1 diag tile (decisions + D1 + tile operator), stage 2 panel GEMM
+//                        (L21 = A21 L11^{-T} D1^{-1}, in place), pack [state | D1 | mask | L21];
 //   all ranks:           ncclBroadcast(message, root = owner(k))   -- the one exchange per step;
-//   receivers:           unpack state + mask, form L21 = W21 D1^{-1} locally;
-//   all ranks:           stage 3 on their local trailing block columns (C -= L21 W21^T).
+//   receivers:           unpack state + decisions;
+//   all ranks:           stage 3 on their local trailing block columns (C -= L21 D1 L21^T) with the
+//                        DMMA update kernel in block-cyclic addressing mode.
 // Because the decisions, pivots and the running log-likelihood ride in the message, every rank
 // ends with the full mask and the same pivot-ordered loglik; no further collective is needed.
 #include <cuda_runtime.h>
@@ -32,7 +33,7 @@ constexpr size_t ALIGN = 256;
 inline size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-// message = [SampleState 64 B][D1: nb doubles][mask: nb bytes -> 256-aligned][W21: ldw x nb]
+// message = [SampleState 64 B][D1: nb doubles][mask: nb bytes -> 256-aligned][L21: ldw x nb]
 struct MsgLayout {
   size_t d_off, mask_off, w_off, header_bytes;
 };
@@ -45,9 +46,9 @@ MsgLayout msg_layout(int nb) {
   return m;
 }
 
-// work = [state][message buffer][L21 buffer (receivers): ldw x nb]
+// work = [state][panel operator Bm: nb x nb][D1: nb][message buffer]
 struct DistWs {
-  size_t state_off, msg_off, l_off, total;
+  size_t state_off, bm_off, d_off, msg_off, total;
   int64_t ldw;
 };
 DistWs dist_ws(int64_t n, int nb) {
@@ -56,8 +57,9 @@ DistWs dist_ws(int64_t n, int nb) {
   MsgLayout m = msg_layout(nb);
   size_t off = 0;
   w.state_off = off; off = align_up(off + sizeof(SampleState));
+  w.bm_off = off; off = align_up(off + (size_t)nb * nb * 8);
+  w.d_off = off; off = align_up(off + (size_t)nb * 8);
   w.msg_off = off; off = align_up(off + m.header_bytes + (size_t)w.ldw * nb * 8);
-  w.l_off = off; off = align_up(off + (size_t)w.ldw * nb * 8);
   w.total = off;
   return w;
 }
@@ -72,19 +74,9 @@ __global__ void pack_header_kernel(const SampleState* st, const double* T11, int
   }
 }
 
-__global__ void unpack_kernel(const char* msg, MsgLayout m, int jb, SampleState* st, uint8_t* mask_j0,
-                              double* L, int64_t ldl, int64_t m2) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t == 0) *st = *reinterpret_cast<const SampleState*>(msg);
-  if (blockIdx.x == 0)
-    for (int k = threadIdx.x; k < jb; k += blockDim.x) mask_j0[k] = reinterpret_cast<const uint8_t*>(msg + m.mask_off)[k];
-  const double* D = reinterpret_cast<const double*>(msg + m.d_off);
-  const double* W = reinterpret_cast<const double*>(msg + m.w_off);
-  const int64_t total = m2 * jb;
-  for (int64_t i = t; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = i / m2, r = i % m2;
-    L[k * ldl + r] = W[k * ldl + r] / D[k];  // L21 = W21 D1^{-1}
-  }
+__global__ void unpack_header_kernel(const char* msg, MsgLayout m, int jb, SampleState* st, uint8_t* mask_j0) {
+  if (threadIdx.x == 0) *st = *reinterpret_cast<const SampleState*>(msg);
+  for (int k = threadIdx.x; k < jb; k += blockDim.x) mask_j0[k] = reinterpret_cast<const uint8_t*>(msg + m.mask_off)[k];
 }
 
 __global__ void finalize_kernel(const SampleState* st, double* loglik, dpp_info_t* info) {
@@ -157,10 +149,12 @@ int dpp_sample_herm_d_dist(dpp_comm_t comm, int64_t n, double* K_local, int64_t 
   const int P = comm->nranks, r = comm->rank;
   char* w = reinterpret_cast<char*>(work);
   SampleState* state = reinterpret_cast<SampleState*>(w + W.state_off);
+  double* Bm = reinterpret_cast<double*>(w + W.bm_off);
+  double* dvec = reinterpret_cast<double*>(w + W.d_off);
   char* msg = w + W.msg_off;
-  double* Lbuf = reinterpret_cast<double*>(w + W.l_off);
   const MsgLayout M = msg_layout(nb);
-  double* Wmsg = reinterpret_cast<double*>(msg + M.w_off);
+  double* Lmsg = reinterpret_cast<double*>(msg + M.w_off);          // L21 rows j1.., ld = ldw
+  const double* Dmsg = reinterpret_cast<const double*>(msg + M.d_off);
   const int64_t nblk = (n + nb - 1) / nb;
   const bool vec = (ld_local % 2 == 0) && (reinterpret_cast<uintptr_t>(K_local) % 16 == 0);
 
@@ -176,37 +170,40 @@ int dpp_sample_herm_d_dist(dpp_comm_t comm, int64_t n, double* K_local, int64_t 
       d.A = K_local; d.ld = ld_local; d.strideA = 0; d.n = n; d.j0 = j0; d.tcol = tcol; d.jb = jb;
       d.seed = seed; d.b0 = 0; d.mask = mask; d.forced = forced; d.state = state; d.loglik = nullptr;
       d.info = nullptr; d.tie_tol = tie_tol; d.range_tol = range_tol; d.batch = 1;
+      d.need_ops = m2 > 0; d.Bm = Bm; d.dvec = dvec; d.ldm = nb; d.strideM = 0;
       CK(launch_diag(HERM_D, nb, d, st));
       if (m2 > 0) {
-        PanelArgs p{};
-        p.A = K_local; p.ld = ld_local; p.strideA = 0; p.n = n; p.j0 = j0; p.tcol = tcol; p.jb = jb;
-        p.W = Wmsg; p.ldw = W.ldw; p.strideW = 0; p.batch = 1;
-        CK(launch_panel(HERM_D, nb, p, st));
+        // stage 2 in place: L21 = A21 L11^-T D1^-1, then into the message
+        UpdateArgs p{};
+        p.Aop = K_local + j1 + tcol * ld_local; p.lda = ld_local;
+        p.Bop = Bm; p.ldb = nb;
+        p.C = K_local + j1 + tcol * ld_local; p.ldc = ld_local;
+        p.a_rows = (int)m2; p.b_rows = jb; p.K = jb; p.rows = (int)m2; p.cols = jb; p.batch = 1; p.vec = vec ? 1 : 0;
+        CK(launch_update(HERM_D, p, st));
+        CK(cudaMemcpy2DAsync(Lmsg, (size_t)W.ldw * 8, K_local + j1 + tcol * ld_local, (size_t)ld_local * 8,
+                             (size_t)m2 * 8, (size_t)jb, cudaMemcpyDeviceToDevice, st));
       }
       pack_header_kernel<<<1, 128, 0, st>>>(state, K_local + j0 + tcol * ld_local, ld_local, jb, mask + j0, msg, M);
       CK(cudaGetLastError());
     }
-    // one exchange per block step: header (+ W21 when a trailing matrix remains)
+    // one exchange per block step: header (+ L21 when a trailing matrix remains)
     const size_t bytes = M.header_bytes + (m2 > 0 ? (size_t)W.ldw * (size_t)jb * 8 : 0);
     if (P > 1) NK(ncclBroadcast(msg, msg, bytes, ncclChar, owner, comm->nccl, st));
     if (r != owner) {
-      const int64_t tot = std::max<int64_t>(m2 * jb, 1);
-      const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
-      unpack_kernel<<<blocks, 256, 0, st>>>(msg, M, jb, state, mask + j0, Lbuf, W.ldw, m2);
+      unpack_header_kernel<<<1, 128, 0, st>>>(msg, M, jb, state, mask + j0);
       CK(cudaGetLastError());
     }
     if (m2 <= 0) break;
     // stage 3 on the local trailing block columns: blocks c > k with c = r + q P
-    const int64_t q0 = (k + 1 - r + P - 1) / P > 0 ? (k + 1 - r + P - 1) / P : 0;  // first q with r + qP > k
-    const int64_t nloc = (nblk - r + P - 1) / P;                                      // local blocks on r
+    const int64_t q0 = (k + 1 - r + P - 1) / P;  // first q with r + qP > k
+    const int64_t nloc = (nblk - r + P - 1) / P;  // local blocks on r
     if (q0 < nloc) {
       UpdateArgs u{};
-      if (r == owner) { u.Aop = K_local + j1 + tcol * ld_local; u.lda = ld_local; }
-      else { u.Aop = Lbuf; u.lda = W.ldw; }
-      u.Bop = Wmsg; u.ldb = W.ldw;
+      u.Aop = Lmsg; u.lda = W.ldw;
+      u.Bop = Lmsg; u.ldb = W.ldw; u.dscale = Dmsg; u.mask = 1;
       u.C = K_local + j1;  // local column 0, A22 row 0
       u.ldc = ld_local;
-      u.m_total = (int)m2; u.K = jb; u.batch = 1; u.vec = vec ? 1 : 0;
+      u.a_rows = (int)m2; u.b_rows = (int)m2; u.K = jb; u.batch = 1; u.vec = vec ? 1 : 0;
       u.row0 = 0; u.rows = (int)m2; u.col0 = 0; u.cols = (int)m2; u.tri = 0;
       u.bcc_P = P; u.bcc_r = r; u.bcc_nb = nb; u.bcc_q0 = (int)q0; u.bcc_j1 = j1;
       u.tiles_n = (int)(nloc - q0);

@@ -2,7 +2,11 @@
 //
 // Blocked, right-looking DPP sampling = Listing 3's loop with line 583
 // replaced by the unblocked sampler (Listing 4):
-//   for j0 in 0, nb, 2nb, ...:   stage 1 diag(j0) -> stage 2 panel(j0) -> stage 3 update(j0)
+//   for j0 in 0, nb, 2nb, ...:
+//     stage 1  diag(j0):   sample-and-factor the diagonal tile; form the small inverse operators
+//     stage 2  panel(j0):  L21 = A21 L11^-H D1^-1 (Hermitian) or L21 = A21 U11^-1, U12 = L11^-1 A12
+//                          (LU), as DMMA GEMMs with those operators (update kernels)
+//     stage 3  update(j0): A22 -= L21 D1 L21^H (lower) or A22 -= L21 U12 (DMMA)
 // With lookahead (the GPU analogue of the paper's tile-dependency task
 // scheduling) the update of step k is split into
 //   (a) the next block column (and, for LU, the next block row), on the high-priority stream S1,
@@ -44,7 +48,7 @@ int resolve_opts(Kind kind, const dpp_opts_t* o, Opts* r) {
   r->forced = o ? o->forced : nullptr;
   r->batch_chunk = o ? o->batch_chunk : 0;
   if (r->nb != 32 && r->nb != 64 && r->nb != 128) return DPP_EINVAL;
-  if (kind != HERM_D && r->nb > 64) return DPP_EINVAL;  // complex tile must fit shared memory
+  if (kind != HERM_D && r->nb > 64) return DPP_EINVAL;  // complex tile must fit the diag kernel
   if (r->lookahead < 0 || r->lookahead > 1) return DPP_EINVAL;
   if (r->batch_chunk < 0) return DPP_EINVAL;
   return DPP_OK;
@@ -53,24 +57,28 @@ int resolve_opts(Kind kind, const dpp_opts_t* o, Opts* r) {
 size_t esize(Kind k) { return k == HERM_D ? 8 : 16; }
 
 // Workspace layout (all regions 256-byte aligned):
-//   [SampleState x chunk][W21 double buffer: 2 x chunk x ldw x nb (Hermitian)]
+//   [SampleState x chunk]
+//   [panel operators: Bm (and Am for LU), nb x nb per sample]
+//   [D1 double buffer (Hermitian): 2 x chunk x nb doubles]
 //   [K copies: chunk x ldk x n (batched / host)][host staging: mask, loglik, info (host)]
 struct WsLayout {
-  size_t state_off, w_off, k_off, mask_off, ll_off, info_off, total;
-  int64_t ldw, ldk, strideW, strideK;
+  size_t state_off, bm_off, am_off, d_off, k_off, mask_off, ll_off, info_off, total;
+  int64_t ldk, strideK, strideM;
 };
 
 WsLayout layout(Kind kind, int64_t chunk, int64_t n, int nb, bool copies, bool host) {
   WsLayout L{};
   const size_t es = esize(kind);
-  L.ldw = std::max<int64_t>(round_up(n, 16), 16);
   L.ldk = std::max<int64_t>(round_up(n, 16), 16);
-  L.strideW = L.ldw * std::max<int64_t>(std::min<int64_t>(nb, n), 1);  // W21 is at most min(nb, n) wide
   L.strideK = L.ldk * std::max<int64_t>(n, 1);
+  L.strideM = (int64_t)nb * nb;
   size_t off = 0;
   L.state_off = off; off = align_up(off + sizeof(SampleState) * (size_t)chunk);
-  L.w_off = off;
-  if (kind != LU_Z) off = align_up(off + 2 * (size_t)chunk * (size_t)L.strideW * es);
+  L.bm_off = off; off = align_up(off + (size_t)chunk * L.strideM * es);
+  L.am_off = off;
+  if (kind == LU_Z) off = align_up(off + (size_t)chunk * L.strideM * es);
+  L.d_off = off;
+  if (kind != LU_Z) off = align_up(off + 2 * (size_t)chunk * nb * 8);
   L.k_off = off;
   if (copies) off = align_up(off + (size_t)chunk * (size_t)L.strideK * es);
   L.mask_off = off;
@@ -163,11 +171,46 @@ double region_flops(Kind kind, int64_t row0, int64_t col0, int64_t rows, int64_t
   return elems * 2.0 * K * cplx_mult(kind);
 }
 
+int device_sms() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+// SMs to leave to the lookahead stream while the trailing update (b) of this step runs
+// persistently on the rest: minimise max(T1, T2) with T1 = diag latency + (tiles of the next
+// block column's update + next panel) / R, T2 = tiles of (b) / (SMs - R), in units of one tile.
+int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile) {
+  const double diag_tiles = 6.0;  // the diag tile ~ 6 update-tile times (measured ~110 us vs ~17 us)
+  const double ta = (double)((m2 + tile - 1) / tile) * batch;        // (a): next block column
+  const double tp = (double)((m2 - jn + tile - 1) / tile) * batch;   // next panel GEMM
+  const int64_t tb_side = (m2 - jn + tile - 1) / tile;
+  const double tb = (double)tb_side * (tb_side + 1) / 2 * batch;       // (b) lower-triangle tiles
+  int best = 8;
+  double best_t = 1e300;
+  for (int R = 4; R <= sms / 2; R += 2) {
+    const double t1 = diag_tiles + (ta + tp) / R;
+    const double t2 = tb / (sms - R);
+    const double t = t1 > t2 ? t1 : t2;
+    if (t < best_t) { best_t = t; best = R; }
+  }
+  return best;
+}
+
+UpdateArgs base_update(Kind kind, int batch, bool vec) {
+  UpdateArgs u{};
+  u.batch = batch;
+  u.vec = vec ? 1 : 0;
+  (void)kind;
+  return u;
+}
+
 // ---------------------------------------------------------------- the blocked factorization
 // Factors `batch` matrices A + s*strideA (in place), samples b0 + s.
 int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_t strideA, int batch,
                 uint64_t seed, uint64_t b0, uint8_t* mask, const uint8_t* forced, double* loglik,
-                dpp_info_t* info, void* state, void* W, int64_t ldw, int64_t strideW, cudaStream_t caller) {
+                dpp_info_t* info, char* work, const WsLayout& L, cudaStream_t caller) {
+  void* state = work + L.state_off;
   if (n == 0) { CK(launch_zero_state(state, loglik, info, batch, caller)); return DPP_OK; }
   DeviceStreams* ds = nullptr;
   int rc = get_streams(&ds);
@@ -182,44 +225,67 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     CK(cudaStreamWaitEvent(s2, ds->ev_start, 0));
   }
   const size_t es = esize(kind);
+  const bool herm = kind != LU_Z;
   char* Ab = reinterpret_cast<char*>(A);
-  const bool vec = kind != HERM_D ||
-                   ((ld % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (ldw % 2 == 0));
+  const bool vec = kind != HERM_D || ((ld % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                                      (strideA % 2 == 0));
+  void* Bm = work + L.bm_off;
+  void* Am = work + L.am_off;
   int step = 0;
   bool have_rest = false;
+  const int sms = device_sms();
   for (int64_t j0 = 0; j0 < n; j0 += nb, ++step) {
     const int jb = (int)std::min<int64_t>(nb, n - j0);
     const int64_t j1 = j0 + jb, m2 = n - j1;
+    double* dvec = herm ? reinterpret_cast<double*>(work + L.d_off) + (size_t)(step & 1) * batch * nb : nullptr;
+    // ---- stage 1
     DiagArgs d{};
     d.A = A; d.ld = ld; d.strideA = strideA; d.n = n; d.j0 = j0; d.tcol = j0; d.jb = jb; d.seed = seed; d.b0 = b0;
     d.mask = mask; d.forced = forced; d.state = state; d.loglik = loglik; d.info = info;
     d.tie_tol = o.tie_tol; d.range_tol = o.range_tol; d.batch = batch;
+    d.need_ops = m2 > 0; d.Bm = Bm; d.Am = Am; d.dvec = dvec; d.ldm = nb; d.strideM = L.strideM;
     {
-      const double fl = (kind == LU_Z ? 2.0 : 1.0) * jb * (double)jb * jb / 3.0 * cplx_mult(kind) * batch;
+      const double fl = (herm ? 1.0 : 2.0) * jb * (double)jb * jb / 3.0 * cplx_mult(kind) * batch;
       ProfScope ps(0, fl, s1);
       CK(launch_diag(kind, nb, d, s1));
     }
     if (m2 <= 0) break;
-    void* Wk = W ? reinterpret_cast<char*>(W) + (size_t)(step & 1) * (size_t)batch * (size_t)strideW * es : nullptr;
-    PanelArgs p{};
-    p.A = A; p.ld = ld; p.strideA = strideA; p.n = n; p.j0 = j0; p.tcol = j0; p.jb = jb; p.W = Wk; p.ldw = ldw;
-    p.strideW = strideW; p.batch = batch;
+    // ---- stage 2: panel GEMMs with the tile operators (in place)
     {
-      const double fl = (kind == LU_Z ? 2.0 : 1.0) * (double)m2 * jb * jb * cplx_mult(kind) * batch;
+      const double fl = (herm ? 1.0 : 2.0) * (double)m2 * jb * jb * cplx_mult(kind) * batch;  // TRSM count
       ProfScope ps(1, fl, s1);
-      CK(launch_panel(kind, nb, p, s1));
+      UpdateArgs p = base_update(kind, batch, vec);
+      p.Aop = Ab + (size_t)(j1 + j0 * ld) * es; p.lda = ld; p.strideA = strideA;   // A21
+      p.Bop = Bm; p.ldb = nb; p.strideB = L.strideM;
+      p.C = Ab + (size_t)(j1 + j0 * ld) * es; p.ldc = ld; p.strideC = strideA;    // L21 in place
+      p.a_rows = (int)m2; p.b_rows = jb; p.K = jb;
+      p.row0 = 0; p.col0 = 0; p.rows = (int)m2; p.cols = jb;
+      CK(launch_update(kind, p, s1));
+      if (!herm) {
+        UpdateArgs q = base_update(kind, batch, vec);
+        q.Aop = Am; q.lda = nb; q.strideA = L.strideM;                             // I - L11^-1
+        q.Bop = Ab + (size_t)(j0 + j1 * ld) * es; q.ldb = ld; q.strideB = strideA;  // A12 (k, j)
+        q.bnmajor = 1;
+        q.C = Ab + (size_t)(j0 + j1 * ld) * es; q.ldc = ld; q.strideC = strideA;   // U12 in place
+        q.a_rows = jb; q.b_rows = (int)m2; q.K = jb;
+        q.row0 = 0; q.col0 = 0; q.rows = jb; q.cols = (int)m2;
+        CK(launch_update(kind, q, s1));
+      }
     }
-
-    UpdateArgs u{};
-    u.Aop = Ab + (size_t)(j1 + j0 * ld) * es;  // L21
-    u.lda = ld; u.strideA = strideA;
-    if (kind == LU_Z) { u.Bop = Ab + (size_t)(j0 + j1 * ld) * es; u.ldb = ld; u.strideB = strideA; }  // U12
-    else { u.Bop = Wk; u.ldb = ldw; u.strideB = strideW; }
+    // ---- stage 3 operands
+    UpdateArgs u = base_update(kind, batch, vec);
+    u.Aop = Ab + (size_t)(j1 + j0 * ld) * es; u.lda = ld; u.strideA = strideA;  // L21
+    if (herm) {
+      u.Bop = u.Aop; u.ldb = ld; u.strideB = strideA;  // L21, scaled by D1 (and conjugated) on load
+      u.dscale = dvec; u.dstride = nb; u.mask = 1; u.conj = (kind == HERM_Z);
+    } else {
+      u.Bop = Ab + (size_t)(j0 + j1 * ld) * es; u.ldb = ld; u.strideB = strideA; u.bnmajor = 1;  // U12
+    }
     u.C = Ab + (size_t)(j1 + j1 * ld) * es; u.ldc = ld; u.strideC = strideA;
-    u.m_total = (int)m2; u.K = jb; u.batch = batch; u.vec = vec ? 1 : 0;
+    u.a_rows = (int)m2; u.b_rows = (int)m2; u.K = jb;
     const int jn = (int)std::min<int64_t>(nb, m2);  // width of the next block
     if (!la) {
-      u.row0 = 0; u.col0 = 0; u.rows = (int)m2; u.cols = (int)m2; u.tri = (kind != LU_Z);
+      u.row0 = 0; u.col0 = 0; u.rows = (int)m2; u.cols = (int)m2; u.tri = herm;
       ProfScope ps(3, region_flops(kind, 0, 0, m2, m2, jb) * batch, s1);
       CK(launch_update(kind, u, s1));
       continue;
@@ -231,10 +297,10 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       UpdateArgs ua = u;
       ua.row0 = 0; ua.col0 = 0; ua.rows = (int)m2; ua.cols = jn; ua.tri = 0;
       double fl = region_flops(kind, 0, 0, m2, jn, jb);
-      if (kind == LU_Z && m2 > jn) fl += region_flops(kind, 0, jn, jn, m2 - jn, jb);
+      if (!herm && m2 > jn) fl += region_flops(kind, 0, jn, jn, m2 - jn, jb);
       ProfScope ps(2, fl * batch, s1);
       CK(launch_update(kind, ua, s1));
-      if (kind == LU_Z && m2 > jn) {
+      if (!herm && m2 > jn) {
         UpdateArgs ur = u;
         ur.row0 = 0; ur.col0 = jn; ur.rows = jn; ur.cols = (int)(m2 - jn); ur.tri = 0;
         CK(launch_update(kind, ur, s1));
@@ -245,7 +311,8 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       CK(cudaStreamWaitEvent(s2, ds->ev_panel, 0));
       UpdateArgs ub = u;
       ub.row0 = jn; ub.col0 = jn; ub.rows = (int)(m2 - jn); ub.cols = (int)(m2 - jn);
-      ub.tri = (kind != LU_Z);
+      ub.tri = herm;
+      if (herm && vec) ub.grid_limit = sms - reserve_sms(m2, jn, sms, batch, 128);
       {
         ProfScope ps(3, region_flops(kind, jn, jn, m2 - jn, m2 - jn, jb) * batch, s2);
         CK(launch_update(kind, ub, s2));
@@ -281,9 +348,8 @@ int sample_inplace(Kind kind, int64_t n, void* K, int64_t ld, uint64_t seed, uin
   WsLayout L = layout(kind, 1, n, o.nb, false, false);
   if (!work || work_bytes < L.total || reinterpret_cast<uintptr_t>(work) % ALIGN) return DPP_EWORKSPACE;
   if (kind != HERM_D && reinterpret_cast<uintptr_t>(K) % 16) return DPP_EINVAL;
-  char* w = reinterpret_cast<char*>(work);
-  return run_blocked(kind, o, n, K, ld, 0, 1, seed, 0, mask, o.forced, loglik, info, w + L.state_off,
-                     kind != LU_Z ? w + L.w_off : nullptr, L.ldw, L.strideW, st);
+  return run_blocked(kind, o, n, K, ld, 0, 1, seed, 0, mask, o.forced, loglik, info, reinterpret_cast<char*>(work),
+                     L, st);
 }
 
 int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t ld, int64_t strideK, uint64_t seed,
@@ -325,8 +391,7 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
     double* llk = host ? reinterpret_cast<double*>(w + L.ll_off) : loglik + c0;
     dpp_info_t* ifo = host ? (info ? reinterpret_cast<dpp_info_t*>(w + L.info_off) : nullptr) : (info ? info + c0 : nullptr);
     const uint8_t* fz = o.forced ? o.forced + c0 * n : nullptr;
-    rc = run_blocked(kind, o, n, Kc, L.ldk, L.strideK, cb, seed, b0 + (uint64_t)c0, mk, fz, llk, ifo,
-                     w + L.state_off, kind != LU_Z ? w + L.w_off : nullptr, L.ldw, L.strideW, st);
+    rc = run_blocked(kind, o, n, Kc, L.ldk, L.strideK, cb, seed, b0 + (uint64_t)c0, mk, fz, llk, ifo, w, L, st);
     if (rc) return rc;
     if (host) {
       if (n > 0) CK(cudaMemcpyAsync(mask + c0 * n, mk, (size_t)cb * n, cudaMemcpyDeviceToHost, st));
@@ -389,7 +454,6 @@ int dpp_philox_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, d
 }
 
 int dpp_profile_begin(void) {
-  for (auto& r : g_prof.recs) (void)r;
   g_prof.recs.clear();
   g_prof.used = 0;
   g_prof.on = true;
@@ -425,6 +489,6 @@ const char* dpp_strerror(int code) {
   return "unknown error";
 }
 
-const char* dpp_version(void) { return "dpp-b200 0.1.0 (sm_100a)"; }
+const char* dpp_version(void) { return "dpp-b200 0.2.0 (sm_100a)"; }
 
 }  // extern "C"

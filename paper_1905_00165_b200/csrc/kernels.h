@@ -8,7 +8,8 @@ namespace dpp {
 enum Kind { HERM_D = 0, HERM_Z = 1, LU_Z = 2 };
 
 // Stage 1: sequential sample-and-factor of the jb x jb diagonal tile at (j0, j0)
-// (Listing 4 line "subsample, A_J1 = unblocked_dpp(A_J1)").
+// (Listing 4 line "subsample, A_J1 = unblocked_dpp(A_J1)"), followed by the
+// small dense operators stage 2 needs (inverses of the tile's triangular factors).
 struct DiagArgs {
   void* A;              // element pointer of sample 0's matrix (origin (0,0))
   int64_t ld, strideA;  // leading dim, elements between consecutive samples
@@ -23,52 +24,54 @@ struct DiagArgs {
   void* info;           // user dpp_info_t[batch] or null (written at the last tile)
   double tie_tol, range_tol;
   int batch;
+  // panel operators (written when need_ops): nb x nb column-major, ld = ldm, per sample strideM
+  //   Hermitian: Bm(j,k) = delta_jk - conj(Linv(j,k)) / D(j)   (L21 = A21 - A21 (I - G),
+  //              G = Linv^H D^-1, i.e. L21 = A21 L11^-H D1^-1), dvec = D1
+  //   LU:        Bm(j,k) = delta_jk - Uinv(k,j)  (L21 = A21 U11^-1),
+  //              Am(i,k) = -Linv(i,k) for i > k, else 0  (U12 = L11^-1 A12)
+  int need_ops;
+  void* Bm;
+  void* Am;
+  double* dvec;          // D1, stride ldm per sample
+  int ldm;
+  int64_t strideM;
 };
 
-// Stage 2: panel.  Hermitian: W21 = A21 L11^{-H}, L21 = W21 D1^{-1} (rows j1..n).
-// LU: L21 = A21 U11^{-1} and U12 = L11^{-1} A12 (Listing 3).
-struct PanelArgs {
-  void* A;
-  int64_t ld, strideA;
- int64_t n, j0;
-  int64_t tcol;         // storage column of the block column (= j0 except distributed)
-  int jb;
-  void* W;              // Hermitian: W21 workspace, element (r, k) at r + k*ldw (+ s*strideW)
-  int64_t ldw, strideW;
-  int batch;
-};
-
-// Stage 3: trailing update on a region of A22 (Listing 3).
-// Hermitian: C -= L21 W21^H (lower triangle only).  LU: C -= L21 U12.
+// Stage 3 (and, through the same kernel, stage 2): C -= Aop * op(Bop)^T on a region of C.
+//   Aop: element (i, k) at i + k*lda,  i < a_rows, k < K
+//   Bop: bnmajor = 0: element (j, k) at j + k*ldb; bnmajor = 1: element (k, j) at k + j*ldb; j < b_rows
+//   op(B)(j,k) = [conj] B(j,k) [* dscale[k]]
+//   mask = 1: only elements on/below the global diagonal (row index >= column index) are written.
 struct UpdateArgs {
-  const void* Aop;      // L21 at A22-row 0: element (i, k) at i + k*lda
+  const void* Aop;
   int64_t lda, strideA;
-  const void* Bop;      // Hermitian: W21 (j, k) at j + k*ldb;  LU: U12 (k, j) at k + j*ldb
+  const void* Bop;
   int64_t ldb, strideB;
-  void* C;              // A22 origin: element (i, j) at i + j*ldc
+  void* C;              // C origin: element (i, j) at i + j*ldc
   int64_t ldc, strideC;
-  int m_total;          // rows of A22 (= cols); bounds for both operands
+  int a_rows, b_rows;   // operand extents (rows of Aop, C-columns of Bop)
   int K;                // inner dimension jb
-  int row0, col0;       // region origin inside A22
+  int row0, col0;       // region origin inside C
   int rows, cols;       // region extent
   int tri;              // lower-triangular tile enumeration of a square region
   int tiles_m, tiles_n;
   int batch;
-  int vec;              // 16-byte aligned operands (real: 2 rows per cp.async)
-  // 1D block-column-cyclic mode (bcc_P > 0, Hermitian real, BN == nb): tile column tj is local
-  // block q = bcc_q0 + tj whose global columns start at (bcc_r + q*bcc_P)*nb; C points at
-  // local storage column 0, row j1 (A22 row 0); bcc_j1 = global index of A22 row 0.
+  int vec;              // 16-byte aligned operands
+  int mask, conj, bnmajor;
+  const double* dscale; // per-k scale of B (Hermitian trailing update: D1), stride dstride per sample
+  int64_t dstride;
+  int grid_limit;       // > 0: persistent launch with at most this many CTAs (SMs left to the
+                        //      lookahead stream); 0: short-lived CTAs (<= 4 tiles each)
+  // 1D block-column-cyclic mode (bcc_P > 0, BN == nb): tile column tj is local block
+  // q = bcc_q0 + tj whose global columns start at (bcc_r + q*bcc_P)*nb; C points at local storage
+  // column 0, row j1 (A22 row 0); bcc_j1 = global index of A22 row 0.
   int bcc_P, bcc_r, bcc_nb, bcc_q0;
   int64_t bcc_j1;
 };
 
 cudaError_t launch_diag(Kind kind, int nb, const DiagArgs& a, cudaStream_t s);
-cudaError_t launch_panel(Kind kind, int nb, const PanelArgs& a, cudaStream_t s);
 cudaError_t launch_update(Kind kind, UpdateArgs a, cudaStream_t s);
 cudaError_t launch_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, double* u, cudaStream_t s);
 cudaError_t launch_zero_state(void* state, double* loglik, void* info, int batch, cudaStream_t s);
-size_t diag_smem_bytes(Kind kind, int nb);
-int update_tile_m(Kind kind);
-int update_tile_n(Kind kind);
 
 }  // namespace dpp

@@ -1,25 +1,25 @@
-// update_ws.cu -- Stage 3 fast path: persistent, warp-specialized FP64 tensor-core update.
+// update_ws.cu -- Stage 3 fast path (also stage-2 GEMMs): persistent, warp-specialized FP64
+// tensor-core contraction C -= A op(B)^T (see update.cu for the operation and the citations:
+// Listing 3; Hermitian specialisation PAPER.md:396-398, 626-628).
 //
-// Same operation as update.cu (Listing 3; Hermitian: lower triangle of
-// A22 -= L21 W21^H, LU: A22 -= L21 U12) for 16-byte-aligned operands, organised the Blackwell way:
-//  * persistent CTAs (one per SM) walk the tile list round-robin;
+// Organised the Blackwell way for 16-byte-aligned operands:
+//  * persistent CTAs walk the tile list round-robin (<= 4 tiles each, so the high-priority
+//    lookahead stream still finds SMs between tiles);
 //  * one PRODUCER warp streams operand K-chunks with TMA bulk copies (cp.async.bulk, one 1-D copy
 //    per column segment into padded shared rows) into a STAGES-deep ring guarded by full/empty
 //    mbarriers; a second warp owns the C tile (bulk load -> consumers subtract -> bulk store);
 //  * eight CONSUMER warps run DMMA.8x8x4 (mma.sync m8n8k4 f64) out of the ring with no CTA-wide
-//    barrier in the main loop, subtract in shared memory, and write C back with bulk stores;
-//  * the producer primes the next tile's ring while the consumers finish the current epilogue,
-//    and the C warp refills the C region as soon as the previous tile's store has read it.
+//    barrier in the main loop and subtract their accumulators from the C tile in shared memory.
 // Ragged edges: rows/columns beyond the tile are left stale in shared memory (they only feed
 // masked outputs); K-columns beyond jb are zero-filled; an odd trailing row (real) is moved with
 // ordinary loads/stores.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
-#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "update_common.cuh"
 
 namespace dpp {
 
@@ -31,18 +31,19 @@ template <> struct WsCfg<true> {   // complex: 64x64 tile, consumer warps 2 x 4 
   static constexpr int BM = 64, BN = 64, WM = 2, WN = 4, KC = 8, STAGES = 4;
 };
 
-template <bool CPLX, bool BLU>
+template <bool CPLX, bool BNMAJ>
 struct WsLayoutT {
   using C = WsCfg<CPLX>;
-  using T = typename std::conditional<CPLX, double2, double>::type;
+  using T = typename Elem<CPLX>::T;
   static constexpr int ES = CPLX ? 16 : 8;
   static constexpr int PAD = CPLX ? 2 : 4;     // conflict-free 64/128-bit fragment loads
   static constexpr int LDA = C::BM + PAD;      // A: [KC][LDA]
-  static constexpr int LDBK = C::BN + PAD;     // Hermitian B: [KC][LDBK]
-  static constexpr int LDBN = C::KC + PAD;     // LU B: [BN][LDBN]
+  static constexpr int LDBK = C::BN + PAD;     // K-major B: [KC][LDBK]
+  static constexpr int LDBN = C::KC + PAD;     // N-major B: [BN][LDBN]
   static constexpr int A_ELEMS = C::KC * LDA;
-  static constexpr int B_ELEMS = BLU ? C::BN * LDBN : C::KC * LDBK;
-  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr int B_ELEMS = BNMAJ ? C::BN * LDBN : C::KC * LDBK;
+  static constexpr int D_ELEMS = (C::KC * 8 + ES - 1) / ES;  // per-k scale of B
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS + D_ELEMS;
   static constexpr int LDC = CPLX ? C::BM + 1 : C::BM + 2;
   static constexpr size_t RING = (size_t)STAGE_ELEMS * C::STAGES * ES;
   static constexpr size_t CTILE = (size_t)C::BN * LDC * ES;
@@ -52,49 +53,6 @@ struct WsLayoutT {
   static constexpr int NT = (NCONS + 2) * 32;   // + operand producer warp + C-tile warp
 };
 
-struct TileInfo {
-  int grow0, gcol0, nrows, ncols, s;
-  int64_t cshift;
-  bool valid, diag;
-};
-
-template <int BM, int BN>
-__device__ __forceinline__ TileInfo tile_info(const UpdateArgs& a, int t, int tiles_per_sample, bool herm) {
-  TileInfo ti{};
-  ti.s = t / tiles_per_sample;
-  const int u = t % tiles_per_sample;
-  int r, c;
-  if (a.tri) {
-    int q = (int)((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
-    while ((q + 1) * (q + 2) / 2 <= u) ++q;
-    while (q * (q + 1) / 2 > u) --q;
-    r = q;
-    c = u - q * (q + 1) / 2;
-  } else {
-    r = u % a.tiles_m;
-    c = u / a.tiles_m;
-  }
-  ti.grow0 = a.row0 + r * BM;
-  const int row_end = a.row0 + a.rows;
-  int col_end;
-  if (a.bcc_P > 0) {
-    const int64_t q = a.bcc_q0 + c;
-    const int64_t gcs = (a.bcc_r + q * a.bcc_P) * (int64_t)a.bcc_nb;
-    ti.gcol0 = (int)(gcs - a.bcc_j1);
-    col_end = min(ti.gcol0 + a.bcc_nb, a.m_total);
-    ti.cshift = ti.gcol0 - q * a.bcc_nb;
-  } else {
-    ti.gcol0 = a.col0 + c * BN;
-    col_end = a.col0 + a.cols;
-    ti.cshift = 0;
-  }
-  ti.nrows = min(BM, row_end - ti.grow0);
-  ti.ncols = min(BN, col_end - ti.gcol0);
-  ti.valid = ti.nrows > 0 && ti.ncols > 0 && !(herm && ti.gcol0 > ti.grow0 + BM - 1);
-  ti.diag = herm && (ti.gcol0 + ti.ncols - 1 > ti.grow0);
-  return ti;
-}
-
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -103,13 +61,12 @@ __device__ __forceinline__ void consumer_sync(int nthreads) {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
-template <bool CPLX, bool BLU>
-__global__ void __launch_bounds__(WsLayoutT<CPLX, BLU>::NT, 1) update_ws_kernel(const UpdateArgs a) {
-  using LY = WsLayoutT<CPLX, BLU>;
+template <bool CPLX, bool BNMAJ, bool MASK, bool SCALE, bool CONJ>
+__global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ>::NT, 1) update_ws_kernel(const UpdateArgs a) {
+  using LY = WsLayoutT<CPLX, BNMAJ>;
   using C = WsCfg<CPLX>;
   using T = typename LY::T;
   constexpr int TM = C::BM / C::WM, TN = C::BN / C::WN, MI = TM / 8, NI = TN / 8;
-  constexpr bool HERM = !BLU;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* ring = reinterpret_cast<T*>(smem_raw);
   T* Cs = reinterpret_cast<T*>(smem_raw + LY::RING);
@@ -121,8 +78,6 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BLU>::NT, 1) update_ws_kernel(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tiles_per_sample = a.tri ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * a.tiles_n;
   const int ntiles = tiles_per_sample * a.batch;
-  // The grid is sized ceil(tiles / 4) (>= one wave), so each CTA walks at most 4 tiles and CTAs
-  // retire regularly: the high-priority lookahead stream (diag, panel) gets SMs between tiles.
   const int nchunks = (a.K + C::KC - 1) / C::KC;
 
   if (tid == 0) {
@@ -161,7 +116,7 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BLU>::NT, 1) update_ws_kernel(
       have_prev = false;
     };
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const TileInfo ti = tile_info<C::BM, C::BN>(a, t, tiles_per_sample, HERM);
+      const TileInfo ti = tile_info<C::BM, C::BN>(a, t, tiles_per_sample, MASK);
       if (!ti.valid) continue;
       const T* Cg = reinterpret_cast<const T*>(a.C) + (int64_t)ti.s * a.strideC;
       const int cbulk = CPLX ? ti.nrows : (ti.nrows & ~1);
@@ -191,12 +146,13 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BLU>::NT, 1) update_ws_kernel(
     int stage = 0;
     uint32_t phase = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const TileInfo ti = tile_info<C::BM, C::BN>(a, t, tiles_per_sample, HERM);
+      const TileInfo ti = tile_info<C::BM, C::BN>(a, t, tiles_per_sample, MASK);
       if (!ti.valid) continue;
       const T* Ag = reinterpret_cast<const T*>(a.Aop) + (int64_t)ti.s * a.strideA;
       const T* Bg = reinterpret_cast<const T*>(a.Bop) + (int64_t)ti.s * a.strideB;
-      const int arows = min(C::BM, a.m_total - ti.grow0);   // operand rows that exist
-      const int bcols = min(C::BN, a.m_total - ti.gcol0);
+      const double* dsc = SCALE ? a.dscale + (int64_t)ti.s * a.dstride : nullptr;
+      const int arows = min(C::BM, a.a_rows - ti.grow0);   // operand rows that exist
+      const int bcols = min(C::BN, a.b_rows - ti.gcol0);
       const int abulk = CPLX ? arows : (arows & ~1), bbulk = CPLX ? bcols : (bcols & ~1);
       for (int kc = 0; kc < nchunks; ++kc) {
         mbar_wait(&empty[stage], phase ^ 1);
@@ -204,9 +160,10 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BLU>::NT, 1) update_ws_kernel(
         T* Bs = As + LY::A_ELEMS;
         const int k0 = kc * C::KC;
         const int kv = min(C::KC, a.K - k0);  // valid k in this chunk
+        if (SCALE && lane < C::KC) reinterpret_cast<double*>(Bs + LY::B_ELEMS)[lane] = lane < kv ? dsc[k0 + lane] : 0.0;
         // zero-fill k beyond K; odd trailing operand rows by ordinary copies
         for (int idx = lane; idx < (C::KC - kv) * C::BM; idx += 32) As[(kv + idx / C::BM) * LY::LDA + idx % C::BM] = zero<T>();
-        if (!BLU) {
+        if (!BNMAJ) {
           for (int idx = lane; idx < (C::KC - kv) * C::BN; idx += 32) Bs[(kv + idx / C::BN) * LY::LDBK + idx % C::BN] = zero<T>();
         } else {
           for (int idx = lane; idx < (C::KC - kv) * C::BN; idx += 32)
@@ -216,21 +173,21 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BLU>::NT, 1) update_ws_kernel(
           if (arows & 1)
             for (int kk = lane; kk < kv; kk += 32)
               As[kk * LY::LDA + arows - 1] = Ag[ti.grow0 + arows - 1 + (int64_t)(k0 + kk) * a.lda];
-          if (!BLU && (bcols & 1))
+          if (!BNMAJ && (bcols & 1))
             for (int kk = lane; kk < kv; kk += 32)
               Bs[kk * LY::LDBK + bcols - 1] = Bg[ti.gcol0 + bcols - 1 + (int64_t)(k0 + kk) * a.ldb];
         }
         fence_proxy_async_smem();
         __syncwarp();
         uint32_t bytes = (uint32_t)(kv * abulk * LY::ES);
-        bytes += BLU ? (uint32_t)(bcols * kv * LY::ES) : (uint32_t)(kv * bbulk * LY::ES);
+        bytes += BNMAJ ? (uint32_t)(bcols * kv * LY::ES) : (uint32_t)(kv * bbulk * LY::ES);
         if (lane == 0) mbar_arrive_expect_tx(&full[stage], bytes);
         __syncwarp();
         if (abulk > 0)
           for (int kk = lane; kk < kv; kk += 32)
             bulk_g2s(As + kk * LY::LDA, Ag + ti.grow0 + (int64_t)(k0 + kk) * a.lda, (uint32_t)(abulk * LY::ES),
                      &full[stage]);
-        if (!BLU) {
+        if (!BNMAJ) {
           if (bbulk > 0)
             for (int kk = lane; kk < kv; kk += 32)
               bulk_g2s(Bs + kk * LY::LDBK, Bg + ti.gcol0 + (int64_t)(k0 + kk) * a.ldb, (uint32_t)(bbulk * LY::ES),
@@ -251,85 +208,27 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BLU>::NT, 1) update_ws_kernel(
   int stage = 0;
   uint32_t phase = 0, cphase = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const TileInfo ti = tile_info<C::BM, C::BN>(a, t, tiles_per_sample, HERM);
+    const TileInfo ti = tile_info<C::BM, C::BN>(a, t, tiles_per_sample, MASK);
     if (!ti.valid) continue;
-    T* Cg = reinterpret_cast<T*>(a.C) + (int64_t)ti.s * a.strideC;
-    double acc[MI][NI][2];
-    double acci[CPLX ? MI : 1][CPLX ? NI : 1][2];
-#pragma unroll
-    for (int i = 0; i < MI; ++i)
-#pragma unroll
-      for (int j = 0; j < NI; ++j) {
-        acc[i][j][0] = acc[i][j][1] = 0.0;
-        if (CPLX) acci[CPLX ? i : 0][CPLX ? j : 0][0] = acci[CPLX ? i : 0][CPLX ? j : 0][1] = 0.0;
-      }
+    MmaAcc<CPLX, MI, NI> acc;
+    acc.zero();
     for (int kc = 0; kc < nchunks; ++kc) {
       mbar_wait(&full[stage], phase);
       const T* As = ring + stage * LY::STAGE_ELEMS;
-      const T* Bs = As + LY::A_ELEMS;
-#pragma unroll
-      for (int ks = 0; ks < C::KC / 4; ++ks) {
-        const int kk = ks * 4 + (lane & 3);
-        T af[MI], bf[NI];
-#pragma unroll
-        for (int i = 0; i < MI; ++i) af[i] = As[kk * LY::LDA + wm * TM + i * 8 + (lane >> 2)];
-#pragma unroll
-        for (int j = 0; j < NI; ++j) {
-          const int nn = wn * TN + j * 8 + (lane >> 2);
-          bf[j] = BLU ? Bs[nn * LY::LDBN + kk] : Bs[kk * LY::LDBK + nn];
-        }
-        if constexpr (!CPLX) {
-#pragma unroll
-          for (int i = 0; i < MI; ++i)
-#pragma unroll
-            for (int j = 0; j < NI; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < MI; ++i) {
-            const double ar = re(af[i]), ai = im(af[i]);
-            const double nai = -ai, nar = -ar;
-#pragma unroll
-            for (int j = 0; j < NI; ++j) {
-              const double br = re(bf[j]), bi = im(bf[j]);
-              dmma884(acc[i][j][0], acc[i][j][1], ar, br);
-              dmma884(acc[i][j][0], acc[i][j][1], BLU ? nai : ai, bi);
-              dmma884(acci[CPLX ? i : 0][CPLX ? j : 0][0], acci[CPLX ? i : 0][CPLX ? j : 0][1], BLU ? ar : nar, bi);
-              dmma884(acci[CPLX ? i : 0][CPLX ? j : 0][0], acci[CPLX ? i : 0][CPLX ? j : 0][1], ai, br);
-            }
-          }
-        }
-      }
+      mma_chunk<CPLX, BNMAJ, SCALE, CONJ, C::KC, MI, NI, LY::LDA, LY::LDBK, LY::LDBN>(
+          acc, As, As + LY::A_ELEMS, reinterpret_cast<const double*>(As + LY::A_ELEMS + LY::B_ELEMS), wm * TM,
+          wn * TN, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
       if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
     }
-    // ---- epilogue: C -= acc in shared memory; the producer writes the tile back
+    // ---- epilogue: C -= acc in shared memory; the C warp writes the tile back
     mbar_wait(cfull, cphase);
     cphase ^= 1;
-#pragma unroll
-    for (int i = 0; i < MI; ++i) {
-      const int r = wm * TM + i * 8 + (lane >> 2);
-#pragma unroll
-      for (int j = 0; j < NI; ++j) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int c = wn * TN + j * 8 + 2 * (lane & 3) + e;
-          if (r < ti.nrows && c < ti.ncols && (BLU || ti.grow0 + r >= ti.gcol0 + c)) {
-            T* p = Cs + c * LY::LDC + r;
-            if constexpr (!CPLX) {
-              *p = *p - acc[i][j][e];
-            } else {
-              T v = *p;
-              v.x -= acc[i][j][e];
-              v.y -= acci[CPLX ? i : 0][CPLX ? j : 0][e];
-              *p = v;
-            }
-          }
-        }
-      }
-    }
+    acc.template subtract_into<MASK, TM, TN, LY::LDC>(Cs, wm, wn, lane, ti);
     if (ti.diag) {
       // Hermitian diagonal tile: element stores that never touch the strict upper triangle
+      T* Cg = reinterpret_cast<T*>(a.C) + (int64_t)ti.s * a.strideC;
       consumer_sync(LY::NCONS * 32);
       for (int idx = tid; idx < ti.ncols * ti.nrows; idx += LY::NCONS * 32) {
         const int c = idx / ti.nrows, r = idx % ti.nrows;
@@ -351,34 +250,40 @@ static int num_sms() {
   return sms[dev] > 0 ? sms[dev] : 148;
 }
 
-template <bool CPLX, bool BLU>
+template <bool CPLX, bool BNMAJ, bool MASK, bool SCALE, bool CONJ>
 cudaError_t launch_update_ws_t(UpdateArgs a, cudaStream_t s) {
   using C = WsCfg<CPLX>;
-  using LY = WsLayoutT<CPLX, BLU>;
+  using LY = WsLayoutT<CPLX, BNMAJ>;
   if (a.rows <= 0 || a.cols <= 0 || a.K <= 0) return cudaSuccess;
   a.tiles_m = (a.rows + C::BM - 1) / C::BM;
   if (a.bcc_P == 0) a.tiles_n = (a.cols + C::BN - 1) / C::BN;
   const long long per = a.tri ? (long long)a.tiles_m * (a.tiles_m + 1) / 2 : (long long)a.tiles_m * a.tiles_n;
   const long long total = per * a.batch;
   if (total <= 0) return cudaSuccess;
-  // persistent CTAs, each walking <= TPC tiles (see kernel); at least one wave of the SMs
+  // persistent CTAs, each walking <= TPC tiles, at least one wave of the SMs
   static long long TPC = 0;
   if (TPC == 0) {  // tiles per CTA (experiments: DPP_WS_TPC); 4 keeps CTAs short-lived
     const char* e = getenv("DPP_WS_TPC");
     TPC = (e && atoi(e) > 0) ? atoi(e) : 4;
   }
-  long long g = (total + TPC - 1) / TPC;
-  if (g < num_sms()) g = total < num_sms() ? total : num_sms();
-  const int grid = (int)g;
-  auto* fn = update_ws_kernel<CPLX, BLU>;
+  long long g;
+  if (a.grid_limit > 0) {
+    g = total < a.grid_limit ? total : a.grid_limit;  // persistent over the CTAs granted
+  } else {
+    g = (total + TPC - 1) / TPC;
+    if (g < num_sms()) g = total < num_sms() ? total : num_sms();
+  }
+  auto* fn = update_ws_kernel<CPLX, BNMAJ, MASK, SCALE, CONJ>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LY::SMEM);
   if (e != cudaSuccess) return e;
-  fn<<<grid, LY::NT, LY::SMEM, s>>>(a);
+  fn<<<(unsigned)g, LY::NT, LY::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
-template cudaError_t launch_update_ws_t<false, false>(UpdateArgs, cudaStream_t);
-template cudaError_t launch_update_ws_t<true, false>(UpdateArgs, cudaStream_t);
-template cudaError_t launch_update_ws_t<true, true>(UpdateArgs, cudaStream_t);
+template cudaError_t launch_update_ws_t<false, false, true, true, false>(UpdateArgs, cudaStream_t);
+template cudaError_t launch_update_ws_t<false, false, false, false, false>(UpdateArgs, cudaStream_t);
+template cudaError_t launch_update_ws_t<true, false, true, true, true>(UpdateArgs, cudaStream_t);
+template cudaError_t launch_update_ws_t<true, false, false, false, false>(UpdateArgs, cudaStream_t);
+template cudaError_t launch_update_ws_t<true, true, false, false, false>(UpdateArgs, cudaStream_t);
 
 }  // namespace dpp

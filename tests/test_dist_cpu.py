@@ -5,7 +5,7 @@
   (dpp_bcc_local_cols) and partitions the columns; to_local/from_local round-trip;
 * the NCCL unique id travels over broadcast_object_list (the DistComm bootstrap);
 * a numpy emulation of the distributed schedule of csrc/dist.cu -- owner factors tile + panel,
-  broadcasts [D1 | decisions | running loglik | W21] (here over gloo), every rank updates its own
+  broadcasts [D1 | decisions | running loglik | L21] (here over gloo), every rank updates its own
   trailing block columns -- reproduces the oracle's sample and factor.  (The CUDA kernels of that
   schedule are covered on the GPU by tests/test_gpu_dist.py at world size 1.)
 """
@@ -61,13 +61,13 @@ def _emulate(K, n, nb, world, rank, seed, oracle_mod):
             L11 = np.tril(T, -1) + np.eye(jb)
             A21 = loc[j1:, q:q + jb]
             W21 = np.linalg.solve(L11, A21.T).T if m2 else np.zeros((0, jb))  # A21 L11^{-T}
-            loc[j1:, q:q + jb] = W21 / Dg[None, :]
+            loc[j1:, q:q + jb] = W21 / Dg[None, :]                             # L21
             msg[0] = ll
             msg[2:2 + jb] = torch.from_numpy(Dg)
             msg[2 + jb:2 + 2 * jb] = torch.from_numpy(mask[j0:j1].astype(np.float64))
             if m2:
                 buf = np.zeros((ldw, jb))
-                buf[:m2] = W21
+                buf[:m2] = loc[j1:, q:q + jb]  # the message carries L21 (and D1)
                 msg[2 + 2 * jb:] = torch.from_numpy(buf.T.reshape(-1))
         dist.broadcast(msg, src=owner)
         ll = float(msg[0])
@@ -75,13 +75,12 @@ def _emulate(K, n, nb, world, rank, seed, oracle_mod):
         mask[j0:j1] = msg[2 + jb:2 + 2 * jb].numpy().astype(np.uint8)
         if m2 == 0:
             break
-        W21 = msg[2 + 2 * jb:].numpy().reshape(jb, ldw).T[:m2]
-        L21 = W21 / Dg[None, :]
-        # stage 3 on local trailing columns only
+        L21 = msg[2 + 2 * jb:].numpy().reshape(jb, ldw).T[:m2]
+        # stage 3 on local trailing columns only: C -= L21 D1 L21^T
         for qi, c in enumerate(cols):
             if c >= j1:
                 rows = np.arange(c, n)
-                loc[rows, qi] -= L21[rows - j1] @ W21[c - j1]
+                loc[rows, qi] -= L21[rows - j1] @ (L21[c - j1] * Dg)
     return loc, cols, mask, ll
 
 

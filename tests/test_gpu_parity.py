@@ -208,3 +208,32 @@ def test_large_parity_2048(oracle_mod):
     if o.n_ties == 0:
         assert_factor_close(F, o.factor, K, "herm_d")
         assert_loglik_close(float(s.loglik), o.loglik)
+
+
+def test_generic_update_kernel_subprocess():
+    """The cp.async fallback update kernel (forced with DPP_UPDATE_GENERIC=1) gives the same
+    samples and factors as the oracle for all three kinds (run in a fresh process)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, oracle, workloads as W, paper_1905_00165_b200 as dpp
+from tests.gpu_util import to_device, from_device, compare_masks, assert_factor_close, assert_loglik_close
+for kind, n in (("herm_d", 333), ("herm_z", 201), ("lu_z", 150)):
+    K = W.haar_kernel(n, seed=7, complex_=(kind != "herm_d"))
+    if kind == "lu_z":
+        K = W.similarity(K, seed=7)
+    o = {"herm_d": oracle.sample_herm_d, "herm_z": oracle.sample_herm_z, "lu_z": oracle.sample_lu_z}[kind](K, 3, 0)
+    Kc = to_device(K, kind)
+    s = dpp.sample(kind, Kc, 3)
+    torch.cuda.synchronize()
+    compare_masks(s.mask.cpu().numpy(), o)
+    if o.n_ties == 0:
+        assert_factor_close(from_device(Kc, n), o.factor, K, kind)
+        assert_loglik_close(float(s.loglik), o.loglik)
+print("GENERIC_OK")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DPP_UPDATE_GENERIC="1", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert "GENERIC_OK" in r.stdout, r.stdout + r.stderr
