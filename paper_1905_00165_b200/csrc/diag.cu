@@ -40,6 +40,8 @@ __device__ __forceinline__ double2 madd(double2 c, double2 a, double2 b) {
   ry = fma(a.y, b.x, ry);
   return make_double2(rx, ry);
 }
+__device__ __forceinline__ double add(double a, double b) { return a + b; }
+__device__ __forceinline__ double2 add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double neg(double a) { return -a; }
 __device__ __forceinline__ double2 neg(double2 a) { return make_double2(-a.x, -a.y); }
 
@@ -78,24 +80,32 @@ __device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
     // T_q = sum_{K=J}^{I-1} L_{IK} X_{KJ}   for (I, J) = (d + q, q)
     for (int q = 0; q + d < nblk; ++q) {
       const int I = d + q, J = q;
-      T s = zero<T>();
+      T s0 = zero<T>(), s1 = zero<T>(), s2 = zero<T>(), s3 = zero<T>();  // 4 chains for ILP
       for (int K = J; K < I; ++K) {
         const T* Lblk = Lb + ((I * (I + 1) / 2 + K) << 8);
         const T* Xblk = Xb + ((K * (K + 1) / 2 + J) << 8);
 #pragma unroll
-        for (int k = 0; k < 16; ++k) s = madd(s, Lblk[r + (k << 4)], Xblk[k + (c << 4)]);
+        for (int k = 0; k < 16; k += 4) {
+          s0 = madd(s0, Lblk[r + (k << 4)], Xblk[k + (c << 4)]);
+          s1 = madd(s1, Lblk[r + ((k + 1) << 4)], Xblk[k + 1 + (c << 4)]);
+          s2 = madd(s2, Lblk[r + ((k + 2) << 4)], Xblk[k + 2 + (c << 4)]);
+          s3 = madd(s3, Lblk[r + ((k + 3) << 4)], Xblk[k + 3 + (c << 4)]);
+        }
       }
-      Tb[(q << 8) + r + (c << 4)] = s;
+      Tb[(q << 8) + r + (c << 4)] = add(add(s0, s1), add(s2, s3));
     }
     __syncthreads();
     // X_{IJ} = -X_{II} T_q
     for (int q = 0; q + d < nblk; ++q) {
       const int I = d + q, J = q;
       const T* Xii = Xb + ((I * (I + 1) / 2 + I) << 8);
-      T s = zero<T>();
+      T s0 = zero<T>(), s1 = zero<T>();
 #pragma unroll
-      for (int l = 0; l < 16; ++l) s = madd(s, Xii[r + (l << 4)], Tb[(q << 8) + l + (c << 4)]);
-      Xb[((I * (I + 1) / 2 + J) << 8) + r + (c << 4)] = neg(s);
+      for (int l = 0; l < 16; l += 2) {
+        s0 = madd(s0, Xii[r + (l << 4)], Tb[(q << 8) + l + (c << 4)]);
+        s1 = madd(s1, Xii[r + ((l + 1) << 4)], Tb[(q << 8) + l + 1 + (c << 4)]);
+      }
+      Xb[((I * (I + 1) / 2 + J) << 8) + r + (c << 4)] = neg(add(s0, s1));
     }
   }
   __syncthreads();
@@ -105,8 +115,9 @@ template <typename T, bool HERM, int NB>
 __global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
   constexpr int TR = 16, TC = 16, RA = NB / TR, CB = NB / TC;
   constexpr int NBLK = NB / 16, NPB = NBLK * (NBLK + 1) / 2;  // packed 16x16 blocks
-  __shared__ T colbuf[2][NB];
-  __shared__ T rowbuf[HERM ? 1 : 2][HERM ? 1 : NB];
+  __shared__ T colbuf[2][2][NB];                    // [buffer][pivot of the pair][row], 0 on/above the pivot
+  __shared__ T rowbuf[HERM ? 1 : 2][2][HERM ? 1 : NB];  // LU: [buffer][pivot][column], 0 on/left of the pivot
+  __shared__ T pivbuf[2][2];                         // the pair's diagonal entries
   __shared__ T pv[NB], rv[NB];
   __shared__ double U[NB], dv[NB], imv[NB], lg[NB];
   __shared__ uint8_t keepv[NB];
@@ -137,74 +148,110 @@ __global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
     U[k] = uniform_u(a.seed, (uint64_t)(a.j0 + k), b);
     if (a.forced) keepv[k] = a.forced[(int64_t)s * a.n + a.j0 + k] != 0;
   }
-  // publish pivot column 0 (and row 0)
-  if (tc == 0) {
-#pragma unroll
-    for (int ia = 0; ia < RA; ++ia) colbuf[0][tr + TR * ia] = R[ia][0];
-  }
-  if (!HERM && tr == 0) {
-#pragma unroll
-    for (int ib = 0; ib < CB; ++ib) rowbuf[0][tc + TC * ib] = R[0][ib];
-  }
-  __syncthreads();
-
-  for (int k = 0; k < jb; ++k) {
-    const int cur = k & 1, nxt = cur ^ 1;
-    T p = colbuf[cur][k];
-    if (HERM) p = make_real(re(p), p);
-    const double d = re(p);
-    const bool keep = a.forced ? (keepv[k] != 0) : (U[k] <= d);
-    if (!keep) p = sub_one(p);  // Listing 1
-    const T r = recip(p);
-    if (tid == 0) {
-      pv[k] = p; rv[k] = r; dv[k] = d; imv[k] = im(colbuf[cur][k]);
-      if (!a.forced) keepv[k] = keep ? 1 : 0;
-    }
-    // multipliers: L(i,k) = w_i / p (line 438) for my rows, conj(w_l) or U(k,l) for my columns
-    T Li[RA], Wl[CB];
-#pragma unroll
-    for (int ia = 0; ia < RA; ++ia) {
-      const int i = tr + TR * ia;
-      Li[ia] = (i > k && i < jb) ? mul(colbuf[cur][i], r) : zero<T>();
-    }
+  // publish pivot columns kn, kn+1 (strictly below their diagonal, zero elsewhere), their
+  // diagonal entries and, LU, rows kn, kn+1 (strictly right of the diagonal).  Zero padding lets
+  // the step below run without per-row predicates.  The owning register is selected with
+  // compile-time indices only (a runtime index into R would demote the tile to local memory).
+  auto publish = [&](int kn, int buf) {
 #pragma unroll
     for (int ib = 0; ib < CB; ++ib) {
       const int l = tc + TC * ib;
-      Wl[ib] = (l > k && l < jb) ? (HERM ? cj(colbuf[cur][l]) : rowbuf[HERM ? 0 : cur][l]) : zero<T>();
+      if (l == kn || l == kn + 1) {
+#pragma unroll
+        for (int ia = 0; ia < RA; ++ia) {
+          const int i = tr + TR * ia;
+          const T v = R[ia][ib];
+          if (i == l) pivbuf[buf][l - kn] = v;
+          colbuf[buf][l - kn][i] = (i > l) ? v : zero<T>();
+        }
+      }
     }
-    // rank-1 update (line 439), branch-free
+    if (!HERM) {
+#pragma unroll
+      for (int ia = 0; ia < RA; ++ia) {
+        const int i = tr + TR * ia;
+        if (i == kn || i == kn + 1) {
+#pragma unroll
+          for (int ib = 0; ib < CB; ++ib) {
+            const int l = tc + TC * ib;
+            rowbuf[HERM ? 0 : buf][i - kn][l] = (l > i) ? R[ia][ib] : zero<T>();
+          }
+        }
+      }
+    }
+  };
+  publish(0, 0);
+  __syncthreads();
+
+  // Two pivots per barrier: every thread redoes the 2x2 micro-step of pivots (k, k+1) from the two
+  // published columns, derives both multiplier columns for its rows and both update rows for its
+  // columns, and applies the two rank-1 updates (line 439) in pivot order -- the same arithmetic,
+  // operation for operation, as two single-pivot steps.  Rows/columns at or above the pivot carry
+  // zeros (tile entries beyond jb are zero too), so only row/column k+1 needs a predicate.
+  for (int k = 0; k < jb; k += 2) {
+    const int cur = (k >> 1) & 1, nxt = cur ^ 1;
+    const bool two = k + 1 < jb;
+    const T* c0 = colbuf[cur][0];
+    const T* c1 = colbuf[cur][1];
+    // pivot k (line 437)
+    T p0 = pivbuf[cur][0];
+    if (HERM) p0 = make_real(re(p0), p0);
+    const double d0 = re(p0);
+    const bool keep0 = a.forced ? (keepv[k] != 0) : (U[k] <= d0);
+    if (!keep0) p0 = sub_one(p0);
+    const T r0 = recip(p0);
+    // pivot k+1 after the rank-1 update of pivot k
+    const T a10 = c0[k + 1];                                                     // A(k+1, k)
+    const T u01 = HERM ? cj(a10) : rowbuf[HERM ? 0 : cur][0][k + 1];             // conj(w) / U(k,k+1)
+    const T p1raw = fms(pivbuf[cur][1], mul(a10, r0), u01);
+    T p1 = p1raw;
+    if (HERM) p1 = make_real(re(p1), p1);
+    const double d1 = re(p1);
+    const bool keep1 = two && (a.forced ? (keepv[k + 1] != 0) : (U[k + 1] <= d1));
+    if (two && !keep1) p1 = sub_one(p1);
+    const T r1 = two ? recip(p1) : zero<T>();
+    if (tid == 0) {
+      pv[k] = p0; rv[k] = r0; dv[k] = d0; imv[k] = im(pivbuf[cur][0]);
+      if (!a.forced) keepv[k] = keep0 ? 1 : 0;
+      if (two) {
+        pv[k + 1] = p1; rv[k + 1] = r1; dv[k + 1] = d1; imv[k + 1] = im(p1raw);
+        if (!a.forced) keepv[k + 1] = keep1 ? 1 : 0;
+      }
+    }
+    // multipliers L(i,k), L(i,k+1) (line 438) for my rows
+    T L0[RA], L1[RA];
+#pragma unroll
+    for (int ia = 0; ia < RA; ++ia) {
+      const int i = tr + TR * ia;
+      const T l0 = mul(c0[i], r0);
+      L0[ia] = l0;
+      L1[ia] = (i == k + 1) ? zero<T>() : mul(fms(c1[i], l0, u01), r1);
+    }
+    // update rows for my columns: conj(w_l) or U(k, l), U(k+1, l)
+    T W0[CB], W1[CB];
+#pragma unroll
+    for (int ib = 0; ib < CB; ++ib) {
+      const int l = tc + TC * ib;
+      if (HERM) {
+        const T w0 = c0[l];
+        W0[ib] = cj(w0);
+        W1[ib] = (l == k + 1) ? zero<T>() : cj(fms(c1[l], mul(w0, r0), u01));
+      } else {
+        const T w0 = rowbuf[HERM ? 0 : cur][0][l];
+        W0[ib] = w0;
+        W1[ib] = (l == k + 1) ? zero<T>() : fms(rowbuf[HERM ? 0 : cur][1][l], mul(a10, r0), w0);
+      }
+    }
+    // two rank-1 updates (line 439), branch-free, pivot order
 #pragma unroll
     for (int ia = 0; ia < RA; ++ia)
 #pragma unroll
       for (int ib = 0; ib < CB; ++ib)
-        if (!HERM || ib <= ia) R[ia][ib] = fms(R[ia][ib], Li[ia], Wl[ib]);
-    // publish pivot column k+1 (and row k+1); the owning register is selected with compile-time
-    // indices only (a runtime index into R would demote the tile to local memory)
-    const int kn = k + 1;
-    if (kn < jb) {
-#pragma unroll
-      for (int ib = 0; ib < CB; ++ib) {
-        if (tc + TC * ib == kn) {
-#pragma unroll
-          for (int ia = 0; ia < RA; ++ia) {
-            const int i = tr + TR * ia;
-            if (i >= kn) colbuf[nxt][i] = R[ia][ib];
-          }
+        if (!HERM || ib <= ia) {
+          R[ia][ib] = fms(R[ia][ib], L0[ia], W0[ib]);
+          R[ia][ib] = fms(R[ia][ib], L1[ia], W1[ib]);
         }
-      }
-      if (!HERM) {
-#pragma unroll
-        for (int ia = 0; ia < RA; ++ia) {
-          if (tr + TR * ia == kn) {
-#pragma unroll
-            for (int ib = 0; ib < CB; ++ib) {
-              const int l = tc + TC * ib;
-              if (l > kn) rowbuf[HERM ? 0 : nxt][l] = R[ia][ib];
-            }
-          }
-        }
-      }
-    }
+    if (k + 2 < jb) publish(k + 2, nxt);
     __syncthreads();
   }
 
@@ -227,36 +274,58 @@ __global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
         if (!HERM && i <= l) Ub[bp(l, i)] = in ? v : (i == l ? one : zero<T>());  // U^T(l, i) = U(i, l)
       }
     }
-  // ---- decisions, likelihood terms and diagnostics, in parallel; summed in pivot order
+  // ---- decisions, likelihood terms and diagnostics: warp 0 reduces the flags with ballots and
+  //      shuffles; the log-likelihood terms are summed by one lane IN PIVOT ORDER
   for (int k = tid; k < jb; k += 256) {
     a.mask[(int64_t)s * a.n + a.j0 + k] = keepv[k];
     lg[k] = log(absval(pv[k]));
   }
   __syncthreads();
-  if (tid == 0) {
-    double ll = 0.0, minabs = INFINITY, maximag = 0.0;
+  if (tid < 32) {
+    const int lane = tid;
     int nkept = 0, nties = 0, firsttie = -1, noor = 0;
-    if (a.j0 > 0) {
-      ll = st->loglik; minabs = st->min_abs_pivot; maximag = st->max_abs_imag_pivot;
-      nkept = st->n_kept; nties = st->n_ties; firsttie = st->first_tie; noor = st->n_out_of_range;
+    double minabs = INFINITY, maximag = 0.0;
+    for (int k0 = 0; k0 < jb; k0 += 32) {
+      const int k = k0 + lane;
+      const bool in = k < jb;
+      const double d = in ? dv[k] : 0.0;
+      const bool tie = in && fabs(U[k] - d) <= a.tie_tol;
+      const unsigned tb = __ballot_sync(0xffffffffu, tie);
+      if (tb && firsttie < 0) firsttie = (int)(a.j0 + k0 + __ffs(tb) - 1);
+      nties += __popc(tb);
+      noor += __popc(__ballot_sync(0xffffffffu, in && (d < -a.range_tol || d > 1.0 + a.range_tol)));
+      nkept += __popc(__ballot_sync(0xffffffffu, in && keepv[k]));
+      if (in) {
+        minabs = fmin(minabs, absval(pv[k]));
+        if (!HERM) maximag = fmax(maximag, fabs(imv[k]));
+      }
     }
-    for (int k = 0; k < jb; ++k) {
-      const double d = dv[k], u = U[k];
-      if (fabs(u - d) <= a.tie_tol) { if (nties == 0) firsttie = (int)(a.j0 + k); ++nties; }
-      if (d < -a.range_tol || d > 1.0 + a.range_tol) ++noor;
-      if (!HERM) maximag = fmax(maximag, fabs(imv[k]));
-      ll += lg[k];
-      minabs = fmin(minabs, absval(pv[k]));
-      nkept += keepv[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      minabs = fmin(minabs, __shfl_xor_sync(0xffffffffu, minabs, o));
+      maximag = fmax(maximag, __shfl_xor_sync(0xffffffffu, maximag, o));
     }
-    st->loglik = ll; st->min_abs_pivot = minabs; st->max_abs_imag_pivot = maximag;
-    st->n_kept = nkept; st->n_ties = nties; st->first_tie = firsttie; st->n_out_of_range = noor;
-    if (a.j0 + jb == a.n && a.loglik) {
-      a.loglik[s] = ll;
-      if (a.info) {
-        dpp_info_t* inf = reinterpret_cast<dpp_info_t*>(a.info) + s;
-        inf->n_kept = nkept; inf->n_ties = nties; inf->first_tie = firsttie; inf->n_out_of_range = noor;
-        inf->min_abs_pivot = minabs; inf->max_abs_imag_pivot = maximag;
+    if (lane == 0) {
+      double ll = 0.0;
+      if (a.j0 > 0) {
+        ll = st->loglik;
+        minabs = fmin(minabs, st->min_abs_pivot);
+        maximag = fmax(maximag, st->max_abs_imag_pivot);
+        nkept += st->n_kept;
+        if (st->n_ties > 0) firsttie = st->first_tie;
+        nties += st->n_ties;
+        noor += st->n_out_of_range;
+      }
+      for (int k = 0; k < jb; ++k) ll += lg[k];
+      st->loglik = ll; st->min_abs_pivot = minabs; st->max_abs_imag_pivot = maximag;
+      st->n_kept = nkept; st->n_ties = nties; st->first_tie = firsttie; st->n_out_of_range = noor;
+      if (a.j0 + jb == a.n && a.loglik) {
+        a.loglik[s] = ll;
+        if (a.info) {
+          dpp_info_t* inf = reinterpret_cast<dpp_info_t*>(a.info) + s;
+          inf->n_kept = nkept; inf->n_ties = nties; inf->first_tie = firsttie; inf->n_out_of_range = noor;
+          inf->min_abs_pivot = minabs; inf->max_abs_imag_pivot = maximag;
+        }
       }
     }
   }
