@@ -137,7 +137,15 @@ def main():
     ap.add_argument("--n", type=int, default=N)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", default="c4", choices=["c4", "ust", "dist", "herm_z", "lu_z"],
+                    help="c4 (default, BASELINE configs[3]); ust: configs[1] batch of UST samples per GPU; "
+                         "dist: configs[4] 1D block-column-cyclic single sample over all ranks; "
+                         "herm_z / lu_z: complex128 Hermitian / non-Hermitian kernels (throughput of the "
+                         "complex paths)")
+    ap.add_argument("--batch", type=int, default=1024, help="ust: samples per GPU per step")
     args = ap.parse_args()
+    if args.workload != "c4" and args.impl == "ours":
+        return extra_workload(args)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -271,7 +279,7 @@ def main():
             "kept_last_sample": kept,
             "roofline": {"bound": "tensor", "kernel": "update_kernel<real,herm> (stage 3, trailing region)",
                          "achieved": round(achieved_tf, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": round(achieved_tf / FP64_PEAK_TFLOPS, 4), "traffic": None,
+                         "frac": round(achieved_tf / FP64_PEAK_TFLOPS, 4), "traffic": _traffic(),
                          "peak_source": PEAK_SOURCE,
                          "per_launch_flops": round(up["flops"] / max(up["launches"], 1)),
                          "avg_launch_ms": round(up["ms"] / max(up["launches"], 1), 4)},
@@ -288,6 +296,158 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _traffic():
+    """DRAM bytes per launch of the trailing-update kernel from the committed ncu capture
+    (profiles/r01_update_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum averaged over
+    the 126 (b) launches of one n=16384 sample); None if absent."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01_update_traffic.json")))
+        return {"bytes_per_launch": int(d["measured_bytes_per_launch"]),
+                "measured_over_algorithmic": d["ratio_measured_over_algorithmic"],
+                "source": "profiles/r01_update_traffic.json (ncu)"}
+    except Exception:
+        return None
+
+
+def _timed(fn, steps, warmup, world, dist):
+    import torch
+    for i in range(warmup):
+        fn(i)
+    torch.cuda.synchronize()
+    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    time.sleep(0.2)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(steps):
+        fn(warmup + i)
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), clocks
+
+
+def extra_workload(args):
+    """The other BASELINE.json configs as throughput runs (same JSON keys as the default line)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    import paper_1905_00165_b200 as dpp
+    import workloads as W
+    line = {"metric": METRIC, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "vs_baseline": None, "data": "synthetic", "impl": "ours"}
+    if args.workload == "ust":
+        n = 3120
+        K = W.ust_kernel(40, 40)
+        Kc = torch.from_numpy(np.ascontiguousarray(K.T)).cuda()
+        B = args.batch
+        opts = dpp.make_opts(nb=128, lookahead=1, batch_chunk=min(B, 256))
+        op = dpp.DPP_OP_HERM_D | dpp.DPP_OP_BATCHED
+        work = torch.empty(dpp.dpp_workspace_bytes(op, B, n, opts), dtype=torch.uint8, device="cuda")
+        mask = torch.empty((B, n), dtype=torch.uint8, device="cuda")
+        ll = torch.empty(B, dtype=torch.float64, device="cuda")
+
+        def step(i):
+            b0 = (rank * (args.warmup + args.steps) + i) * B
+            dpp.dpp_sample_herm_d_batched(B, n, Kc, n, 0, SEED, b0, mask, ll, None, opts, work)
+        ms, clocks = _timed(step, args.steps, args.warmup, world, dist)
+        ok = bool((mask.sum(dim=1) == 1599).all())
+        flops = model_flops(n) * B * args.steps * world
+        line.update(value=round(flops / (ms / 1e3) / 1e9, 2), ms_per_step=round(ms / args.steps, 3), scaling="weak",
+                    dtype="f64", samples_per_s=round(B * args.steps * world / (ms / 1e3), 2),
+                    config={"workload": f"BASELINE configs[1]: UST of the 40x40 grid (n=3120, rank 1599), {B} "
+                                        f"independent samples per GPU per step", "n": n, "global_batch": B * world,
+                            "nb": 128, "batch_chunk": min(B, 256), "seq_len": None,
+                            "parallelism": f"dp{world} (independent samples)"},
+                    all_samples_are_spanning_trees_with_1599_edges=ok,
+                    pct_fp64_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), 2), clocks=clocks)
+    elif args.workload in ("herm_z", "lu_z"):
+        n = args.n if args.n != N else 8192
+        Kc = W.haar_kernel_torch(n, seed=KSEED, spectrum="uniform", complex_=True)
+        if args.workload == "lu_z":  # D^-1 K D (Prop. 2), a non-Hermitian kernel with the same DPP
+            g = torch.Generator(device="cuda"); g.manual_seed(7)
+            dv = torch.exp(torch.rand(n, generator=g, device="cuda", dtype=torch.float64) - 0.5).to(torch.complex128)
+            Kc = (Kc * dv[None, :]) / dv[:, None]  # storage (l, i) = K(i, l): K' = D^-1 K D
+        opts = dpp.make_opts(nb=64, lookahead=1)
+        op = (dpp.DPP_OP_HERM_Z if args.workload == "herm_z" else dpp.DPP_OP_LU_Z) | dpp.DPP_OP_BATCHED
+        work = torch.empty(dpp.dpp_workspace_bytes(op, 1, n, opts), dtype=torch.uint8, device="cuda")
+        mask = torch.empty((1, n), dtype=torch.uint8, device="cuda")
+        ll = torch.empty(1, dtype=torch.float64, device="cuda")
+        fn = dpp.dpp_sample_herm_z_batched if args.workload == "herm_z" else dpp.dpp_sample_lu_z_batched
+
+        def step(i):
+            fn(1, n, Kc, n, 0, SEED, rank * 1000 + i, mask, ll, None, opts, work)
+        ms, clocks = _timed(step, args.steps, args.warmup, world, dist)
+        mult = 4.0 if args.workload == "herm_z" else 8.0  # complex LDL^H 4n^3/3, complex LU 8n^3/3 (R11)
+        flops = mult * n ** 3 / 3.0 * args.steps * world
+        line.update(value=round(flops / (ms / 1e3) / 1e9, 2), ms_per_step=round(ms / args.steps, 3), scaling="weak",
+                    dtype="c128", samples_per_s=round(args.steps * world / (ms / 1e3), 3),
+                    config={"workload": f"complex128 {'Hermitian' if args.workload == 'herm_z' else 'non-Hermitian (D^-1 K D)'} "
+                                        f"Haar kernel n={n}, one sample per GPU per step", "n": n, "nb": 64,
+                            "global_batch": world, "seq_len": None, "parallelism": f"dp{world}"},
+                    pct_fp64_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), 2), clocks=clocks)
+    else:  # dist
+        from paper_1905_00165_b200 import dist as D
+        n = args.n if args.n != N else 65536
+        nb = 128
+        g = torch.Generator(device="cuda"); g.manual_seed(KSEED)
+        # K = Q diag(lam) Q^T with Q from QR of a Gaussian (every rank builds the same Q, keeps its columns)
+        G = torch.randn(n, n, generator=g, device="cuda", dtype=torch.float64)
+        Q, R = torch.linalg.qr(G)
+        del G
+        Q = Q * torch.sign(torch.diagonal(R))[None, :]
+        del R
+        lam = torch.rand(n, generator=g, device="cuda", dtype=torch.float64)
+        cols = torch.as_tensor(D.bcc_columns(n, nb, world, rank), device="cuda")
+        loc0 = ((Q * lam[None, :]) @ Q[cols].T).T.contiguous()  # local columns, storage (q, i) = K(i, cols[q])
+        del Q
+        torch.cuda.empty_cache()
+        loc = torch.empty_like(loc0)
+        comm = dpp.dpp_comm_init(D.unique_id() if world == 1 else _shared_uid(dist, rank), world, rank)
+        work = torch.empty(dpp.dpp_dist_workspace_bytes(dpp.DPP_OP_HERM_D, n, world), dtype=torch.uint8, device="cuda")
+        mask = torch.empty(n, dtype=torch.uint8, device="cuda")
+        ll = torch.empty((), dtype=torch.float64, device="cuda")
+
+        def step(i):
+            loc.copy_(loc0)
+            dpp.dpp_sample_herm_d_dist(comm, n, loc, n, SEED + i, mask, ll, None, None, work)
+        ms, clocks = _timed(step, args.steps, args.warmup, world, dist)
+        dpp.dpp_comm_destroy(comm)
+        flops = model_flops(n) * args.steps
+        line.update(value=round(flops / (ms / 1e3) / 1e9, 2), ms_per_step=round(ms / args.steps, 3), scaling="strong",
+                    dtype="f64", samples_per_s=round(args.steps / (ms / 1e3), 3),
+                    config={"workload": f"BASELINE configs[4]: dense real-symmetric fp64 K=Q diag(lam) Q^T, lam~U(0,1), "
+                                        f"n={n}, ONE sample per step factored 1D block-column-cyclic over {world} GPU(s) "
+                                        f"(NCCL broadcast of each panel); step includes restoring the local columns",
+                            "n": n, "nb": nb, "global_batch": 1, "seq_len": None, "parallelism": f"bcc{world}"},
+                    pct_fp64_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), 2), clocks=clocks)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def _shared_uid(dist, rank):
+    from paper_1905_00165_b200 import dist as D
+    uid = [D.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    return uid[0]
 
 
 def reference_arm(args, n):

@@ -180,12 +180,12 @@ int device_sms() {
 // SMs to leave to the lookahead stream while the trailing update (b) of this step runs
 // persistently on the rest: minimise max(T1, T2) with T1 = diag latency + (tiles of the next
 // block column's update + next panel) / R, T2 = tiles of (b) / (SMs - R), in units of one tile.
-int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile) {
-  const double diag_tiles = 6.0;  // the diag tile ~ 6 update-tile times (measured ~110 us vs ~17 us)
-  const double ta = (double)((m2 + tile - 1) / tile) * batch;        // (a): next block column
-  const double tp = (double)((m2 - jn + tile - 1) / tile) * batch;   // next panel GEMM
-  const int64_t tb_side = (m2 - jn + tile - 1) / tile;
-  const double tb = (double)tb_side * (tb_side + 1) / 2 * batch;       // (b) lower-triangle tiles
+int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile, bool herm) {
+  const double diag_tiles = 5.0;  // the diag tile ~ 5 update-tile times (measured ~100 us vs ~20 us)
+  const double side = (double)((m2 + tile - 1) / tile), side_b = (double)((m2 - jn + tile - 1) / tile);
+  const double ta = (herm ? 1.0 : 2.0) * side * batch;     // (a): next block column (LU: + row)
+  const double tp = (herm ? 1.0 : 2.0) * side_b * batch;   // next panel GEMM(s)
+  const double tb = (herm ? side_b * (side_b + 1) / 2 : side_b * side_b) * batch;  // (b) tiles
   int best = 8;
   double best_t = 1e300;
   for (int R = 4; R <= sms / 2; R += 2) {
@@ -312,7 +312,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       UpdateArgs ub = u;
       ub.row0 = jn; ub.col0 = jn; ub.rows = (int)(m2 - jn); ub.cols = (int)(m2 - jn);
       ub.tri = herm;
-      if (herm && vec) ub.grid_limit = sms - reserve_sms(m2, jn, sms, batch, 128);
+      if (vec) ub.grid_limit = sms - reserve_sms(m2, jn, sms, batch, kind == HERM_D ? 128 : 64, herm);
       {
         ProfScope ps(3, region_flops(kind, jn, jn, m2 - jn, m2 - jn, jb) * batch, s2);
         CK(launch_update(kind, ub, s2));
