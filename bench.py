@@ -137,11 +137,12 @@ def main():
     ap.add_argument("--n", type=int, default=N)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="c4", choices=["c4", "ust", "dist", "herm_z", "lu_z"],
+    ap.add_argument("--workload", default="c4", choices=["c4", "ust", "dist", "dist_z", "herm_z", "lu_z", "aztec"],
                     help="c4 (default, BASELINE configs[3]); ust: configs[1] batch of UST samples per GPU; "
-                         "dist: configs[4] 1D block-column-cyclic single sample over all ranks; "
+                         "dist / dist_z: configs[4] 1D block-column-cyclic single sample over all ranks (real n=65536 / "
+                         "complex n=32768); "
                          "herm_z / lu_z: complex128 Hermitian / non-Hermitian kernels (throughput of the "
-                         "complex paths)")
+                         "complex paths); aztec: configs[2], order-80 Aztec diamond LU sampler")
     ap.add_argument("--batch", type=int, default=1024, help="ust: samples per GPU per step")
     args = ap.parse_args()
     if args.workload != "c4" and args.impl == "ours":
@@ -376,6 +377,40 @@ def extra_workload(args):
                             "parallelism": f"dp{world} (independent samples)"},
                     all_samples_are_spanning_trees_with_1599_edges=ok,
                     pct_fp64_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), 2), clocks=clocks)
+    elif args.workload == "aztec":
+        d = 80
+        n = 4 * d * d
+        Kc = W.aztec_kernel_balanced(d, device="cuda")  # balanced-gauge Kenyon kernel (reading R13)
+        torch.cuda.synchronize()
+        opts = dpp.make_opts(nb=64, lookahead=1)
+        op = dpp.DPP_OP_LU_Z | dpp.DPP_OP_BATCHED
+        work = torch.empty(dpp.dpp_workspace_bytes(op, 1, n, opts), dtype=torch.uint8, device="cuda")
+        mask = torch.empty((1, n), dtype=torch.uint8, device="cuda")
+        ll = torch.empty(1, dtype=torch.float64, device="cuda")
+
+        def step(i):
+            dpp.dpp_sample_lu_z_batched(1, n, Kc, n, 0, SEED, rank * 1000 + i, mask, ll, None, opts, work)
+        dpp.dpp_profile_begin()
+        ms, clocks = _timed(step, args.steps, args.warmup, world, dist)
+        prof = dpp.dpp_profile_end()
+        ok = W.is_aztec_tiling(d, mask[0].cpu().numpy())
+        flops = 8.0 * n ** 3 / 3.0 * args.steps * world  # complex LU, paper convention (R11)
+        up = prof["update_trailing"]
+        ach = up["flops"] / max(up["ms"], 1e-9) / 1e9
+        line.update(value=round(flops / (ms / 1e3) / 1e9, 2), ms_per_step=round(ms / args.steps, 3), scaling="weak",
+                    dtype="c128", samples_per_s=round(args.steps * world / (ms / 1e3), 4),
+                    config={"workload": f"BASELINE configs[2]: order-{d} Aztec diamond, n={n} complex128 non-Hermitian "
+                                        f"LU sampler on the balanced-gauge Kenyon kernel, one sample per GPU per step",
+                            "n": n, "nb": 64, "global_batch": world, "seq_len": None, "parallelism": f"dp{world}",
+                            "api": "dpp_sample_lu_z_batched(batch=1): K copied into the workspace each step"},
+                    last_sample_is_perfect_tiling=ok, last_loglik=float(ll[0]),
+                    loglik_closed_form=-d * (d + 1) / 2 * float(np.log(2.0)),
+                    roofline={"bound": "tensor", "kernel": "update_ws_kernel<cplx> trailing update (b)",
+                              "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                              "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": None},
+                    stages={k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                                "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3)} for k, v in prof.items()},
+                    pct_fp64_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), 2), clocks=clocks)
     elif args.workload in ("herm_z", "lu_z"):
         n = args.n if args.n != N else 8192
         Kc = W.haar_kernel_torch(n, seed=KSEED, spectrum="uniform", complex_=True)
@@ -401,40 +436,47 @@ def extra_workload(args):
                                         f"Haar kernel n={n}, one sample per GPU per step", "n": n, "nb": 64,
                             "global_batch": world, "seq_len": None, "parallelism": f"dp{world}"},
                     pct_fp64_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), 2), clocks=clocks)
-    else:  # dist
+    else:  # dist / dist_z: ONE sample factored 1D block-column-cyclic over all ranks
         from paper_1905_00165_b200 import dist as D
-        n = args.n if args.n != N else 65536
-        nb = 128
-        g = torch.Generator(device="cuda"); g.manual_seed(KSEED)
-        # K = Q diag(lam) Q^T with Q from QR of a Gaussian (every rank builds the same Q, keeps its columns)
-        G = torch.randn(n, n, generator=g, device="cuda", dtype=torch.float64)
-        Q, R = torch.linalg.qr(G)
-        del G
-        Q = Q * torch.sign(torch.diagonal(R))[None, :]
-        del R
-        lam = torch.rand(n, generator=g, device="cuda", dtype=torch.float64)
-        cols = torch.as_tensor(D.bcc_columns(n, nb, world, rank), device="cuda")
-        loc0 = ((Q * lam[None, :]) @ Q[cols].T).T.contiguous()  # local columns, storage (q, i) = K(i, cols[q])
-        del Q
+        cplx = args.workload == "dist_z"
+        n = args.n if args.n != N else (32768 if cplx else 65536)
+        nb = 64 if cplx else 128
+        # K = Q diag(lam) Q^H, lam ~ U(0,1), Q Haar-like; every rank builds the same Q, keeps its columns
+        loc0 = W.haar_kernel_bcc_torch(n, nb, world, rank, seed=KSEED, spectrum="uniform", complex_=cplx)
         torch.cuda.empty_cache()
         loc = torch.empty_like(loc0)
         comm = dpp.dpp_comm_init(D.unique_id() if world == 1 else _shared_uid(dist, rank), world, rank)
-        work = torch.empty(dpp.dpp_dist_workspace_bytes(dpp.DPP_OP_HERM_D, n, world), dtype=torch.uint8, device="cuda")
+        op = dpp.DPP_OP_HERM_Z if cplx else dpp.DPP_OP_HERM_D
+        work = torch.empty(dpp.dpp_dist_workspace_bytes(op, n, world), dtype=torch.uint8, device="cuda")
         mask = torch.empty(n, dtype=torch.uint8, device="cuda")
         ll = torch.empty((), dtype=torch.float64, device="cuda")
+        fn = dpp.dpp_sample_herm_z_dist if cplx else dpp.dpp_sample_herm_d_dist
+        copy_ms = []
 
         def step(i):
             loc.copy_(loc0)
-            dpp.dpp_sample_herm_d_dist(comm, n, loc, n, SEED + i, mask, ll, None, None, work)
+            fn(comm, n, loc, n, SEED + i, mask, ll, None, None, work)
         ms, clocks = _timed(step, args.steps, args.warmup, world, dist)
+        # the restore copy is inside the timed step; measure it alone to report the sampler's own rate
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            loc.copy_(loc0)
+        e1.record()
+        torch.cuda.synchronize()
+        copy_ms = e0.elapsed_time(e1)
         dpp.dpp_comm_destroy(comm)
-        flops = model_flops(n) * args.steps
+        flops = (4.0 if cplx else 1.0) * n ** 3 / 3.0 * args.steps  # complex LDL^H 4n^3/3 (R11)
         line.update(value=round(flops / (ms / 1e3) / 1e9, 2), ms_per_step=round(ms / args.steps, 3), scaling="strong",
-                    dtype="f64", samples_per_s=round(args.steps / (ms / 1e3), 3),
-                    config={"workload": f"BASELINE configs[4]: dense real-symmetric fp64 K=Q diag(lam) Q^T, lam~U(0,1), "
-                                        f"n={n}, ONE sample per step factored 1D block-column-cyclic over {world} GPU(s) "
-                                        f"(NCCL broadcast of each panel); step includes restoring the local columns",
+                    dtype="c128" if cplx else "f64", samples_per_s=round(args.steps / (ms / 1e3), 4),
+                    config={"workload": f"BASELINE configs[4]: dense {'complex Hermitian' if cplx else 'real-symmetric'} "
+                                        f"K=Q diag(lam) Q^H, lam~U(0,1), n={n}, ONE sample per step factored 1D "
+                                        f"block-column-cyclic over {world} GPU(s) (NCCL broadcast of each panel, "
+                                        f"depth-1 lookahead); step includes restoring the local columns",
                             "n": n, "nb": nb, "global_batch": 1, "seq_len": None, "parallelism": f"bcc{world}"},
+                    restore_copy_ms_per_step=round(copy_ms / args.steps, 3),
+                    value_excluding_restore=round(flops / ((ms - copy_ms) / 1e3) / 1e9, 2),
+                    kept=int(mask.sum()), loglik=float(ll),
                     pct_fp64_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), 2), clocks=clocks)
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -155,20 +155,37 @@ int dpp_philox_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, d
                         dpp_stream_t stream);
 
 /* ---- distributed 1D block-column-cyclic factorization (one sample) ---------
+ * SURVEY §8(e) mode 2; Listing 3/4 with the block
+ * columns dealt round-robin over the ranks.  Hermitian kernels only (real:
+ * nb = 128, complex: nb = 64 -- opts->nb must be 0 or that value).
  * Rank r of P owns block columns c = r, r+P, r+2P, ... (block width nb), stored
  * contiguously as an n x ncols_local column-major array K_local with leading
- * dimension ld_local >= n (ncols_local = dpp_bcc_local_cols(n, nb, P, r)).
+ * dimension ld_local >= n (ncols_local = dpp_bcc_local_cols(n, nb, P, r));
+ * only rows >= the block's first column are read/written (lower triangle).
  * Per block step the owner factors its diagonal tile and panel and broadcasts
- * [panel | pivots | decisions | partial loglik] with NCCL; every rank then
- * updates its local trailing columns.  On return every rank holds the full
- * mask (n bytes) and loglik; K_local holds the local columns of the factor.
- * comm wraps an ncclComm_t created from a 128-byte ncclUniqueId. */
+ * [partial loglik + counters | pivots D1 | decisions | panel L21] with NCCL
+ * (ncclBroadcast, root = owner); every rank then updates its local trailing
+ * columns.  With opts->lookahead != 0 (default) the owner of block k+1 updates
+ * that block column first and factors it while every rank's trailing update
+ * of step k runs (two prioritised streams per comm).  On return (stream-
+ * ordered) every rank holds the full mask (n bytes) and loglik; K_local holds
+ * the local columns of the factor.  Every rank must call with the same n,
+ * seed and opts.  comm wraps an ncclComm_t created from a 128-byte
+ * ncclUniqueId (all ranks pass the same id) on the CURRENT device; it owns two
+ * streams and its events.  Errors: DPP_EINVAL (bad sizes/nb/pointers),
+ * DPP_EWORKSPACE, DPP_ECUDA, DPP_ENCCL (a failed collective; the comm must
+ * then be destroyed).  Uniforms: global pivot j, sample index b = 0. */
 typedef struct dpp_comm_s* dpp_comm_t;
 int dpp_comm_init(const void* nccl_unique_id, int nranks, int rank, dpp_comm_t* comm);
 int dpp_comm_destroy(dpp_comm_t comm);
 int64_t dpp_bcc_local_cols(int64_t n, int32_t nb, int nranks, int rank);
+/* op: DPP_OP_HERM_D or DPP_OP_HERM_Z; 0 if unsupported */
 size_t dpp_dist_workspace_bytes(int op, int64_t n, int nranks, const dpp_opts_t* opts);
 int dpp_sample_herm_d_dist(dpp_comm_t comm, int64_t n, double* K_local, int64_t ld_local,
+                           uint64_t seed, uint8_t* mask, double* loglik, dpp_info_t* info,
+                           const dpp_opts_t* opts, void* work, size_t work_bytes,
+                           dpp_stream_t stream);
+int dpp_sample_herm_z_dist(dpp_comm_t comm, int64_t n, dpp_complex_t* K_local, int64_t ld_local,
                            uint64_t seed, uint8_t* mask, double* loglik, dpp_info_t* info,
                            const dpp_opts_t* opts, void* work, size_t work_bytes,
                            dpp_stream_t stream);

@@ -63,7 +63,8 @@ _sig("dpp_comm_init", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.POIN
 _sig("dpp_comm_destroy", ctypes.c_int, [_P])
 _sig("dpp_bcc_local_cols", _I64, [_I64, ctypes.c_int32, ctypes.c_int, ctypes.c_int])
 _sig("dpp_dist_workspace_bytes", _SZ, [ctypes.c_int, _I64, ctypes.c_int, _P])
-_sig("dpp_sample_herm_d_dist", ctypes.c_int, [_P, _I64, _P, _I64, _U64, _P, _P, _P, _P, _P, _SZ, _P])
+for _n in ("dpp_sample_herm_d_dist", "dpp_sample_herm_z_dist"):
+    _sig(_n, ctypes.c_int, [_P, _I64, _P, _I64, _U64, _P, _P, _P, _P, _P, _SZ, _P])
 class dpp_profile_t(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64 * 4), ("ms", ctypes.c_double * 4), ("flops", ctypes.c_double * 4)]
 
@@ -77,7 +78,7 @@ EXPORTS = ["dpp_workspace_bytes", "dpp_sample_herm_d", "dpp_sample_herm_z", "dpp
            "dpp_sample_herm_d_batched", "dpp_sample_herm_z_batched", "dpp_sample_lu_z_batched",
            "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host",
            "dpp_philox_uniforms", "dpp_comm_init", "dpp_comm_destroy", "dpp_bcc_local_cols",
-           "dpp_dist_workspace_bytes", "dpp_sample_herm_d_dist", "dpp_profile_begin", "dpp_profile_end",
+           "dpp_dist_workspace_bytes", "dpp_sample_herm_d_dist", "dpp_sample_herm_z_dist", "dpp_profile_begin", "dpp_profile_end",
            "dpp_strerror", "dpp_version"]
 
 
@@ -184,6 +185,13 @@ def dpp_comm_destroy(comm):
 def dpp_sample_herm_d_dist(comm, n, K_local, ld_local, seed, mask, loglik, info=None, opts=None, work=None,
                            work_bytes=None, stream=None):
     _check(_lib.dpp_sample_herm_d_dist(comm, n, _ptr(K_local), ld_local, seed, _ptr(mask), _ptr(loglik),
+                                       _ptr(info), _optp(opts), _ptr(work),
+                                       work_bytes if work_bytes is not None else work.numel(), _stream(stream)))
+
+
+def dpp_sample_herm_z_dist(comm, n, K_local, ld_local, seed, mask, loglik, info=None, opts=None, work=None,
+                           work_bytes=None, stream=None):
+    _check(_lib.dpp_sample_herm_z_dist(comm, n, _ptr(K_local), ld_local, seed, _ptr(mask), _ptr(loglik),
                                        _ptr(info), _optp(opts), _ptr(work),
                                        work_bytes if work_bytes is not None else work.numel(), _stream(stream)))
 

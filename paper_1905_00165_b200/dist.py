@@ -7,7 +7,7 @@
   ``to_local`` / ``from_local`` move between a full matrix and a rank's local storage, and
   ``DistComm`` wraps the library's NCCL communicator (``dpp_comm_init``), created from a unique id
   that rank 0 draws and ``torch.distributed.broadcast_object_list`` distributes.
-The sampling itself (diag / panel / broadcast / update) runs inside ``dpp_sample_herm_d_dist``.
+The sampling itself (diag / panel / broadcast / update) runs inside ``dpp_sample_herm_{d,z}_dist``.
 """
 from __future__ import annotations
 
@@ -54,14 +54,15 @@ def from_local(locals_: list, n: int, nb: int, world: int, like: torch.Tensor) -
     return full
 
 
-def message_bytes(n: int, nb: int, k: int) -> int:
-    """Bytes broadcast at block step k (mirrors csrc/dist.cu: header + W21 of the trailing rows)."""
+def message_bytes(n: int, nb: int, k: int, elem_bytes: int = 8) -> int:
+    """Bytes broadcast at block step k (mirrors csrc/dist.cu: header + L21 of the trailing rows;
+    elem_bytes 8 for real, 16 for complex Hermitian kernels)."""
     ldw = max(((n + 15) // 16) * 16, 16)
     header = 64 + 8 * nb + nb
     header = (header + 255) // 256 * 256
     j1 = min(n, (k + 1) * nb)
     jb = min(nb, n - k * nb)
-    return header + (ldw * jb * 8 if n - j1 > 0 else 0)
+    return header + (ldw * jb * elem_bytes if n - j1 > 0 else 0)
 
 
 class DistComm:

@@ -6,7 +6,8 @@
 * the NCCL unique id travels over broadcast_object_list (the DistComm bootstrap);
 * a numpy emulation of the distributed schedule of csrc/dist.cu -- owner factors tile + panel,
   broadcasts [D1 | decisions | running loglik | L21] (here over gloo), every rank updates its own
-  trailing block columns -- reproduces the oracle's sample and factor.  (The CUDA kernels of that
+  trailing block columns, in the lookahead order of csrc/dist.cu -- reproduces the oracle's sample
+  and factor for real and complex Hermitian kernels.  (The CUDA kernels of that
   schedule are covered on the GPU by tests/test_gpu_dist.py at world size 1.)
 """
 import os
@@ -28,60 +29,89 @@ def _free_port():
 
 
 def _emulate(K, n, nb, world, rank, seed, oracle_mod):
-    """Distributed blocked LDL^T DPP sampling with numpy compute and gloo broadcasts."""
+    """Distributed blocked LDL^H DPP sampling with numpy compute and gloo broadcasts, in the
+    lookahead order of csrc/dist.cu: with message k in hand, owner(k+1) updates block column k+1
+    with it, factors tile + panel k+1 and broadcasts message k+1; only then does every rank apply
+    step k to the rest of its trailing block columns.  Real or complex Hermitian K."""
     from paper_1905_00165_b200 import dist as D
+    cplx = np.iscomplexobj(K)
     cols = D.bcc_columns(n, nb, world, rank)
     Kc = torch.from_numpy(np.ascontiguousarray(K.T))            # column-major storage
     loc = D.to_local(Kc, n, nb, world, rank).numpy().T.copy()  # natural: loc[:, q] = K[:, cols[q]]
     mask = np.zeros(n, dtype=np.uint8)
-    ll = 0.0
+    ll = [0.0]
     nblk = (n + nb - 1) // nb
-    for k in range(nblk):
-        owner = D.owner_of_block(k, world)
+    ldw = max(((n + 15) // 16) * 16, 16)
+    msgs = {}
+
+    def span(k):
         j0, j1 = k * nb, min(n, (k + 1) * nb)
-        jb, m2 = j1 - j0, n - j1
-        ldw = max(((n + 15) // 16) * 16, 16)
-        msg = torch.zeros(2 + 2 * jb + ldw * jb, dtype=torch.float64)
+        return j0, j1, j1 - j0, n - j1
+
+    def factor(k):  # owner(k): stage 1 (Listing 1 on the tile, lower triangle) + stage 2, packed
+        j0, j1, jb, m2 = span(k)
+        q = np.searchsorted(cols, j0)
+        T = loc[j0:j1, q:q + jb]
+        for t in range(jb):
+            d = T[t, t].real
+            keep = oracle_mod.uniform(seed, j0 + t, 0) <= d
+            if not keep:
+                d -= 1.0
+            T[t, t] = d
+            mask[j0 + t] = keep
+            ll[0] += np.log(abs(d))
+            w = T[t + 1:, t].copy()
+            T[t + 1:, t] = w / d
+            T[t + 1:, t + 1:] -= np.tril(np.outer(T[t + 1:, t], w.conj()))
+        Dg = np.diag(T).real.copy()
+        L11 = np.tril(T, -1) + np.eye(jb)
+        A21 = loc[j1:, q:q + jb]
+        W21 = np.linalg.solve(L11, A21.conj().T).conj().T if m2 else np.zeros((0, jb))  # A21 L11^{-H}
+        loc[j1:, q:q + jb] = W21 / Dg[None, :]                                         # L21
+        buf = np.zeros((ldw, jb), dtype=loc.dtype)
+        buf[:m2] = loc[j1:, q:q + jb]
+        return [ll[0], Dg, mask[j0:j1].copy(), buf]
+
+    def exchange(k):  # ncclBroadcast(message k, root = owner(k)) -- here over gloo
+        j0, j1, jb, m2 = span(k)
+        owner = D.owner_of_block(k, world)
+        body = np.zeros(ldw * jb, dtype=loc.dtype)
+        msg = torch.zeros(2 + 2 * jb + (2 if cplx else 1) * ldw * jb, dtype=torch.float64)
         if rank == owner:
-            q = np.searchsorted(cols, j0)
-            T = loc[j0:j1, q:q + jb]
-            # stage 1: unblocked sampler on the tile (Listing 1, lower triangle)
-            for t in range(jb):
-                d = T[t, t]
-                keep = oracle_mod.uniform(seed, j0 + t, 0) <= d
-                if not keep:
-                    d -= 1.0
-                T[t, t] = d
-                mask[j0 + t] = keep
-                ll += np.log(abs(d))
-                w = T[t + 1:, t].copy()
-                T[t + 1:, t] = w / d
-                T[t + 1:, t + 1:] -= np.tril(np.outer(T[t + 1:, t], w))
-            Dg = np.diag(T).copy()
-            L11 = np.tril(T, -1) + np.eye(jb)
-            A21 = loc[j1:, q:q + jb]
-            W21 = np.linalg.solve(L11, A21.T).T if m2 else np.zeros((0, jb))  # A21 L11^{-T}
-            loc[j1:, q:q + jb] = W21 / Dg[None, :]                             # L21
-            msg[0] = ll
+            lk, Dg, mk, buf = msgs[k]
+            msg[0] = lk
             msg[2:2 + jb] = torch.from_numpy(Dg)
-            msg[2 + jb:2 + 2 * jb] = torch.from_numpy(mask[j0:j1].astype(np.float64))
-            if m2:
-                buf = np.zeros((ldw, jb))
-                buf[:m2] = loc[j1:, q:q + jb]  # the message carries L21 (and D1)
-                msg[2 + 2 * jb:] = torch.from_numpy(buf.T.reshape(-1))
+            msg[2 + jb:2 + 2 * jb] = torch.from_numpy(mk.astype(np.float64))
+            body = buf.T.reshape(-1)
+            msg[2 + 2 * jb:] = torch.from_numpy(body.view(np.float64))
         dist.broadcast(msg, src=owner)
-        ll = float(msg[0])
-        Dg = msg[2:2 + jb].numpy()
+        ll[0] = float(msg[0])
         mask[j0:j1] = msg[2 + jb:2 + 2 * jb].numpy().astype(np.uint8)
-        if m2 == 0:
-            break
-        L21 = msg[2 + 2 * jb:].numpy().reshape(jb, ldw).T[:m2]
-        # stage 3 on local trailing columns only: C -= L21 D1 L21^T
+        L21 = msg[2 + 2 * jb:].numpy().copy().view(loc.dtype).reshape(jb, ldw).T[:m2]
+        msgs[k] = (msg[2:2 + jb].numpy().copy(), L21)
+
+    def update(k, blocks):  # stage 3 of step k on the given local block columns: C -= L21 D1 L21^H
+        j0, j1, jb, m2 = span(k)
+        Dg, L21 = msgs[k]
         for qi, c in enumerate(cols):
-            if c >= j1:
+            if c // nb in blocks:
                 rows = np.arange(c, n)
-                loc[rows, qi] -= L21[rows - j1] @ (L21[c - j1] * Dg)
-    return loc, cols, mask, ll
+                loc[rows, qi] -= L21[rows - j1] @ (L21[c - j1].conj() * Dg)
+
+    if rank == D.owner_of_block(0, world):
+        msgs[0] = factor(0)
+    exchange(0)
+    for k in range(nblk):
+        if n - span(k)[1] == 0:
+            break
+        kn = k + 1
+        if rank == D.owner_of_block(kn, world):
+            update(k, {kn})           # lookahead: block column k+1 first
+            msgs[kn] = factor(kn)
+        exchange(kn)
+        rest = {c // nb for c in cols if c // nb > kn or (c // nb == kn and rank != D.owner_of_block(kn, world))}
+        update(k, rest)
+    return loc, cols, mask, ll[0]
 
 
 def _worker(rank, world, port, results):
@@ -114,25 +144,28 @@ def _worker(rank, world, port, results):
         ids = [None] * world
         dist.all_gather_object(ids, uid[0])
         out["uid_ok"] = len(uid[0]) == 128 and ids[0] == ids[1]
-        # (4) emulated distributed sampler vs the oracle
+        # (4) emulated distributed sampler (lookahead order) vs the oracle, real and complex
         n, nb, seed = 300, 32, 17
-        K = W.haar_kernel(n, seed=3)
-        loc, cols, mask, ll = _emulate(K.copy(), n, nb, world, rank, seed, oracle)
-        pieces = [None] * world
-        dist.all_gather_object(pieces, (cols.tolist(), loc[:, :len(cols)]))
-        F = np.zeros((n, n))
-        for cl, lc in pieces:
-            F[:, cl] = lc
-        o = oracle.sample_herm_d(K, seed, 0)
-        out["mask_ok"] = bool(np.array_equal(mask, o.mask)) and o.n_ties == 0
-        out["factor_err"] = float(np.max(np.abs(np.tril(F) - np.tril(o.factor))))
-        out["ll_err"] = abs(ll - o.loglik) / abs(o.loglik)
+        for cplx in (False, True):
+            K = W.haar_kernel(n, seed=3, complex_=cplx)
+            loc, cols, mask, ll = _emulate(K.copy(), n, nb, world, rank, seed, oracle)
+            pieces = [None] * world
+            dist.all_gather_object(pieces, (cols.tolist(), loc[:, :len(cols)]))
+            F = np.zeros((n, n), dtype=K.dtype)
+            for cl, lc in pieces:
+                F[:, cl] = lc
+            o = (oracle.sample_herm_z if cplx else oracle.sample_herm_d)(K, seed, 0)
+            tag = "z" if cplx else "d"
+            out["mask_ok_" + tag] = bool(np.array_equal(mask, o.mask)) and o.n_ties == 0
+            out["factor_err_" + tag] = float(np.max(np.abs(np.tril(F) - np.tril(o.factor))))
+            out["ll_err_" + tag] = abs(ll - o.loglik) / abs(o.loglik)
         # round trip of the local storage helpers
         Kc = torch.from_numpy(np.ascontiguousarray(K.T))
         locs = [None] * world
         dist.all_gather_object(locs, D.to_local(Kc, n, nb, world, rank))
         out["roundtrip_ok"] = bool(torch.equal(D.from_local(locs, n, nb, world, Kc), Kc))
         out["msg0"] = D.message_bytes(16384, 128, 0)
+        out["msg0z"] = D.message_bytes(32768, 64, 0, elem_bytes=16)
         results[rank] = out
     finally:
         dist.destroy_process_group()
@@ -147,8 +180,10 @@ def test_two_rank_gloo_host_logic():
     for r in range(world):
         res = results[r]
         assert res["shard_ok"] and res["layout_ok"] and res["uid_ok"] and res["roundtrip_ok"], res
-        assert res["mask_ok"], res
-        assert res["factor_err"] < 1e-10, res
-        assert res["ll_err"] < 1e-12, res
+        for tag in ("d", "z"):
+            assert res["mask_ok_" + tag], res
+            assert res["factor_err_" + tag] < 1e-10, res
+            assert res["ll_err_" + tag] < 1e-12, res
         # header (64 B state + 128 pivots + 128 decision bytes, 256-aligned) + W21 (ldw x nb)
         assert res["msg0"] == 1280 + 16384 * 128 * 8, res
+        assert res["msg0z"] == 768 + 32768 * 64 * 16, res

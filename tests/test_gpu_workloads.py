@@ -4,7 +4,8 @@
   reading-#12 3-sigma criteria; marginals vs diag(K).
 * config 1: UST of the 40x40 grid, batch of samples: spanning trees with the closed-form
   likelihood -ln tau = -1794.2382 (paper: exp(-1794.24)).
-* config 2 (scaled to d = 10 / 20): Aztec tilings with loglik -d(d+1)/2 ln 2.
+* config 2: Aztec tilings with loglik -d(d+1)/2 ln 2: d = 10 / 20 in
+  the plain gauge, d = 80 (n = 25600, the config itself) in the balanced gauge (reading R13).
 * config 3: n = 16384 Beta(1/2,1/2) kernel at the bench's launch configuration: prefix parity
   against the oracle on K[:m,:m] (loop invariant) + full-size invariants.
 """
@@ -95,8 +96,7 @@ def test_config1_ust_40x40_batch(oracle_mod):
 
 @pytest.mark.parametrize("d", [10, 20])
 def test_config2_aztec(oracle_mod, d):
-    """Config 2 scaled down: Aztec diamond tilings; d = 80 needs the balanced
-    gauge (next round)."""
+    """Config 2 scaled down: Aztec diamond tilings, plain gauge."""
     K = W.aztec_kernel(d)
     Kc = to_device(K, "lu_z")
     batch = 4
@@ -110,6 +110,34 @@ def test_config2_aztec(oracle_mod, d):
         assert round(lls[0], 4) == GOLD["aztec_d10_loglik"]["value"]
         o = oracle_mod.sample_lu_z(K, 0, 0)
         compare_masks(masks[0], o)
+
+
+def test_config2_aztec_d80_balanced(oracle_mod):
+    """Config 2 itself: order-80 Aztec diamond, n = 25600 complex128 non-Hermitian LU sampler on
+    the balanced-gauge Kenyon kernel (reading R13), in place at the default nb = 64 with
+    lookahead.  Every sample is a perfect tiling with 80*81 = 6480 dominoes and likelihood
+    exp(-3240 ln 2) (paper: e^{-2245.8}); the leading 1024 x 1024 block of the
+    factor and its decisions equal the oracle's sample of K[:1024, :1024] (prefix property)."""
+    d, m = 80, 1024
+    n = 4 * d * d
+    Kc = W.aztec_kernel_balanced(d, device="cuda")
+    assert Kc.shape == (n, n)
+    Kpre = Kc[:m, :m].cpu().numpy().T.copy()
+    s = dpp.sample("lu_z", Kc, 0)
+    torch.cuda.synchronize()
+    mask = s.mask.cpu().numpy()
+    assert int(mask.sum()) == GOLD["aztec_d80_dominoes"]["value"]
+    assert W.is_aztec_tiling(d, mask)
+    want = -d * (d + 1) / 2 * np.log(2.0)
+    ll = float(s.loglik)
+    assert abs(ll - want) <= 1e-9 * abs(want), (ll, want)
+    assert round(ll, 1) == GOLD["aztec_d80_loglik"]["value"]
+    info = s.info_dicts()[0]
+    assert info["n_kept"] == 6480 and info["n_ties"] == 0
+    o = oracle_mod.sample_lu_z(Kpre, 0, 0)
+    compare_masks(mask[:m], o)
+    if o.n_ties == 0:
+        assert_factor_close(Kc[:m, :m].cpu().numpy().T, o.factor, Kpre, "lu_z")
 
 
 def test_config3_n16384_prefix_parity(oracle_mod):

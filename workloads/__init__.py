@@ -108,6 +108,48 @@ def haar_kernel_torch(n: int, seed: int = 0, spectrum: str = "uniform", complex_
     return K.T.contiguous()
 
 
+def haar_kernel_bcc_torch(n: int, nb: int, world: int, rank: int, seed: int = 0, spectrum: str = "uniform",
+                          complex_: bool = False, device: str = "cuda", chunk: int = 4096):
+    """The same Haar recipe (G drawn first, then lam; Q from a Householder QR of G with the sign
+    fix) for the 1D block-column-cyclic layout at large n (configs[4]: n = 65536 real, 34 GB per
+    copy; n = 32768 complex): returns this rank's local storage L (ncols_local x n, C-contiguous)
+    with L[q, i] = K(i, cols[q]), cols = the rank's global columns in block-cyclic order.  Memory:
+    G and the QR factors are never alive together with K; K = (Q lam^1/2)(Q lam^1/2)^H is formed
+    chunk by chunk.  Every rank draws the same G and lam (same seed), so the ranks' columns
+    belong to one kernel."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    dt = torch.complex128 if complex_ else torch.float64
+    if complex_:
+        G = torch.complex(torch.randn(n, n, generator=g, device=device, dtype=torch.float64),
+                          torch.randn(n, n, generator=g, device=device, dtype=torch.float64)) / np.sqrt(2.0)
+    else:
+        G = torch.randn(n, n, generator=g, device=device, dtype=torch.float64)
+    a, tau = torch.geqrf(G)
+    del G
+    d = torch.diagonal(a).clone()
+    Q = torch.linalg.householder_product(a, tau)
+    del a, tau
+    if spectrum == "uniform":
+        lam = torch.rand(n, generator=g, device=device, dtype=torch.float64)
+    elif spectrum == "beta":
+        u = torch.rand(n, generator=g, device=device, dtype=torch.float64)
+        lam = torch.sin(0.5 * np.pi * u) ** 2
+    else:
+        raise ValueError(spectrum)
+    Q.mul_(((d / d.abs()) * lam.sqrt().to(dt))[None, :])   # Q <- Q phase(diag R) lam^1/2
+    nblk = (n + nb - 1) // nb
+    cols = [torch.arange(c * nb, min(n, (c + 1) * nb), device=device) for c in range(rank, nblk, world)]
+    cols = torch.cat(cols) if cols else torch.zeros(0, dtype=torch.long, device=device)
+    L = torch.empty((max(len(cols), 1), n), dtype=dt, device=device)
+    for c0 in range(0, len(cols), chunk):
+        rows = Q.index_select(0, cols[c0:c0 + chunk])          # Q(cols[q], :)
+        L[c0:c0 + len(rows)] = (rows.conj() if complex_ else rows) @ Q.T
+    del Q
+    return L
+
+
 # --------------------------------------------------------------------------- UST
 def grid_edges(rows: int, cols: int):
     """Edges of a rows x cols grid graph; vertex id = y*cols + x.  Horizontal
@@ -220,6 +262,112 @@ def aztec_kernel(d: int) -> np.ndarray:
     M = kv[:, None] * Kinv[widx][:, bidx]
     assert M.shape == (n, n)
     return np.asfortranarray(M)
+
+
+def _aztec_kast_torch(d: int, a_exp: dict, c_exp: dict, device: str):
+    """Gauged Kasteleyn matrix K'(b, w) = 2^{a_b} Kast(b, w) 2^{c_w} (exact: powers of two) and the
+    edge list; a_exp / c_exp map square -> integer exponent (missing squares: 0)."""
+    import torch
+    edges, blacks, whites = aztec_edges(d)
+    m = len(blacks)
+    a = torch.tensor([float(a_exp.get(s, 0)) for s in blacks], dtype=torch.float64)
+    c = torch.tensor([float(c_exp.get(s, 0)) for s in whites], dtype=torch.float64)
+    K = torch.zeros((m, m), dtype=torch.complex128)
+    bi = torch.tensor([e[0] for e in edges])
+    wi = torch.tensor([e[1] for e in edges])
+    kv = torch.tensor([1j if e[2] else 1.0 for e in edges], dtype=torch.complex128)
+    K[bi, wi] = kv * torch.exp2(a[bi] + c[wi]).to(torch.complex128)
+    return K.to(device), a.to(device), c.to(device), edges, blacks, whites
+
+
+def _osborne_bipartite(Kp, Ki, a, c, rounds: int = 40):
+    """Osborne balancing of Z = [[0, K'], [K'^{-1}, 0]] with power-of-two scalings, sweeping all
+    black indices, then all white ones (Z is bipartite, so a simultaneous sweep over one colour IS
+    the sequential Osborne sweep).  Scales Kp, Ki in place (exactly) and updates the exponents."""
+    import torch
+    for _ in range(rounds):
+        changed = False
+        # black b: row b of Z = K'(b, :), column b of Z = K'^{-1}(:, b)
+        r = Kp.abs().sum(dim=1)
+        cc = Ki.abs().sum(dim=0)
+        e = torch.round(0.5 * torch.log2(r / cc))
+        if bool((e != 0).any()):
+            changed = True
+            a -= e
+            Kp *= torch.exp2(-e).to(Kp.dtype)[:, None]
+            Ki *= torch.exp2(e).to(Ki.dtype)[None, :]
+        # white w: row w of Z = K'^{-1}(w, :), column w of Z = K'(:, w)
+        r = Ki.abs().sum(dim=1)
+        cc = Kp.abs().sum(dim=0)
+        e = torch.round(0.5 * torch.log2(r / cc))
+        if bool((e != 0).any()):
+            changed = True
+            c += e
+            Ki *= torch.exp2(-e).to(Ki.dtype)[:, None]
+            Kp *= torch.exp2(e).to(Kp.dtype)[None, :]
+        if not changed:
+            break
+
+
+def aztec_kernel_balanced(d: int, device: str = "cpu", d_start: int = 20, d_step: int = 5,
+                          passes: int = 2, storage: str = "colmajor", return_info: bool = False):
+    """Kenyon's kernel of the order-d Aztec diamond in an Osborne-balanced gauge (reading R13;
+    SURVEY.md Appendix A.5), built with torch on `device` (harness code, not the method).
+
+    M'_ij = K'(b_i, w_i) K'^{-1}(w_i, b_j) with K' = diag(2^a) Kast diag(2^c).  Then
+    M' = D M D^{-1} with D_ii = 2^{a(b_i)}, which defines the same DPP as Kenyon's M (Prop. 2,
+    PAPER.md:178-195) but stays well conditioned in fp64 at d = 80, where the plain gauge's
+    inverse is garbage (max|Kast^{-1}| ~ 7e21).  Exponents are found at d_start (plain gauge,
+    accurate there) and carried outward in steps of d_step: each new square takes the exponent of
+    the nearest same-colour square inward along the diagonal, then `passes` rounds of
+    (invert, balance) fix them up.
+
+    storage="colmajor" returns a torch tensor T (n x n, C-contiguous) with T[j, i] = M'[i, j]
+    (the sampler's column-major layout); "natural" returns M' itself."""
+    import torch
+    a_exp: dict = {}
+    c_exp: dict = {}
+    dd = min(d, d_start)
+    info = {"steps": []}
+    while True:
+        Kp, a, c, edges, blacks, whites = _aztec_kast_torch(dd, a_exp, c_exp, device)
+        for _ in range(passes):
+            Ki = torch.linalg.inv(Kp)
+            _osborne_bipartite(Kp, Ki, a, c)
+        Ki = torch.linalg.inv(Kp)
+        eye = torch.eye(Kp.shape[0], dtype=Kp.dtype, device=Kp.device)
+        res = float((Kp @ Ki - eye).abs().max())
+        info["steps"].append({"d": dd, "inverse_residual": res, "max_abs_Kinv": float(Ki.abs().max())})
+        a_exp = {s: int(v) for s, v in zip(blacks, a.cpu().tolist())}
+        c_exp = {s: int(v) for s, v in zip(whites, c.cpu().tolist())}
+        if dd == d:
+            break
+        dn = min(d, dd + d_step)
+        # seed the new squares from the nearest same-colour square inward along the diagonal
+        for x, y in aztec_squares(dn):
+            s = (x, y)
+            tgt = a_exp if (x + y) % 2 == 0 else c_exp
+            if s in tgt:
+                continue
+            px, py = x, y
+            while (px, py) not in tgt:  # each diagonal step lowers |x+1/2| + |y+1/2| by >= 1
+                px, py = px - (1 if px + 0.5 > 0 else -1), py - (1 if py + 0.5 > 0 else -1)
+            tgt[s] = tgt[(px, py)]
+        dd = dn
+    bidx = torch.tensor([e[0] for e in edges], device=Kp.device)
+    widx = torch.tensor([e[1] for e in edges], device=Kp.device)
+    kd = Kp[bidx, widx]                                   # K'(b_i, w_i)
+    if storage == "colmajor":
+        # T[j, i] = M'[i, j] = kd_i Ki[w_i, b_j] = kd_i (Ki^T)[b_j, w_i]
+        T = Ki.T.contiguous()[bidx]                       # n x m: rows b_j
+        T = T[:, widx] * kd[None, :]
+    else:
+        T = kd[:, None] * Ki[widx][:, bidx]
+    if return_info:
+        info["a_black"] = a.cpu().numpy()
+        info["edges"] = edges
+        return T, info
+    return T
 
 
 def is_aztec_tiling(d: int, kept: np.ndarray) -> bool:
