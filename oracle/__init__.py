@@ -18,6 +18,9 @@ Pinned by ``tests/test_oracle_*.py`` (-m "not gpu"):
   * factor:    L D L^H = K - 1_{Y^c}, L U = K - 1_{Y^c}; loglik = ln|det| (slogdet).
   * prefix:    decisions on K[:m,:m] = first m decisions on K (loop invariant,
                PAPER.md:402-405).
+  * greedy MAP: K = diag(p) closed form; every decision takes the
+               branch whose leading-principal-minor probability |det| is larger
+               (numpy det, brute force over both branches at every pivot).
 """
 from __future__ import annotations
 
@@ -84,6 +87,10 @@ def lib():
             f.restype = ctypes.c_int
             f.argtypes = [ctypes.c_int64, P, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, P,
                           ctypes.c_double, ctypes.c_double, P, P, P]
+        for name in ("oracle_map_herm_d", "oracle_map_herm_z", "oracle_map_lu_z"):
+            f = getattr(_lib, name)
+            f.restype = ctypes.c_int
+            f.argtypes = [ctypes.c_int64, P, ctypes.c_int64, P, ctypes.c_double, ctypes.c_double, P, P, P]
         _lib.oracle_uniform.restype = ctypes.c_double
         _lib.oracle_uniform.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64]
         _lib.oracle_philox4x32_10.restype = None
@@ -129,6 +136,29 @@ def sample(kind: int, K: np.ndarray, seed: int = 0, b: int = 0, forced=None,
           LU_Z: lib().oracle_sample_lu_z}[kind]
     rc = fn(n, A.ctypes.data, max(n, 1), seed, b, fptr, tie_tol, range_tol,
             mask.ctypes.data, ctypes.byref(ll), ctypes.byref(info))
+    if rc != 0:
+        raise RuntimeError(f"oracle returned {rc}")
+    return OracleResult(mask[:n].copy(), ll.value, A, info.n_kept, info.n_ties, info.first_tie,
+                        info.n_out_of_range, info.min_abs_pivot, info.max_abs_imag_pivot)
+
+
+def greedy_map(kind: int, K: np.ndarray, forced=None, tie_tol: float = TIE_TOL,
+               range_tol: float = RANGE_TOL) -> OracleResult:
+    """Greedy maximum-likelihood inference (reading R18): Listing 1 with each
+    Bernoulli draw replaced by the more probable branch, keep iff Re p >= 1/2."""
+    A = _as_colmajor(K, kind)
+    n = A.shape[0]
+    assert A.shape == (n, n)
+    mask = np.zeros(max(n, 1), dtype=np.uint8)
+    ll = ctypes.c_double(0.0)
+    info = _Info()
+    fptr = None
+    if forced is not None:
+        forced = np.ascontiguousarray(np.asarray(forced, dtype=np.uint8))
+        fptr = forced.ctypes.data
+    fn = {HERM_D: lib().oracle_map_herm_d, HERM_Z: lib().oracle_map_herm_z, LU_Z: lib().oracle_map_lu_z}[kind]
+    rc = fn(n, A.ctypes.data, max(n, 1), fptr, tie_tol, range_tol, mask.ctypes.data, ctypes.byref(ll),
+            ctypes.byref(info))
     if rc != 0:
         raise RuntimeError(f"oracle returned {rc}")
     return OracleResult(mask[:n].copy(), ll.value, A, info.n_kept, info.n_ties, info.first_tie,

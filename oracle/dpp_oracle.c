@@ -40,6 +40,11 @@
  *   R8  Ties: a pivot with |u - d| <= tie_tol is counted and the first such
  *       pivot index recorded.  If `forced` is non-NULL the decision for pivot j
  *       is forced[j] != 0 instead of the draw (replay, SPEC log_likelihood_of).
+ *   R18 Greedy MAP ("replacing the Bernoulli samples ... with
+ *       the maximum-likelihood result for each index inclusion"): the more
+ *       probable branch, keep iff Re p >= 1/2 (include at exactly 1/2); a tie
+ *       is |Re p - 1/2| <= tie_tol.  No uniform is drawn.  oracle_map_* below
+ *       are the same loops with this decision.
  *
  * Build: gcc -O2 -ffp-contract=off -std=c11 -shared -fPIC (single thread, no BLAS).
  */
@@ -102,17 +107,18 @@ static void info_init(oracle_info_t* info) {
   info->max_abs_imag_pivot = 0.0;
 }
 
-/* Decision at pivot j with real pivot value d (Listing 1; R1, R3, R8). */
+/* Decision at pivot j with real pivot value d (Listing 1; R1, R3, R8);
+   map != 0: the greedy maximum-likelihood decision of R18 instead of the draw. */
 static int decide(double d, int64_t j, uint64_t seed, uint64_t b, const uint8_t* forced,
-                  double tie_tol, double range_tol, oracle_info_t* info) {
-  double u = oracle_uniform(seed, (uint64_t)j, b);
+                  double tie_tol, double range_tol, oracle_info_t* info, int map) {
+  double u = map ? 0.5 : oracle_uniform(seed, (uint64_t)j, b);
   if (fabs(u - d) <= tie_tol) {
     if (info->n_ties == 0) info->first_tie = (int32_t)j;
     info->n_ties++;
   }
   if (d < -range_tol || d > 1.0 + range_tol) info->n_out_of_range++;
   if (forced) return forced[j] != 0;
-  return u <= d;
+  return map ? d >= 0.5 : u <= d;
 }
 
 /*
@@ -120,7 +126,7 @@ static int decide(double d, int64_t j, uint64_t seed, uint64_t b, const uint8_t*
  * On return A's strict lower triangle holds L (unit diagonal implicit), its
  * diagonal holds D, and L D L^T = K - 1_{Y^c}.  The upper triangle is untouched.
  */
-int oracle_sample_herm_d(int64_t n, double* A, int64_t ld, uint64_t seed, uint64_t b,
+static int run_herm_d(int map, int64_t n, double* A, int64_t ld, uint64_t seed, uint64_t b,
                          const uint8_t* forced, double tie_tol, double range_tol,
                          uint8_t* mask, double* loglik, oracle_info_t* info) {
   if (n < 0 || ld < (n > 1 ? n : 1)) return -1;
@@ -132,7 +138,7 @@ int oracle_sample_herm_d(int64_t n, double* A, int64_t ld, uint64_t seed, uint64
 #define A_(i, l) A[(size_t)(l) * (size_t)ld + (size_t)(i)]
   for (int64_t j = 0; j < n; ++j) {
     double d = A_(j, j);
-    int keep = decide(d, j, seed, b, forced, tie_tol, range_tol, &inf);
+    int keep = decide(d, j, seed, b, forced, tie_tol, range_tol, &inf, map);
     if (!keep) d -= 1.0;                      /* line 437: A_j -= 1 */
     A_(j, j) = d;
     mask[j] = (uint8_t)keep;
@@ -155,7 +161,7 @@ int oracle_sample_herm_d(int64_t n, double* A, int64_t ld, uint64_t seed, uint64
 }
 
 /* Complex Hermitian kernel, LDL^H specialisation (lower triangle, R5). */
-int oracle_sample_herm_z(int64_t n, double* Araw, int64_t ld, uint64_t seed, uint64_t b,
+static int run_herm_z(int map, int64_t n, double* Araw, int64_t ld, uint64_t seed, uint64_t b,
                          const uint8_t* forced, double tie_tol, double range_tol,
                          uint8_t* mask, double* loglik, oracle_info_t* info) {
   if (n < 0 || ld < (n > 1 ? n : 1)) return -1;
@@ -168,7 +174,7 @@ int oracle_sample_herm_z(int64_t n, double* Araw, int64_t ld, uint64_t seed, uin
 #define A_(i, l) A[(size_t)(l) * (size_t)ld + (size_t)(i)]
   for (int64_t j = 0; j < n; ++j) {
     double d = creal(A_(j, j));               /* R5: Im of a diagonal entry is 0 */
-    int keep = decide(d, j, seed, b, forced, tie_tol, range_tol, &inf);
+    int keep = decide(d, j, seed, b, forced, tie_tol, range_tol, &inf, map);
     if (!keep) d -= 1.0;
     A_(j, j) = d;                             /* stored with zero imaginary part */
     mask[j] = (uint8_t)keep;
@@ -191,7 +197,7 @@ int oracle_sample_herm_z(int64_t n, double* Araw, int64_t ld, uint64_t seed, uin
 }
 
 /* Complex non-Hermitian kernel: Listing 1 literally (unpivoted LU, R4). */
-int oracle_sample_lu_z(int64_t n, double* Araw, int64_t ld, uint64_t seed, uint64_t b,
+static int run_lu_z(int map, int64_t n, double* Araw, int64_t ld, uint64_t seed, uint64_t b,
                        const uint8_t* forced, double tie_tol, double range_tol,
                        uint8_t* mask, double* loglik, oracle_info_t* info) {
   if (n < 0 || ld < (n > 1 ? n : 1)) return -1;
@@ -203,7 +209,7 @@ int oracle_sample_lu_z(int64_t n, double* Araw, int64_t ld, uint64_t seed, uint6
   for (int64_t j = 0; j < n; ++j) {
     double complex p = A_(j, j);
     if (fabs(cimag(p)) > inf.max_abs_imag_pivot) inf.max_abs_imag_pivot = fabs(cimag(p));
-    int keep = decide(creal(p), j, seed, b, forced, tie_tol, range_tol, &inf);
+    int keep = decide(creal(p), j, seed, b, forced, tie_tol, range_tol, &inf, map);
     if (!keep) p -= 1.0;                      /* line 437 */
     A_(j, j) = p;
     mask[j] = (uint8_t)keep;
@@ -221,6 +227,22 @@ int oracle_sample_lu_z(int64_t n, double* Araw, int64_t ld, uint64_t seed, uint6
   if (info) *info = inf;
   return 0;
 }
+
+/* Exported entry points: sampling (Listing 1) and greedy MAP (R18). */
+#define ORACLE_EXPORT(name)                                                                     \
+  int oracle_sample_##name(int64_t n, double* A, int64_t ld, uint64_t seed, uint64_t b,         \
+                           const uint8_t* forced, double tie_tol, double range_tol,             \
+                           uint8_t* mask, double* loglik, oracle_info_t* info) {                \
+    return run_##name(0, n, A, ld, seed, b, forced, tie_tol, range_tol, mask, loglik, info);    \
+  }                                                                                             \
+  int oracle_map_##name(int64_t n, double* A, int64_t ld, const uint8_t* forced,               \
+                        double tie_tol, double range_tol, uint8_t* mask, double* loglik,        \
+                        oracle_info_t* info) {                                                  \
+    return run_##name(1, n, A, ld, 0, 0, forced, tie_tol, range_tol, mask, loglik, info);       \
+  }
+ORACLE_EXPORT(herm_d)
+ORACLE_EXPORT(herm_z)
+ORACLE_EXPORT(lu_z)
 
 /*
  * Many independent samples b = b0 .. b0+batch-1 of ONE kernel K (read-only),

@@ -303,3 +303,53 @@ def test_aztec_d10_paper_pin(oracle_mod):
         assert r.loglik == pytest.approx(-55 * np.log(2.0), rel=1e-10)
         assert round(r.loglik, 4) == GOLD["aztec_d10_loglik"]["value"]
         assert r.max_abs_imag_pivot < 1e-10
+
+
+# ------------------------------------------------------------------ greedy MAP
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_map_diag_closed_form(oracle_mod, kind):
+    """K = diag(p): the greedy decisions are p_j >= 1/2 (include at exactly 1/2, reading R18) and
+    the log-likelihood is sum ln max(p, 1 - p)."""
+    p = np.array([0.1, 0.5, 0.9, 0.49, 0.51, 0.0, 1.0, 0.25])
+    K = np.diag(p).astype(np.complex128 if kind else np.float64)
+    r = oracle_mod.greedy_map(kind, K)
+    assert np.array_equal(r.mask, (p >= 0.5).astype(np.uint8))
+    want = np.sum(np.log(np.where(p >= 0.5, p, 1 - p)))
+    assert abs(r.loglik - want) <= 1e-15
+    assert r.n_ties == 1 and r.first_tie == 1   # p = 1/2 exactly
+
+
+@pytest.mark.parametrize("kind,n", [(0, 10), (1, 9), (2, 9), (0, 60)])
+def test_map_is_greedy_on_leading_minors(oracle_mod, kind, n):
+    """At every pivot j the greedy result takes the more probable branch: with Y_j the decisions
+    on [0, j], P(Y cap [0,j] = Y_j) = |det((K - 1_{Y^c})[0:j+1, 0:j+1])| (the leading principal
+    minors of K - 1_{S^c}, PAPER.md:452-455 applied to the restriction, Def. 1), so the chosen
+    minor must be >= the one with decision j flipped.  Also loglik = ln|det(K - 1_{Y^c})|."""
+    K = W.haar_kernel(n, seed=100 + n, complex_=(kind != 0))
+    if kind == 2:
+        K = W.similarity(K, seed=n)
+    r = oracle_mod.greedy_map(kind, K)
+    keep = r.mask.astype(bool)
+    for j in range(n):
+        M = K[: j + 1, : j + 1].copy()
+        M[np.arange(j + 1), np.arange(j + 1)] -= (~keep[: j + 1]).astype(float)
+        alt = M.copy()
+        alt[j, j] += 1.0 if not keep[j] else -1.0
+        assert abs(np.linalg.det(M)) >= abs(np.linalg.det(alt)) * (1 - 1e-12), j
+    Kd = K.copy()
+    Kd[np.arange(n), np.arange(n)] -= (~keep).astype(float)
+    assert abs(r.loglik - np.linalg.slogdet(Kd)[1]) <= 1e-10 * max(1.0, abs(r.loglik))
+
+
+def test_map_deterministic_and_brute_force_likelihood(oracle_mod):
+    """The greedy result is deterministic and its likelihood is the brute-force probability
+    |det(K - 1_{Y^c})| of the returned set."""
+    n = 8
+    K = W.haar_kernel(n, seed=5)
+    r1 = oracle_mod.greedy_map(0, K)
+    r2 = oracle_mod.greedy_map(0, K)
+    assert np.array_equal(r1.mask, r2.mask) and r1.loglik == r2.loglik
+    from tests.stats_util import subset_probabilities
+    p = subset_probabilities(K)
+    idx = int(sum(int(v) << j for j, v in enumerate(r1.mask)))
+    assert abs(np.log(p[idx]) - r1.loglik) <= 1e-10 * abs(r1.loglik)
