@@ -112,6 +112,24 @@ int dpp_sample_lu_z(int64_t n, dpp_complex_t* K, int64_t ld, uint64_t seed, uint
                     double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
                     size_t work_bytes, dpp_stream_t stream);
 
+/* ---- greedy MAP inference (in place) ----------------------------------------
+ * "By replacing the Bernoulli samples of algorithm [Listing 1]
+ * with the maximum-likelihood result for each index inclusion, we arrive at an
+ * analogous (approximate) maximum-likelihood inference algorithm."  Same
+ * arguments, layout and factor as dpp_sample_* (no seed): item j is kept iff
+ * Re p_j >= 1/2 (include at exactly 1/2; reading R18); a tie is
+ * |Re p_j - 1/2| <= tie_tol.  loglik = sum_j ln|final pivot_j| is the
+ * log-probability of the returned set.  Deterministic. */
+int dpp_map_herm_d(int64_t n, double* K, int64_t ld, uint8_t* mask, double* loglik,
+                   dpp_info_t* info, const dpp_opts_t* opts, void* work, size_t work_bytes,
+                   dpp_stream_t stream);
+int dpp_map_herm_z(int64_t n, dpp_complex_t* K, int64_t ld, uint8_t* mask, double* loglik,
+                   dpp_info_t* info, const dpp_opts_t* opts, void* work, size_t work_bytes,
+                   dpp_stream_t stream);
+int dpp_map_lu_z(int64_t n, dpp_complex_t* K, int64_t ld, uint8_t* mask, double* loglik,
+                 dpp_info_t* info, const dpp_opts_t* opts, void* work, size_t work_bytes,
+                 dpp_stream_t stream);
+
 /* ---- batched independent samples b = b0 .. b0+batch-1 ----------------------
  * K is READ-ONLY: strideK == 0 -> one kernel shared by every sample; else
  * sample s reads the kernel at K + s*strideK (elements).  Each sample is

@@ -55,6 +55,8 @@ def _sig(name, res, args):
 _sig("dpp_workspace_bytes", _SZ, [ctypes.c_int, _I64, _I64, _P])
 for _n in ("dpp_sample_herm_d", "dpp_sample_herm_z", "dpp_sample_lu_z"):
     _sig(_n, ctypes.c_int, [_I64, _P, _I64, _U64, _P, _P, _P, _P, _P, _SZ, _P])
+for _n in ("dpp_map_herm_d", "dpp_map_herm_z", "dpp_map_lu_z"):
+    _sig(_n, ctypes.c_int, [_I64, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P])
 for _n in ("dpp_sample_herm_d_batched", "dpp_sample_herm_z_batched", "dpp_sample_lu_z_batched",
            "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host"):
     _sig(_n, ctypes.c_int, [_I64, _I64, _P, _I64, _I64, _U64, _U64, _P, _P, _P, _P, _P, _SZ, _P])
@@ -75,6 +77,7 @@ _sig("dpp_strerror", ctypes.c_char_p, [ctypes.c_int])
 _sig("dpp_version", ctypes.c_char_p, [])
 
 EXPORTS = ["dpp_workspace_bytes", "dpp_sample_herm_d", "dpp_sample_herm_z", "dpp_sample_lu_z",
+           "dpp_map_herm_d", "dpp_map_herm_z", "dpp_map_lu_z",
            "dpp_sample_herm_d_batched", "dpp_sample_herm_z_batched", "dpp_sample_lu_z_batched",
            "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host",
            "dpp_philox_uniforms", "dpp_comm_init", "dpp_comm_destroy", "dpp_bcc_local_cols",
@@ -137,6 +140,21 @@ def dpp_sample_herm_z(n, K, ld, seed, mask, loglik, info=None, opts=None, work=N
 def dpp_sample_lu_z(n, K, ld, seed, mask, loglik, info=None, opts=None, work=None, work_bytes=None, stream=None):
     _check(_lib.dpp_sample_lu_z(n, _ptr(K), ld, seed, _ptr(mask), _ptr(loglik), _ptr(info), _optp(opts),
                                 _ptr(work), work_bytes if work_bytes is not None else work.numel(), _stream(stream)))
+
+
+def _map(name):
+    fn = getattr(_lib, name)
+
+    def call(n, K, ld, mask, loglik, info=None, opts=None, work=None, work_bytes=None, stream=None):
+        _check(fn(n, _ptr(K), ld, _ptr(mask), _ptr(loglik), _ptr(info), _optp(opts), _ptr(work),
+                  work_bytes if work_bytes is not None else work.numel(), _stream(stream)))
+    call.__name__ = name
+    return call
+
+
+dpp_map_herm_d = _map("dpp_map_herm_d")
+dpp_map_herm_z = _map("dpp_map_herm_z")
+dpp_map_lu_z = _map("dpp_map_lu_z")
 
 
 def _batched(name):
@@ -259,6 +277,22 @@ def sample(kind: str, Kc: torch.Tensor, seed: int = 0, opts=None, work=None, str
     if work is None:
         work = workspace(kind, n, opts=opts, device=dev)
     _INPLACE[kind](n, Kc, ld, seed, mask, ll, info, opts, work, stream=stream)
+    return Sample(mask[:n], ll, info)
+
+
+_MAP = {"herm_d": dpp_map_herm_d, "herm_z": dpp_map_herm_z, "lu_z": dpp_map_lu_z}
+
+
+def greedy_map(kind: str, Kc: torch.Tensor, opts=None, work=None, stream=None) -> Sample:
+    """Greedy MAP inference; Kc (column-major storage) is OVERWRITTEN."""
+    n, ld = Kc.shape[0], Kc.shape[1]
+    dev = Kc.device
+    mask = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    ll = torch.empty((), dtype=torch.float64, device=dev)
+    info = torch.empty(INFO_BYTES, dtype=torch.uint8, device=dev)
+    if work is None:
+        work = workspace(kind, n, opts=opts, device=dev)
+    _MAP[kind](n, Kc, ld, mask, ll, info, opts, work, stream=stream)
     return Sample(mask[:n], ll, info)
 
 

@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
       R[ia][ib] = (i < jb && l < jb && (!HERM || i >= l)) ? A[(int64_t)l * a.ld + i] : zero<T>();
     }
   for (int k = tid; k < jb; k += 256) {
-    U[k] = uniform_u(a.seed, (uint64_t)(a.j0 + k), b);
+    // greedy MAP: the decision u <= d with u = 1/2 is "keep iff Re p >= 1/2" (reading R18)
+    U[k] = a.map ? 0.5 : uniform_u(a.seed, (uint64_t)(a.j0 + k), b);
     if (a.forced) keepv[k] = a.forced[(int64_t)s * a.n + a.j0 + k] != 0;
   }
   // publish pivot columns kn, kn+1 (strictly below their diagonal, zero elsewhere), their

@@ -209,7 +209,7 @@ UpdateArgs base_update(Kind kind, int batch, bool vec) {
 // Factors `batch` matrices A + s*strideA (in place), samples b0 + s.
 int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_t strideA, int batch,
                 uint64_t seed, uint64_t b0, uint8_t* mask, const uint8_t* forced, double* loglik,
-                dpp_info_t* info, char* work, const WsLayout& L, cudaStream_t caller) {
+                dpp_info_t* info, char* work, const WsLayout& L, cudaStream_t caller, bool map = false) {
   void* state = work + L.state_off;
   if (n == 0) { CK(launch_zero_state(state, loglik, info, batch, caller)); return DPP_OK; }
   DeviceStreams* ds = nullptr;
@@ -242,7 +242,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     DiagArgs d{};
     d.A = A; d.ld = ld; d.strideA = strideA; d.n = n; d.j0 = j0; d.tcol = j0; d.jb = jb; d.seed = seed; d.b0 = b0;
     d.mask = mask; d.forced = forced; d.state = state; d.loglik = loglik; d.info = info;
-    d.tie_tol = o.tie_tol; d.range_tol = o.range_tol; d.batch = batch;
+    d.tie_tol = o.tie_tol; d.range_tol = o.range_tol; d.batch = batch; d.map = map ? 1 : 0;
     d.need_ops = m2 > 0; d.Bm = Bm; d.Am = Am; d.dvec = dvec; d.ldm = nb; d.strideM = L.strideM;
     {
       const double fl = (herm ? 1.0 : 2.0) * jb * (double)jb * jb / 3.0 * cplx_mult(kind) * batch;
@@ -339,7 +339,8 @@ int validate(int64_t n, int64_t ld, const void* K, const uint8_t* mask, const do
 }
 
 int sample_inplace(Kind kind, int64_t n, void* K, int64_t ld, uint64_t seed, uint8_t* mask, double* loglik,
-                   dpp_info_t* info, const dpp_opts_t* opts, void* work, size_t work_bytes, cudaStream_t st) {
+                   dpp_info_t* info, const dpp_opts_t* opts, void* work, size_t work_bytes, cudaStream_t st,
+                   bool map = false) {
   Opts o;
   int rc = resolve_opts(kind, opts, &o);
   if (rc) return rc;
@@ -349,7 +350,7 @@ int sample_inplace(Kind kind, int64_t n, void* K, int64_t ld, uint64_t seed, uin
   if (!work || work_bytes < L.total || reinterpret_cast<uintptr_t>(work) % ALIGN) return DPP_EWORKSPACE;
   if (kind != HERM_D && reinterpret_cast<uintptr_t>(K) % 16) return DPP_EINVAL;
   return run_blocked(kind, o, n, K, ld, 0, 1, seed, 0, mask, o.forced, loglik, info, reinterpret_cast<char*>(work),
-                     L, st);
+                     L, st, map);
 }
 
 int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t ld, int64_t strideK, uint64_t seed,
@@ -431,6 +432,20 @@ int dpp_sample_herm_z(int64_t n, dpp_complex_t* K, int64_t ld, uint64_t seed, ui
 int dpp_sample_lu_z(int64_t n, dpp_complex_t* K, int64_t ld, uint64_t seed, uint8_t* mask, double* loglik,
                     dpp_info_t* info, const dpp_opts_t* opts, void* work, size_t work_bytes, dpp_stream_t stream) {
   return sample_inplace(LU_Z, n, K, ld, seed, mask, loglik, info, opts, work, work_bytes, (cudaStream_t)stream);
+}
+
+// greedy MAP inference: the same blocked factorization, decisions Re p >= 1/2
+int dpp_map_herm_d(int64_t n, double* K, int64_t ld, uint8_t* mask, double* loglik, dpp_info_t* info,
+                   const dpp_opts_t* opts, void* work, size_t work_bytes, dpp_stream_t stream) {
+  return sample_inplace(HERM_D, n, K, ld, 0, mask, loglik, info, opts, work, work_bytes, (cudaStream_t)stream, true);
+}
+int dpp_map_herm_z(int64_t n, dpp_complex_t* K, int64_t ld, uint8_t* mask, double* loglik, dpp_info_t* info,
+                   const dpp_opts_t* opts, void* work, size_t work_bytes, dpp_stream_t stream) {
+  return sample_inplace(HERM_Z, n, K, ld, 0, mask, loglik, info, opts, work, work_bytes, (cudaStream_t)stream, true);
+}
+int dpp_map_lu_z(int64_t n, dpp_complex_t* K, int64_t ld, uint8_t* mask, double* loglik, dpp_info_t* info,
+                 const dpp_opts_t* opts, void* work, size_t work_bytes, dpp_stream_t stream) {
+  return sample_inplace(LU_Z, n, K, ld, 0, mask, loglik, info, opts, work, work_bytes, (cudaStream_t)stream, true);
 }
 
 #define BATCHED(name, kind, T, host)                                                                          \

@@ -24,6 +24,7 @@ struct DiagArgs {
   void* info;           // user dpp_info_t[batch] or null (written at the last tile)
   double tie_tol, range_tol;
   int batch;
+  int map;              // greedy MAP (reading R18): u_j := 1/2, keep iff Re p >= 1/2
   // panel operators (written when need_ops): nb x nb column-major, ld = ldm, per sample strideM
   //   Hermitian: Bm(j,k) = delta_jk - conj(Linv(j,k)) / D(j)   (L21 = A21 - A21 (I - G),
   //              G = Linv^H D^-1, i.e. L21 = A21 L11^-H D1^-1), dvec = D1
