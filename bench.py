@@ -144,6 +144,7 @@ def main():
                          "herm_z / lu_z: complex128 Hermitian / non-Hermitian kernels (throughput of the "
                          "complex paths); aztec: configs[2], order-80 Aztec diamond LU sampler")
     ap.add_argument("--batch", type=int, default=1024, help="ust: samples per GPU per step")
+    ap.add_argument("--batch-chunk", type=int, default=256, help="ust: samples factored concurrently")
     args = ap.parse_args()
     if args.workload != "c4" and args.impl == "ours":
         return extra_workload(args)
@@ -280,7 +281,8 @@ def main():
             "kept_last_sample": kept,
             "roofline": {"bound": "tensor", "kernel": "update_kernel<real,herm> (stage 3, trailing region)",
                          "achieved": round(achieved_tf, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": round(achieved_tf / FP64_PEAK_TFLOPS, 4), "traffic": _traffic(),
+                         "frac": round(achieved_tf / FP64_PEAK_TFLOPS, 4),
+                         "traffic": (_traffic() or {}).get("bytes_per_launch"), "traffic_detail": _traffic(),
                          "peak_source": PEAK_SOURCE,
                          "per_launch_flops": round(up["flops"] / max(up["launches"], 1)),
                          "avg_launch_ms": round(up["ms"] / max(up["launches"], 1), 4)},
@@ -357,7 +359,7 @@ def extra_workload(args):
         K = W.ust_kernel(40, 40)
         Kc = torch.from_numpy(np.ascontiguousarray(K.T)).cuda()
         B = args.batch
-        opts = dpp.make_opts(nb=128, lookahead=1, batch_chunk=min(B, 256))
+        opts = dpp.make_opts(nb=128, lookahead=1, batch_chunk=min(B, args.batch_chunk))
         op = dpp.DPP_OP_HERM_D | dpp.DPP_OP_BATCHED
         work = torch.empty(dpp.dpp_workspace_bytes(op, B, n, opts), dtype=torch.uint8, device="cuda")
         mask = torch.empty((B, n), dtype=torch.uint8, device="cuda")
@@ -373,7 +375,7 @@ def extra_workload(args):
                     dtype="f64", samples_per_s=round(B * args.steps * world / (ms / 1e3), 2),
                     config={"workload": f"BASELINE configs[1]: UST of the 40x40 grid (n=3120, rank 1599), {B} "
                                         f"independent samples per GPU per step", "n": n, "global_batch": B * world,
-                            "nb": 128, "batch_chunk": min(B, 256), "seq_len": None,
+                            "nb": 128, "batch_chunk": min(B, args.batch_chunk), "seq_len": None,
                             "parallelism": f"dp{world} (independent samples)"},
                     all_samples_are_spanning_trees_with_1599_edges=ok,
                     pct_fp64_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), 2), clocks=clocks)

@@ -60,9 +60,10 @@ size_t esize(Kind k) { return k == HERM_D ? 8 : 16; }
 //   [SampleState x chunk]
 //   [panel operators: Bm (and Am for LU), nb x nb per sample]
 //   [D1 double buffer (Hermitian): 2 x chunk x nb doubles]
+//   [U12^T double buffer (LU): 2 x chunk x ldk x nb complex -- the row panel in K-major form]
 //   [K copies: chunk x ldk x n (batched / host)][host staging: mask, loglik, info (host)]
 struct WsLayout {
-  size_t state_off, bm_off, am_off, d_off, k_off, mask_off, ll_off, info_off, total;
+  size_t state_off, bm_off, am_off, d_off, ut_off, k_off, mask_off, ll_off, info_off, total;
   int64_t ldk, strideK, strideM;
 };
 
@@ -79,6 +80,8 @@ WsLayout layout(Kind kind, int64_t chunk, int64_t n, int nb, bool copies, bool h
   if (kind == LU_Z) off = align_up(off + (size_t)chunk * L.strideM * es);
   L.d_off = off;
   if (kind != LU_Z) off = align_up(off + 2 * (size_t)chunk * nb * 8);
+  L.ut_off = off;
+  if (kind == LU_Z) off = align_up(off + 2 * (size_t)chunk * (size_t)L.ldk * nb * es);
   L.k_off = off;
   if (copies) off = align_up(off + (size_t)chunk * (size_t)L.strideK * es);
   L.mask_off = off;
@@ -238,6 +241,9 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     const int jb = (int)std::min<int64_t>(nb, n - j0);
     const int64_t j1 = j0 + jb, m2 = n - j1;
     double* dvec = herm ? reinterpret_cast<double*>(work + L.d_off) + (size_t)(step & 1) * batch * nb : nullptr;
+    // LU: U12^T (m2 x jb, ld = ldk, K-major GEMM operand), double-buffered like D1
+    const int64_t strideU = L.ldk * nb;
+    char* UT = herm ? nullptr : work + L.ut_off + (size_t)(step & 1) * batch * strideU * es;
     // ---- stage 1
     DiagArgs d{};
     d.A = A; d.ld = ld; d.strideA = strideA; d.n = n; d.j0 = j0; d.tcol = j0; d.jb = jb; d.seed = seed; d.b0 = b0;
@@ -262,14 +268,18 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       p.row0 = 0; p.col0 = 0; p.rows = (int)m2; p.cols = jb;
       CK(launch_update(kind, p, s1));
       if (!herm) {
+        // U12 = L11^-1 A12 = A12 - Am A12 (Am = I - L11^-1), computed transposed so that every
+        // operand is K-major:  U12^T = A12^T - A12^T Am^T  in the U12^T buffer, then copied back.
+        char* A12 = Ab + (size_t)(j0 + j1 * ld) * es;
+        CK(launch_transpose_z(A12, ld, strideA, UT, L.ldk, strideU, jb, (int)m2, batch, s1));
         UpdateArgs q = base_update(kind, batch, vec);
-        q.Aop = Am; q.lda = nb; q.strideA = L.strideM;                             // I - L11^-1
-        q.Bop = Ab + (size_t)(j0 + j1 * ld) * es; q.ldb = ld; q.strideB = strideA;  // A12 (k, j)
-        q.bnmajor = 1;
-        q.C = Ab + (size_t)(j0 + j1 * ld) * es; q.ldc = ld; q.strideC = strideA;   // U12 in place
-        q.a_rows = jb; q.b_rows = (int)m2; q.K = jb;
-        q.row0 = 0; q.col0 = 0; q.rows = jb; q.cols = (int)m2;
+        q.Aop = UT; q.lda = L.ldk; q.strideA = strideU;                            // A12^T (j, k)
+        q.Bop = Am; q.ldb = nb; q.strideB = L.strideM;                             // Am (i, k)
+        q.C = UT; q.ldc = L.ldk; q.strideC = strideU;                              // U12^T in place
+        q.a_rows = (int)m2; q.b_rows = jb; q.K = jb;
+        q.row0 = 0; q.col0 = 0; q.rows = (int)m2; q.cols = jb;
         CK(launch_update(kind, q, s1));
+        CK(launch_transpose_z(UT, L.ldk, strideU, A12, ld, strideA, (int)m2, jb, batch, s1));  // U12 -> K
       }
     }
     // ---- stage 3 operands
@@ -279,7 +289,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       u.Bop = u.Aop; u.ldb = ld; u.strideB = strideA;  // L21, scaled by D1 (and conjugated) on load
       u.dscale = dvec; u.dstride = nb; u.mask = 1; u.conj = (kind == HERM_Z);
     } else {
-      u.Bop = Ab + (size_t)(j0 + j1 * ld) * es; u.ldb = ld; u.strideB = strideA; u.bnmajor = 1;  // U12
+      u.Bop = UT; u.ldb = L.ldk; u.strideB = strideU;  // U12^T (j, k), K-major
     }
     u.C = Ab + (size_t)(j1 + j1 * ld) * es; u.ldc = ld; u.strideC = strideA;
     u.a_rows = (int)m2; u.b_rows = (int)m2; u.K = jb;

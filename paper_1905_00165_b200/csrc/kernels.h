@@ -72,6 +72,10 @@ struct UpdateArgs {
 
 cudaError_t launch_diag(Kind kind, int nb, const DiagArgs& a, cudaStream_t s);
 cudaError_t launch_update(Kind kind, UpdateArgs a, cudaStream_t s);
+// dst(j, k) = src(k, j) for k < rows, j < cols (complex128), `batch` matrices at the given strides:
+// the LU row panel A12 / U12 (jb x m2, N-major as a GEMM operand) <-> its K-major transpose.
+cudaError_t launch_transpose_z(const void* src, int64_t lds, int64_t strideS, void* dst, int64_t ldd,
+                               int64_t strideD, int rows, int cols, int batch, cudaStream_t s);
 cudaError_t launch_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, double* u, cudaStream_t s);
 cudaError_t launch_zero_state(void* state, double* loglik, void* info, int batch, cudaStream_t s);
 

@@ -178,6 +178,36 @@ static cudaError_t launch_generic(UpdateArgs a, cudaStream_t s) {
 template <bool CPLX, bool BNMAJ, bool MASK, bool SCALE, bool CONJ>
 cudaError_t launch_update_ws_t(UpdateArgs a, cudaStream_t s);
 
+// 32 x 32 tiles through shared memory: coalesced 16-byte reads of src columns and dst columns.
+__global__ void __launch_bounds__(256) transpose_z_kernel(const double2* src, int64_t lds, int64_t strideS,
+                                                          double2* dst, int64_t ldd, int64_t strideD, int rows,
+                                                          int cols) {
+  __shared__ double2 t[32][33];
+  const int s = blockIdx.z;
+  const int k0 = blockIdx.x * 32, j0 = blockIdx.y * 32;  // src rows k (< rows), src cols j (< cols)
+  const double2* S = src + (int64_t)s * strideS;
+  double2* D = dst + (int64_t)s * strideD;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int jj = ty; jj < 32; jj += 8) {
+    const int k = k0 + tx, j = j0 + jj;
+    if (k < rows && j < cols) t[jj][tx] = S[k + (int64_t)j * lds];
+  }
+  __syncthreads();
+  for (int kk = ty; kk < 32; kk += 8) {
+    const int j = j0 + tx, k = k0 + kk;
+    if (k < rows && j < cols) D[j + (int64_t)k * ldd] = t[tx][kk];
+  }
+}
+
+cudaError_t launch_transpose_z(const void* src, int64_t lds, int64_t strideS, void* dst, int64_t ldd,
+                               int64_t strideD, int rows, int cols, int batch, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0 || batch <= 0) return cudaSuccess;
+  dim3 grid((rows + 31) / 32, (cols + 31) / 32, batch);
+  transpose_z_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(src), lds, strideS,
+                                          reinterpret_cast<double2*>(dst), ldd, strideD, rows, cols);
+  return cudaGetLastError();
+}
+
 // Dispatch on (kind, operand layout, flags).  Fast path: update_ws.cu (persistent,
 // warp-specialized, TMA-fed) for 16-byte-aligned operands; this file's cp.async kernel otherwise.
 static int g_force_generic = -1;
