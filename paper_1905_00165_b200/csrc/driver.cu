@@ -61,10 +61,11 @@ size_t esize(Kind k) { return k == HERM_D ? 8 : 16; }
 //   [panel operators: Bm (and Am for LU), nb x nb per sample]
 //   [D1 double buffer (Hermitian): 2 x chunk x nb doubles]
 //   [U12^T double buffer (LU): 2 x chunk x ldk x nb complex -- the row panel in K-major form]
+//   [W21 double buffer (Hermitian): 2 x chunk x ldk x nb -- the pre-scaled panel L21 D1]
 //   [K copies: chunk x ldk x n (batched / host)][host staging: mask, loglik, info (host)]
 struct WsLayout {
   size_t state_off, bm_off, am_off, d_off, ut_off, k_off, mask_off, ll_off, info_off, total;
-  int64_t ldk, strideK, strideM;
+  int64_t ldk, strideK, strideM, strideU;
 };
 
 WsLayout layout(Kind kind, int64_t chunk, int64_t n, int nb, bool copies, bool host) {
@@ -73,6 +74,7 @@ WsLayout layout(Kind kind, int64_t chunk, int64_t n, int nb, bool copies, bool h
   L.ldk = std::max<int64_t>(round_up(n, 16), 16);
   L.strideK = L.ldk * std::max<int64_t>(n, 1);
   L.strideM = (int64_t)nb * nb;
+  L.strideU = L.ldk * std::min<int64_t>(nb, std::max<int64_t>(n, 1));  // panel buffers: ldk x min(nb, n)
   size_t off = 0;
   L.state_off = off; off = align_up(off + sizeof(SampleState) * (size_t)chunk);
   L.bm_off = off; off = align_up(off + (size_t)chunk * L.strideM * es);
@@ -80,8 +82,8 @@ WsLayout layout(Kind kind, int64_t chunk, int64_t n, int nb, bool copies, bool h
   if (kind == LU_Z) off = align_up(off + (size_t)chunk * L.strideM * es);
   L.d_off = off;
   if (kind != LU_Z) off = align_up(off + 2 * (size_t)chunk * nb * 8);
-  L.ut_off = off;
-  if (kind == LU_Z) off = align_up(off + 2 * (size_t)chunk * (size_t)L.ldk * nb * es);
+  L.ut_off = off;  // LU: U12^T; Hermitian: W21 (same shape)
+  off = align_up(off + 2 * (size_t)chunk * (size_t)L.strideU * es);
   L.k_off = off;
   if (copies) off = align_up(off + (size_t)chunk * (size_t)L.strideK * es);
   L.mask_off = off;
@@ -241,9 +243,10 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     const int jb = (int)std::min<int64_t>(nb, n - j0);
     const int64_t j1 = j0 + jb, m2 = n - j1;
     double* dvec = herm ? reinterpret_cast<double*>(work + L.d_off) + (size_t)(step & 1) * batch * nb : nullptr;
-    // LU: U12^T (m2 x jb, ld = ldk, K-major GEMM operand), double-buffered like D1
-    const int64_t strideU = L.ldk * nb;
-    char* UT = herm ? nullptr : work + L.ut_off + (size_t)(step & 1) * batch * strideU * es;
+    // LU: U12^T (m2 x jb, ld = ldk, K-major GEMM operand); Hermitian: W21 = L21 D1 (same shape);
+    // double-buffered like D1
+    const int64_t strideU = L.strideU;
+    char* UT = work + L.ut_off + (size_t)(step & 1) * batch * strideU * es;
     // ---- stage 1
     DiagArgs d{};
     d.A = A; d.ld = ld; d.strideA = strideA; d.n = n; d.j0 = j0; d.tcol = j0; d.jb = jb; d.seed = seed; d.b0 = b0;
@@ -286,8 +289,12 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     UpdateArgs u = base_update(kind, batch, vec);
     u.Aop = Ab + (size_t)(j1 + j0 * ld) * es; u.lda = ld; u.strideA = strideA;  // L21
     if (herm) {
-      u.Bop = u.Aop; u.ldb = ld; u.strideB = strideA;  // L21, scaled by D1 (and conjugated) on load
-      u.dscale = dvec; u.dstride = nb; u.mask = 1; u.conj = (kind == HERM_Z);
+      // A22 -= W21 L21^H with W21 = L21 D1 (pre-scaled copy; the DMMA loop does no scaling)
+      CK(launch_scale_cols(kind == HERM_Z, Ab + (size_t)(j1 + j0 * ld) * es, ld, strideA, UT, L.ldk, strideU, dvec,
+                           nb, (int)m2, jb, batch, s1));
+      u.Aop = UT; u.lda = L.ldk; u.strideA = strideU;  // W21
+      u.Bop = Ab + (size_t)(j1 + j0 * ld) * es; u.ldb = ld; u.strideB = strideA;  // L21 (conjugated on load)
+      u.mask = 1; u.conj = (kind == HERM_Z);
     } else {
       u.Bop = UT; u.ldb = L.ldk; u.strideB = strideU;  // U12^T (j, k), K-major
     }

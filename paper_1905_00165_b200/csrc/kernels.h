@@ -76,6 +76,10 @@ cudaError_t launch_update(Kind kind, UpdateArgs a, cudaStream_t s);
 // the LU row panel A12 / U12 (jb x m2, N-major as a GEMM operand) <-> its K-major transpose.
 cudaError_t launch_transpose_z(const void* src, int64_t lds, int64_t strideS, void* dst, int64_t ldd,
                                int64_t strideD, int rows, int cols, int batch, cudaStream_t s);
+// W(i, k) = L(i, k) d[k] (i < rows, k < cols), real or complex, `batch` panels at the given strides
+cudaError_t launch_scale_cols(bool cplx, const void* L, int64_t ldl, int64_t strideL, void* W, int64_t ldw,
+                              int64_t strideW, const double* d, int64_t strideD, int rows, int cols, int batch,
+                              cudaStream_t s);
 cudaError_t launch_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, double* u, cudaStream_t s);
 cudaError_t launch_zero_state(void* state, double* loglik, void* info, int batch, cudaStream_t s);
 

@@ -15,6 +15,7 @@
 // 4 real DMMAs each (no 3M trick: keeps the textbook rounding and the paper's flop count).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -178,6 +179,33 @@ static cudaError_t launch_generic(UpdateArgs a, cudaStream_t s) {
 template <bool CPLX, bool BNMAJ, bool MASK, bool SCALE, bool CONJ>
 cudaError_t launch_update_ws_t(UpdateArgs a, cudaStream_t s);
 
+// W(i, k) = L(i, k) * d[k] for i < rows, k < cols: the pre-scaled panel W21 = L21 D1 of the
+// Hermitian trailing update (A operand), so the DMMA loop needs no per-k scaling.
+template <typename T>
+__global__ void __launch_bounds__(256) scale_cols_kernel(const T* L, int64_t ldl, int64_t strideL, T* W, int64_t ldw,
+                                                         int64_t strideW, const double* d, int64_t strideD, int rows,
+                                                         int cols) {
+  const int s = blockIdx.z, k = blockIdx.y;
+  const double dk = d[(int64_t)s * strideD + k];
+  const T* src = L + (int64_t)s * strideL + (int64_t)k * ldl;
+  T* dst = W + (int64_t)s * strideW + (int64_t)k * ldw;
+  for (int i = blockIdx.x * 256 + threadIdx.x; i < rows; i += gridDim.x * 256) dst[i] = scal(src[i], dk);
+}
+
+cudaError_t launch_scale_cols(bool cplx, const void* L, int64_t ldl, int64_t strideL, void* W, int64_t ldw,
+                              int64_t strideW, const double* d, int64_t strideD, int rows, int cols, int batch,
+                              cudaStream_t s) {
+  if (rows <= 0 || cols <= 0 || batch <= 0) return cudaSuccess;
+  dim3 grid((unsigned)std::min<int64_t>((rows + 255) / 256, 16), cols, batch);
+  if (cplx)
+    scale_cols_kernel<double2><<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(L), ldl, strideL,
+                                                    reinterpret_cast<double2*>(W), ldw, strideW, d, strideD, rows, cols);
+  else
+    scale_cols_kernel<double><<<grid, 256, 0, s>>>(reinterpret_cast<const double*>(L), ldl, strideL,
+                                                   reinterpret_cast<double*>(W), ldw, strideW, d, strideD, rows, cols);
+  return cudaGetLastError();
+}
+
 // 32 x 32 tiles through shared memory: coalesced 16-byte reads of src columns and dst columns.
 __global__ void __launch_bounds__(256) transpose_z_kernel(const double2* src, int64_t lds, int64_t strideS,
                                                           double2* dst, int64_t ldd, int64_t strideD, int rows,
@@ -225,11 +253,13 @@ cudaError_t launch_update(Kind kind, UpdateArgs a, cudaStream_t s) {
                      : launch_generic<CP, BN_, MK, SC, CJ, false>(a, s))
   if (kind == HERM_D) {
     if (a.bnmajor || a.conj) return cudaErrorInvalidValue;
-    if (a.mask && scale) DPP_GO(false, false, true, true, false);      // trailing update
+    if (a.mask && scale) DPP_GO(false, false, true, true, false);      // trailing update, B scaled by D1
+    if (a.mask && !scale) DPP_GO(false, false, true, false, false);    // trailing update, A = W21
     if (!a.mask && !scale) DPP_GO(false, false, false, false, false);  // panel GEMM
   } else if (kind == HERM_Z) {
     if (a.bnmajor) return cudaErrorInvalidValue;
     if (a.mask && scale && a.conj) DPP_GO(true, false, true, true, true);
+    if (a.mask && !scale && a.conj) DPP_GO(true, false, true, false, true);
     if (!a.mask && !scale && !a.conj) DPP_GO(true, false, false, false, false);
   } else {
     if (a.mask || scale || a.conj) return cudaErrorInvalidValue;

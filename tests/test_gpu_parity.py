@@ -210,9 +210,11 @@ def test_large_parity_2048(oracle_mod):
         assert_loglik_close(float(s.loglik), o.loglik)
 
 
-def test_generic_update_kernel_subprocess():
-    """The cp.async fallback update kernel (forced with DPP_UPDATE_GENERIC=1) gives the same
-    samples and factors as the oracle for all three kinds (run in a fresh process)."""
+@pytest.mark.parametrize("env", [{"DPP_UPDATE_GENERIC": "1"}, {"DPP_WS_VARIANT": "0"}])
+def test_alternate_update_kernels_subprocess(env):
+    """The cp.async fallback update kernel (forced with DPP_UPDATE_GENERIC=1) and the 8-consumer-
+    warp layout of the warp-specialized kernel (DPP_WS_VARIANT=0) give the same samples and
+    factors as the oracle for all three kinds (each run in a fresh process)."""
     import os
     import subprocess
     import sys
@@ -234,6 +236,6 @@ for kind, n in (("herm_d", 333), ("herm_z", 201), ("lu_z", 150)):
 print("GENERIC_OK")
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, DPP_UPDATE_GENERIC="1", PYTHONPATH=root)
+    env = dict(os.environ, PYTHONPATH=root, **env)
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert "GENERIC_OK" in r.stdout, r.stdout + r.stderr

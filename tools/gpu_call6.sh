@@ -1,0 +1,11 @@
+set -x
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+DPP_WS_VARIANT=1 timeout 900 python -m pytest tests -m gpu -q -x -k "herm_d or config3 or config1 or config0 or map" > gpurun_out/pytest_v1.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_v1.log
+timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_v0.json 2> gpurun_out/bench_v0.err
+DPP_WS_VARIANT=1 timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_v1.json 2> gpurun_out/bench_v1.err
+for w in herm_z ust; do timeout 900 python bench.py --workload $w > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; done
+DPP_WS_VARIANT=1 timeout 900 python bench.py --workload ust > gpurun_out/bench_ust_v1.json 2> gpurun_out/bench_ust_v1.err
+CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+DPP_WS_VARIANT=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"update_ws_kernel" -s 50 -c 1 -o gpurun_out/prof_c4_v1b $CMD > gpurun_out/ncu_full_v1.log 2>&1
+echo done
