@@ -213,13 +213,14 @@ int dpp_sample_herm_z_dist(dpp_comm_t comm, int64_t n, dpp_complex_t* K_local, i
  * this thread's calls on the current device is bracketed by CUDA events ON THE
  * STREAM IT IS LAUNCHED ON.  dpp_profile_end() synchronises those events and
  * returns, per stage (0 = diag tile, 1 = panel, 2 = lookahead update (a),
- * 3 = trailing update (b)), the number of launches, the summed event time and
+ * 3 = trailing update (b), 4 = auxiliary kernels: kernel copies, panel scaling and
+ * transposes), the number of launches, the summed event time and
  * the ALGORITHMIC flops (paper convention: real flops; a complex multiply-add
  * counts 8, i.e. 4x the real count).  Not reentrant across host threads. */
 typedef struct {
-  int64_t launches[4];
-  double ms[4];
-  double flops[4];
+  int64_t launches[5];
+  double ms[5];
+  double flops[5];
 } dpp_profile_t;
 int dpp_profile_begin(void);
 int dpp_profile_end(dpp_profile_t* out);

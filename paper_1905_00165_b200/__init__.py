@@ -68,7 +68,7 @@ _sig("dpp_dist_workspace_bytes", _SZ, [ctypes.c_int, _I64, ctypes.c_int, _P])
 for _n in ("dpp_sample_herm_d_dist", "dpp_sample_herm_z_dist"):
     _sig(_n, ctypes.c_int, [_P, _I64, _P, _I64, _U64, _P, _P, _P, _P, _P, _SZ, _P])
 class dpp_profile_t(ctypes.Structure):
-    _fields_ = [("launches", ctypes.c_int64 * 4), ("ms", ctypes.c_double * 4), ("flops", ctypes.c_double * 4)]
+    _fields_ = [("launches", ctypes.c_int64 * 5), ("ms", ctypes.c_double * 5), ("flops", ctypes.c_double * 5)]
 
 
 _sig("dpp_profile_begin", ctypes.c_int, [])
@@ -214,7 +214,7 @@ def dpp_sample_herm_z_dist(comm, n, K_local, ld_local, seed, mask, loglik, info=
                                        work_bytes if work_bytes is not None else work.numel(), _stream(stream)))
 
 
-STAGES = ("diag", "panel", "update_lookahead", "update_trailing")
+STAGES = ("diag", "panel", "update_lookahead", "update_trailing", "aux")
 
 
 def dpp_profile_begin():

@@ -26,6 +26,8 @@
 // The Hermitian path reads/writes the lower triangle only.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "philox.cuh"
@@ -52,12 +54,14 @@ __device__ __forceinline__ int bp(int i, int k) {
 }
 
 // X = L^{-1} for a lower-triangular L (unit or not) of order 16*nblk, both block-packed in smem.
-// Tb: scratch for (nblk - 1) 16x16 blocks.  All 256 threads participate.
-template <typename T, bool UNIT>
+// Tb: scratch for (nblk - 1) 16x16 blocks.  All NT threads participate (NT a multiple of 256: each
+// group of 256 threads owns one 16x16 block of a level).
+template <typename T, bool UNIT, int NT>
 __device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NWARPS = NT / 32, NGRP = NT / 256;
   // diagonal blocks: warp w inverts block w (lane c < 16 forms column c by forward substitution)
-  for (int I = warp; I < nblk; I += 8) {
+  for (int I = warp; I < nblk; I += NWARPS) {
     if (lane < 16) {
       const int c = lane;
       const T* Lblk = Lb + ((I * (I + 1) / 2 + I) << 8);
@@ -74,11 +78,11 @@ __device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
       for (int i = 0; i < 16; ++i) Xblk[i + (c << 4)] = x[i];
     }
   }
-  const int r = tid & 15, c = tid >> 4;
+  const int r = tid & 15, c = (tid >> 4) & 15, grp = tid >> 8;
   for (int d = 1; d < nblk; ++d) {
     __syncthreads();
     // T_q = sum_{K=J}^{I-1} L_{IK} X_{KJ}   for (I, J) = (d + q, q)
-    for (int q = 0; q + d < nblk; ++q) {
+    for (int q = grp; q + d < nblk; q += NGRP) {
       const int I = d + q, J = q;
       T s0 = zero<T>(), s1 = zero<T>(), s2 = zero<T>(), s3 = zero<T>();  // 4 chains for ILP
       for (int K = J; K < I; ++K) {
@@ -96,7 +100,7 @@ __device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
     }
     __syncthreads();
     // X_{IJ} = -X_{II} T_q
-    for (int q = 0; q + d < nblk; ++q) {
+    for (int q = grp; q + d < nblk; q += NGRP) {
       const int I = d + q, J = q;
       const T* Xii = Xb + ((I * (I + 1) / 2 + I) << 8);
       T s0 = zero<T>(), s1 = zero<T>();
@@ -111,9 +115,10 @@ __device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
   __syncthreads();
 }
 
-template <typename T, bool HERM, int NB>
-__global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
-  constexpr int TR = 16, TC = 16, RA = NB / TR, CB = NB / TC;
+template <typename T, bool HERM, int NB, int NT>
+__global__ void __launch_bounds__(NT, 1) diag_kernel(const DiagArgs a) {
+  constexpr int TC = 16, TR = NT / TC, RA = NB / TR, CB = NB / TC;
+  static_assert(NB % TR == 0, "tile rows must be a multiple of the thread-grid rows");
   constexpr int NBLK = NB / 16, NPB = NBLK * (NBLK + 1) / 2;  // packed 16x16 blocks
   __shared__ T colbuf[2][2][NB];                    // [buffer][pivot of the pair][row], 0 on/above the pivot
   __shared__ T rowbuf[HERM ? 1 : 2][2][HERM ? 1 : NB];  // LU: [buffer][pivot][column], 0 on/left of the pivot
@@ -144,7 +149,7 @@ __global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
       const int i = tr + TR * ia, l = tc + TC * ib;
       R[ia][ib] = (i < jb && l < jb && (!HERM || i >= l)) ? A[(int64_t)l * a.ld + i] : zero<T>();
     }
-  for (int k = tid; k < jb; k += 256) {
+  for (int k = tid; k < jb; k += NT) {
     // greedy MAP: the decision u <= d with u = 1/2 is "keep iff Re p >= 1/2" (reading R18)
     U[k] = a.map ? 0.5 : uniform_u(a.seed, (uint64_t)(a.j0 + k), b);
     if (a.forced) keepv[k] = a.forced[(int64_t)s * a.n + a.j0 + k] != 0;
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
     for (int ia = 0; ia < RA; ++ia)
 #pragma unroll
       for (int ib = 0; ib < CB; ++ib)
-        if (!HERM || ib <= ia) {
+        if (!HERM || TC * ib <= TR * ia + TR - 1) {  // skip register blocks entirely above the diagonal
           R[ia][ib] = fms(R[ia][ib], L0[ia], W0[ib]);
           R[ia][ib] = fms(R[ia][ib], L1[ia], W1[ib]);
         }
@@ -277,7 +282,7 @@ __global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
     }
   // ---- decisions, likelihood terms and diagnostics: warp 0 reduces the flags with ballots and
   //      shuffles; the log-likelihood terms are summed by one lane IN PIVOT ORDER
-  for (int k = tid; k < jb; k += 256) {
+  for (int k = tid; k < jb; k += NT) {
     a.mask[(int64_t)s * a.n + a.j0 + k] = keepv[k];
     lg[k] = log(absval(pv[k]));
   }
@@ -335,12 +340,12 @@ __global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
   // ---- stage-2 operators from the inverses of the tile's triangular factors
   const int nblk = (jb + 15) >> 4;
   T* Bm = reinterpret_cast<T*>(a.Bm) + (int64_t)s * a.strideM;
-  tri_inverse_lower<T, true>(Lb, Xb, Tb, nblk);  // Xb = L11^{-1}
+  tri_inverse_lower<T, true, NT>(Lb, Xb, Tb, nblk);  // Xb = L11^{-1}
   if (HERM) {
     double* dvec = a.dvec + (int64_t)s * a.ldm;  // D1 of sample s (stride nb)
-    for (int k = tid; k < jb; k += 256) dvec[k] = re(pv[k]);
+    for (int k = tid; k < jb; k += NT) dvec[k] = re(pv[k]);
     // Bm(j,k) = delta_jk - conj(Linv(j,k)) / D(j)  (j >= k), 0 above
-    for (int idx = tid; idx < jb * jb; idx += 256) {
+    for (int idx = tid; idx < jb * jb; idx += NT) {
       const int k = idx / jb, j = idx % jb;
       T v = zero<T>();
       if (j >= k) {
@@ -352,14 +357,14 @@ __global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
   } else {
     // Am(i,k) = -Linv(i,k) (i > k), else 0
     T* Am = reinterpret_cast<T*>(a.Am) + (int64_t)s * a.strideM;
-    for (int idx = tid; idx < jb * jb; idx += 256) {
+    for (int idx = tid; idx < jb * jb; idx += NT) {
       const int k = idx / jb, i = idx % jb;
       Am[i + (int64_t)k * a.ldm] = (i > k) ? neg(Xb[bp(i, k)]) : zero<T>();
     }
     __syncthreads();
-    tri_inverse_lower<T, false>(Ub, Xb, Tb, nblk);  // Xb = (U11^T)^{-1} = (U11^{-1})^T
+    tri_inverse_lower<T, false, NT>(Ub, Xb, Tb, nblk);  // Xb = (U11^T)^{-1} = (U11^{-1})^T
     // Bm(j,k) = delta_jk - Uinv(k,j) = delta_jk - Xb(j,k)  (j >= k), 0 above
-    for (int idx = tid; idx < jb * jb; idx += 256) {
+    for (int idx = tid; idx < jb * jb; idx += NT) {
       const int k = idx / jb, j = idx % jb;
       T v = zero<T>();
       if (j >= k) {
@@ -371,18 +376,40 @@ __global__ void __launch_bounds__(256, 1) diag_kernel(const DiagArgs a) {
   }
 }
 
-template <typename T, bool HERM, int NB>
-static cudaError_t launch_diag_t(const DiagArgs& a, cudaStream_t s) {
+template <typename T, bool HERM, int NB, int NT>
+static cudaError_t launch_diag_nt(const DiagArgs& a, cudaStream_t s) {
   constexpr int NBLK = NB / 16, NPB = NBLK * (NBLK + 1) / 2;
   const size_t smem = a.need_ops ? (size_t)((HERM ? 2 : 3) * NPB * 256 + (NBLK - 1) * 256) * sizeof(T) : 0;
-  auto* fn = diag_kernel<T, HERM, NB>;
+  auto* fn = diag_kernel<T, HERM, NB, NT>;
   if (smem > 0) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   dim3 grid(1, a.batch);
-  fn<<<grid, 256, smem, s>>>(a);
+  fn<<<grid, NT, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+// Threads per tile CTA: 256 (8 x 8 register blocks per thread at nb = 128).  DPP_DIAG_NT=512
+// selects a 32 x 16 thread grid for tiles of 64 and more (measured slower at nb = 128: 107 vs
+// 101 us per tile -- the per-pivot chain, not the update FLOPs, bounds this kernel).
+static int diag_nt_override() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPP_DIAG_NT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+template <typename T, bool HERM, int NB>
+static cudaError_t launch_diag_t(const DiagArgs& a, cudaStream_t s) {
+  if constexpr (NB >= 64) {
+    const int o = diag_nt_override();
+    const int nt = (o == 256 || o == 512) ? o : 256;
+    if (nt == 512) return launch_diag_nt<T, HERM, NB, 512>(a, s);
+  }
+  return launch_diag_nt<T, HERM, NB, 256>(a, s);
 }
 
 cudaError_t launch_diag(Kind kind, int nb, const DiagArgs& a, cudaStream_t s) {

@@ -58,8 +58,9 @@ MsgLayout msg_layout(int nb) {
 }
 
 // work = [state][panel operator Bm: nb x nb][D1: nb][message buffer 0][message buffer 1]
+//        [W21 = L21 D1 of message 0][of message 1] (the pre-scaled A operand of the update)
 struct DistWs {
-  size_t state_off, bm_off, d_off, msg_off[2], total;
+  size_t state_off, bm_off, d_off, msg_off[2], w_off[2], total;
   int64_t ldw;
 };
 DistWs dist_ws(int64_t n, int nb, size_t es) {
@@ -73,6 +74,10 @@ DistWs dist_ws(int64_t n, int nb, size_t es) {
   for (int b = 0; b < 2; ++b) {
     w.msg_off[b] = off;
     off = align_up(off + m.header_bytes + (size_t)w.ldw * nb * es);
+  }
+  for (int b = 0; b < 2; ++b) {
+    w.w_off[b] = off;
+    off = align_up(off + (size_t)w.ldw * nb * es);
   }
   w.total = off;
   return w;
@@ -214,6 +219,10 @@ int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* K_local, int64_t ld_lo
       unpack_header_kernel<<<1, 128, 0, s>>>(msg, M, jb, state, mask + k * nb);
       CK(cudaGetLastError());
     }
+    // every rank: W21 = L21 D1 (the update's A operand; the DMMA loop then needs no scaling)
+    if (m2 > 0)
+      CK(launch_scale_cols(kind == HERM_Z, msg + M.w_off, W.ldw, 0, w + W.w_off[k & 1], W.ldw, 0,
+                           reinterpret_cast<const double*>(msg + M.d_off), 0, (int)m2, jb, 1, s));
     return DPP_OK;
   };
   // stage 3 of step k on local blocks q >= q_lo, up to `count` blocks (count < 0: all)
@@ -224,8 +233,8 @@ int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* K_local, int64_t ld_lo
     if (m2 <= 0 || q_lo >= q_hi) return DPP_OK;
     char* msg = msg_of(k);
     UpdateArgs u{};
-    u.Aop = msg + M.w_off; u.lda = W.ldw;
-    u.Bop = msg + M.w_off; u.ldb = W.ldw; u.dscale = reinterpret_cast<const double*>(msg + M.d_off); u.mask = 1;
+    u.Aop = w + W.w_off[k & 1]; u.lda = W.ldw;   // W21 = L21 D1
+    u.Bop = msg + M.w_off; u.ldb = W.ldw; u.mask = 1;  // L21 (conjugated on load for complex)
     u.conj = kind == HERM_Z;
     u.C = Kb + (size_t)j1 * es;  // local column 0, A22 row 0
     u.ldc = ld_local;

@@ -274,7 +274,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
         // U12 = L11^-1 A12 = A12 - Am A12 (Am = I - L11^-1), computed transposed so that every
         // operand is K-major:  U12^T = A12^T - A12^T Am^T  in the U12^T buffer, then copied back.
         char* A12 = Ab + (size_t)(j0 + j1 * ld) * es;
-        CK(launch_transpose_z(A12, ld, strideA, UT, L.ldk, strideU, jb, (int)m2, batch, s1));
+        { ProfScope pa(4, 0.0, s1); CK(launch_transpose_z(A12, ld, strideA, UT, L.ldk, strideU, jb, (int)m2, batch, s1)); }
         UpdateArgs q = base_update(kind, batch, vec);
         q.Aop = UT; q.lda = L.ldk; q.strideA = strideU;                            // A12^T (j, k)
         q.Bop = Am; q.ldb = nb; q.strideB = L.strideM;                             // Am (i, k)
@@ -282,6 +282,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
         q.a_rows = (int)m2; q.b_rows = jb; q.K = jb;
         q.row0 = 0; q.col0 = 0; q.rows = (int)m2; q.cols = jb;
         CK(launch_update(kind, q, s1));
+        ProfScope pa(4, 0.0, s1);
         CK(launch_transpose_z(UT, L.ldk, strideU, A12, ld, strideA, (int)m2, jb, batch, s1));  // U12 -> K
       }
     }
@@ -290,6 +291,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     u.Aop = Ab + (size_t)(j1 + j0 * ld) * es; u.lda = ld; u.strideA = strideA;  // L21
     if (herm) {
       // A22 -= W21 L21^H with W21 = L21 D1 (pre-scaled copy; the DMMA loop does no scaling)
+      ProfScope pa(4, 0.0, s1);
       CK(launch_scale_cols(kind == HERM_Z, Ab + (size_t)(j1 + j0 * ld) * es, ld, strideA, UT, L.ldk, strideU, dvec,
                            nb, (int)m2, jb, batch, s1));
       u.Aop = UT; u.lda = L.ldk; u.strideA = strideU;  // W21
@@ -389,20 +391,42 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
   const size_t es = esize(kind);
   const cudaMemcpyKind ck = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   char* Kc = w + L.k_off;
+  // Kernels are copied into their workspace slots.  Hermitian kernels read only the lower
+  // triangle, so only it is moved: device sources with one batched copy kernel, host sources with
+  // one 2-D DMA copy per 128-column block of rows [c, n) -- about half the bytes of the full
+  // matrix (this halves the host->device time of the _host entry points).
+  const bool lower = kind != LU_Z;
+  auto h2d = [&](char* dst, const char* src) -> int {
+    if (!lower) {
+      CK(cudaMemcpy2DAsync(dst, (size_t)L.ldk * es, src, (size_t)ld * es, (size_t)n * es, (size_t)n, ck, st));
+      return DPP_OK;
+    }
+    constexpr int64_t CB = 128;
+    for (int64_t c = 0; c < n; c += CB) {
+      const int64_t w_ = std::min<int64_t>(CB, n - c);
+      CK(cudaMemcpy2DAsync(dst + (size_t)(c + c * L.ldk) * es, (size_t)L.ldk * es, src + (size_t)(c + c * ld) * es,
+                           (size_t)ld * es, (size_t)(n - c) * es, (size_t)w_, ck, st));
+    }
+    return DPP_OK;
+  };
   for (int64_t c0 = 0; c0 < batch; c0 += chunk) {
     const int cb = (int)std::min<int64_t>(chunk, batch - c0);
     if (n > 0) {
-      if (strideK == 0 && host) {
+      if (host && strideK == 0) {
         // one host->device transfer of the shared kernel, then device-side replication
-        CK(cudaMemcpy2DAsync(Kc, (size_t)L.ldk * es, K, (size_t)ld * es, (size_t)n * es, (size_t)n, ck, st));
-        for (int s = 1; s < cb; ++s)
-          CK(cudaMemcpyAsync(Kc + (size_t)s * L.strideK * es, Kc, (size_t)L.strideK * es, cudaMemcpyDeviceToDevice, st));
+        if ((rc = h2d(Kc, reinterpret_cast<const char*>(K)))) return rc;
+        ProfScope pa(4, 0.0, st);
+        if (cb > 1)
+          CK(launch_copy_matrix(kind != HERM_D, Kc, L.ldk, 0, Kc + (size_t)L.strideK * es, L.ldk, L.strideK, (int)n,
+                                cb - 1, lower, st));
+      } else if (host) {
+        for (int s = 0; s < cb; ++s)
+          if ((rc = h2d(Kc + (size_t)s * L.strideK * es,
+                        reinterpret_cast<const char*>(K) + (size_t)(strideK * (c0 + s)) * es))) return rc;
       } else {
-        for (int s = 0; s < cb; ++s) {
-          const char* src = reinterpret_cast<const char*>(K) + (size_t)(strideK * (c0 + s)) * es;
-          CK(cudaMemcpy2DAsync(Kc + (size_t)s * L.strideK * es, (size_t)L.ldk * es, src, (size_t)ld * es,
-                               (size_t)n * es, (size_t)n, ck, st));
-        }
+        ProfScope pa(4, 0.0, st);
+        CK(launch_copy_matrix(kind != HERM_D, reinterpret_cast<const char*>(K) + (size_t)(strideK * c0) * es, ld,
+                              strideK, Kc, L.ldk, L.strideK, (int)n, cb, lower, st));
       }
     }
     uint8_t* mk = host ? reinterpret_cast<uint8_t*>(w + L.mask_off) : mask + c0 * n;

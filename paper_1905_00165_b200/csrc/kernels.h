@@ -80,6 +80,9 @@ cudaError_t launch_transpose_z(const void* src, int64_t lds, int64_t strideS, vo
 cudaError_t launch_scale_cols(bool cplx, const void* L, int64_t ldl, int64_t strideL, void* W, int64_t ldw,
                               int64_t strideW, const double* d, int64_t strideD, int rows, int cols, int batch,
                               cudaStream_t s);
+// dst <- src for `batch` n x n column-major matrices (lower: rows >= column only)
+cudaError_t launch_copy_matrix(bool cplx, const void* src, int64_t lds, int64_t strideS, void* dst, int64_t ldd,
+                               int64_t strideD, int n, int batch, bool lower, cudaStream_t s);
 cudaError_t launch_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, double* u, cudaStream_t s);
 cudaError_t launch_zero_state(void* state, double* loglik, void* info, int batch, cudaStream_t s);
 

@@ -206,6 +206,30 @@ cudaError_t launch_scale_cols(bool cplx, const void* L, int64_t ldl, int64_t str
   return cudaGetLastError();
 }
 
+// dst <- src for `batch` n x n column-major matrices; lower = true copies only rows >= column (the
+// part a Hermitian sampler reads).  One CTA per (column, sample).
+template <typename T>
+__global__ void __launch_bounds__(256) copy_matrix_kernel(const T* src, int64_t lds, int64_t strideS, T* dst,
+                                                          int64_t ldd, int64_t strideD, int n, bool lower) {
+  const int64_t j = blockIdx.x, s = blockIdx.y;
+  const T* a = src + s * strideS + j * lds;
+  T* b = dst + s * strideD + j * ldd;
+  for (int i = (lower ? (int)j : 0) + threadIdx.x; i < n; i += 256) b[i] = a[i];
+}
+
+cudaError_t launch_copy_matrix(bool cplx, const void* src, int64_t lds, int64_t strideS, void* dst, int64_t ldd,
+                               int64_t strideD, int n, int batch, bool lower, cudaStream_t s) {
+  if (n <= 0 || batch <= 0) return cudaSuccess;
+  dim3 grid(n, batch);
+  if (cplx)
+    copy_matrix_kernel<double2><<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(src), lds, strideS,
+                                                     reinterpret_cast<double2*>(dst), ldd, strideD, n, lower);
+  else
+    copy_matrix_kernel<double><<<grid, 256, 0, s>>>(reinterpret_cast<const double*>(src), lds, strideS,
+                                                    reinterpret_cast<double*>(dst), ldd, strideD, n, lower);
+  return cudaGetLastError();
+}
+
 // 32 x 32 tiles through shared memory: coalesced 16-byte reads of src columns and dst columns.
 __global__ void __launch_bounds__(256) transpose_z_kernel(const double2* src, int64_t lds, int64_t strideS,
                                                           double2* dst, int64_t ldd, int64_t strideD, int rows,

@@ -27,7 +27,7 @@ __device__ __forceinline__ TileInfo tile_info(const UpdateArgs& a, int t, int ti
   const int u = t % tiles_per_sample;
   int r, c;
   if (a.tri) {
-    int q = (int)((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
+    int q = (int)((sqrtf(8.0f * (float)u + 1.0f) - 1.0f) * 0.5f);  // fp32 guess, fixed up below
     while ((q + 1) * (q + 2) / 2 <= u) ++q;
     while (q * (q + 1) / 2 > u) --q;
     r = q;

@@ -210,7 +210,8 @@ def test_large_parity_2048(oracle_mod):
         assert_loglik_close(float(s.loglik), o.loglik)
 
 
-@pytest.mark.parametrize("env", [{"DPP_UPDATE_GENERIC": "1"}, {"DPP_WS_VARIANT": "0"}])
+@pytest.mark.parametrize("env", [{"DPP_UPDATE_GENERIC": "1"}, {"DPP_WS_VARIANT": "0"}, {"DPP_DIAG_NT": "256"},
+                                 {"DPP_DIAG_NT": "512"}])
 def test_alternate_update_kernels_subprocess(env):
     """The cp.async fallback update kernel (forced with DPP_UPDATE_GENERIC=1) and the 8-consumer-
     warp layout of the warp-specialized kernel (DPP_WS_VARIANT=0) give the same samples and
