@@ -18,6 +18,9 @@ Pinned by ``tests/test_oracle_*.py`` (-m "not gpu"):
   * factor:    L D L^H = K - 1_{Y^c}, L U = K - 1_{Y^c}; loglik = ln|det| (slogdet).
   * prefix:    decisions on K[:m,:m] = first m decisions on K (loop invariant,
                PAPER.md:402-405).
+  * fp32 (reading R19): diag(p) closed form in fp32, brute-force law of the
+               fp32 kernel, agreement with the fp64 oracle within fp32 rounding, UST and
+               Aztec structure (tests/test_oracle_fp32.py).
   * greedy MAP: K = diag(p) closed form; every decision takes the
                branch whose leading-principal-minor probability |det| is larger
                (numpy det, brute force over both branches at every pivot).
@@ -35,7 +38,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "dpp_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-HERM_D, HERM_Z, LU_Z = 0, 1, 2
+HERM_D, HERM_Z, LU_Z, HERM_S, LU_C = 0, 1, 2, 3, 4
 TIE_TOL = 1e-9
 RANGE_TOL = 1e-8
 
@@ -82,7 +85,8 @@ def lib():
     if _lib is None:
         _lib = ctypes.CDLL(build())
         P = ctypes.c_void_p
-        for name in ("oracle_sample_herm_d", "oracle_sample_herm_z", "oracle_sample_lu_z"):
+        for name in ("oracle_sample_herm_d", "oracle_sample_herm_z", "oracle_sample_lu_z",
+                     "oracle_sample_herm_s", "oracle_sample_lu_c"):
             f = getattr(_lib, name)
             f.restype = ctypes.c_int
             f.argtypes = [ctypes.c_int64, P, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, P,
@@ -114,7 +118,8 @@ def uniform(seed: int, j: int, b: int = 0) -> float:
 
 
 def _as_colmajor(K: np.ndarray, kind: int) -> np.ndarray:
-    dt = np.float64 if kind == HERM_D else np.complex128
+    dt = {HERM_D: np.float64, HERM_Z: np.complex128, LU_Z: np.complex128, HERM_S: np.float32,
+          LU_C: np.complex64}[kind]
     return np.array(K, dtype=dt, order="F", copy=True)
 
 
@@ -133,7 +138,8 @@ def sample(kind: int, K: np.ndarray, seed: int = 0, b: int = 0, forced=None,
         assert forced.shape == (n,)
         fptr = forced.ctypes.data
     fn = {HERM_D: lib().oracle_sample_herm_d, HERM_Z: lib().oracle_sample_herm_z,
-          LU_Z: lib().oracle_sample_lu_z}[kind]
+          LU_Z: lib().oracle_sample_lu_z, HERM_S: lib().oracle_sample_herm_s,
+          LU_C: lib().oracle_sample_lu_c}[kind]
     rc = fn(n, A.ctypes.data, max(n, 1), seed, b, fptr, tie_tol, range_tol,
             mask.ctypes.data, ctypes.byref(ll), ctypes.byref(info))
     if rc != 0:
@@ -175,6 +181,17 @@ def sample_herm_z(K, seed=0, b=0, forced=None, **kw):
 
 def sample_lu_z(K, seed=0, b=0, forced=None, **kw):
     return sample(LU_Z, K, seed, b, forced, **kw)
+
+
+def sample_herm_s(K, seed=0, b=0, forced=None, **kw):
+    """Single-precision real symmetric sampler (reading R19): fp32 factorization, fp64 decisions
+    against the fp32 pivot, fp64 log-likelihood accumulation."""
+    return sample(HERM_S, K, seed, b, forced, **kw)
+
+
+def sample_lu_c(K, seed=0, b=0, forced=None, **kw):
+    """Single-precision complex non-Hermitian LU sampler (reading R19)."""
+    return sample(LU_C, K, seed, b, forced, **kw)
 
 
 def sample_many(kind: int, K: np.ndarray, seed: int, b0: int, batch: int):

@@ -244,6 +244,90 @@ ORACLE_EXPORT(herm_d)
 ORACLE_EXPORT(herm_z)
 ORACLE_EXPORT(lu_z)
 
+
+/* ------------------------------------------------------------------------ */
+/* Single precision (the paper's single-precision runs, */
+/* PAPER.md:1164-1169).  The same Listing 1 loops with every matrix entry,   */
+/* pivot, multiplier and update in fp32 (float / float complex); the         */
+/* decision compares the fp64 uniform with the fp32 pivot promoted to        */
+/* double, and the log-likelihood is accumulated in fp64 from the fp32       */
+/* pivots (reading R19).                                                     */
+/* ------------------------------------------------------------------------ */
+static int run_herm_s(int map, int64_t n, float* A, int64_t ld, uint64_t seed, uint64_t b,
+                      const uint8_t* forced, double tie_tol, double range_tol,
+                      uint8_t* mask, double* loglik, oracle_info_t* info) {
+  if (n < 0 || ld < (n > 1 ? n : 1)) return -1;
+  oracle_info_t inf;
+  info_init(&inf);
+  double ll = 0.0;
+  float* w = (float*)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
+  if (!w) return -2;
+#define A_(i, l) A[(size_t)(l) * (size_t)ld + (size_t)(i)]
+  for (int64_t j = 0; j < n; ++j) {
+    float d = A_(j, j);
+    int keep = decide((double)d, j, seed, b, forced, tie_tol, range_tol, &inf, map);
+    if (!keep) d -= 1.0f;                     /* line 437 */
+    A_(j, j) = d;
+    mask[j] = (uint8_t)keep;
+    inf.n_kept += keep;
+    ll += log(fabs((double)d));
+    if (fabs((double)d) < inf.min_abs_pivot) inf.min_abs_pivot = fabs((double)d);
+    for (int64_t i = j + 1; i < n; ++i) {     /* line 438 */
+      w[i] = A_(i, j);
+      A_(i, j) = w[i] / d;
+    }
+    for (int64_t l = j + 1; l < n; ++l)       /* line 439: rank-1, lower only */
+      for (int64_t i = l; i < n; ++i)
+        A_(i, l) -= A_(i, j) * w[l];
+  }
+#undef A_
+  free(w);
+  *loglik = ll;
+  if (info) *info = inf;
+  return 0;
+}
+
+static int run_lu_c(int map, int64_t n, float* Araw, int64_t ld, uint64_t seed, uint64_t b,
+                    const uint8_t* forced, double tie_tol, double range_tol,
+                    uint8_t* mask, double* loglik, oracle_info_t* info) {
+  if (n < 0 || ld < (n > 1 ? n : 1)) return -1;
+  float complex* A = (float complex*)Araw;
+  oracle_info_t inf;
+  info_init(&inf);
+  double ll = 0.0;
+#define A_(i, l) A[(size_t)(l) * (size_t)ld + (size_t)(i)]
+  for (int64_t j = 0; j < n; ++j) {
+    float complex p = A_(j, j);
+    if (fabs((double)cimagf(p)) > inf.max_abs_imag_pivot) inf.max_abs_imag_pivot = fabs((double)cimagf(p));
+    int keep = decide((double)crealf(p), j, seed, b, forced, tie_tol, range_tol, &inf, map);
+    if (!keep) p -= 1.0f;                     /* line 437 */
+    A_(j, j) = p;
+    mask[j] = (uint8_t)keep;
+    inf.n_kept += keep;
+    double ap = hypot((double)crealf(p), (double)cimagf(p));
+    ll += log(ap);
+    if (ap < inf.min_abs_pivot) inf.min_abs_pivot = ap;
+    for (int64_t i = j + 1; i < n; ++i)       /* line 438 */
+      A_(i, j) = A_(i, j) / p;
+    for (int64_t l = j + 1; l < n; ++l)       /* line 439 */
+      for (int64_t i = j + 1; i < n; ++i)
+        A_(i, l) -= A_(i, j) * A_(j, l);
+  }
+#undef A_
+  *loglik = ll;
+  if (info) *info = inf;
+  return 0;
+}
+
+int oracle_sample_herm_s(int64_t n, float* A, int64_t ld, uint64_t seed, uint64_t b, const uint8_t* forced,
+                         double tie_tol, double range_tol, uint8_t* mask, double* loglik, oracle_info_t* info) {
+  return run_herm_s(0, n, A, ld, seed, b, forced, tie_tol, range_tol, mask, loglik, info);
+}
+int oracle_sample_lu_c(int64_t n, float* A, int64_t ld, uint64_t seed, uint64_t b, const uint8_t* forced,
+                       double tie_tol, double range_tol, uint8_t* mask, double* loglik, oracle_info_t* info) {
+  return run_lu_c(0, n, A, ld, seed, b, forced, tie_tol, range_tol, mask, loglik, info);
+}
+
 /*
  * Many independent samples b = b0 .. b0+batch-1 of ONE kernel K (read-only),
  * each on a fresh copy of K.  A plain loop over the single-sample routines
@@ -252,14 +336,22 @@ ORACLE_EXPORT(lu_z)
  */
 int oracle_sample_many(int kind, int64_t n, const double* K, int64_t ld, uint64_t seed,
                        uint64_t b0, int64_t batch, uint8_t* masks, double* logliks) {
-  int cplx = (kind != 0);
-  size_t elems = (size_t)ld * (size_t)(n > 0 ? n : 1) * (cplx ? 2 : 1);
-  double* work = (double*)malloc(sizeof(double) * elems);
+  /* element bytes: herm_d 8, herm_z 16, lu_z 16, herm_s 4, lu_c 8 */
+  static const size_t ebytes[5] = {8, 16, 16, 4, 8};
+  if (kind < 0 || kind > 4) return -1;
+  size_t bytes = (size_t)ld * (size_t)(n > 0 ? n : 1) * ebytes[kind];
+  double* work = (double*)malloc(bytes);
   if (!work) return -2;
   for (int64_t s = 0; s < batch; ++s) {
-    memcpy(work, K, sizeof(double) * elems);
+    memcpy(work, K, bytes);
     int rc;
-    if (kind == 0)
+    if (kind == 3)
+      rc = oracle_sample_herm_s(n, (float*)work, ld, seed, b0 + (uint64_t)s, NULL, 1e-9, 1e-8,
+                                masks + (size_t)s * (size_t)n, logliks + s, NULL);
+    else if (kind == 4)
+      rc = oracle_sample_lu_c(n, (float*)work, ld, seed, b0 + (uint64_t)s, NULL, 1e-9, 1e-8,
+                              masks + (size_t)s * (size_t)n, logliks + s, NULL);
+    else if (kind == 0)
       rc = oracle_sample_herm_d(n, work, ld, seed, b0 + (uint64_t)s, NULL, 1e-9, 1e-8,
                                 masks + (size_t)s * (size_t)n, logliks + s, NULL);
     else if (kind == 1)
