@@ -53,13 +53,93 @@ __device__ __forceinline__ int bp(int i, int k) {
   return ((I * (I + 1) / 2 + J) << 8) + (i & 15) + ((k & 15) << 4);
 }
 
+// C (16x16) += A (16x16) B (16x16) on 16x16 column-major blocks in shared memory, one warp, with
+// DMMA.8x8x4: 2x2 output tiles of 8x8, four k-steps of 4.  Fragments of mma.m8n8k4.row.col:
+// a = A[m = lane>>2][k = lane&3], b = B[k = lane&3][n = lane>>2], c = C[lane>>2][2(lane&3) + e].
+// Complex blocks take four real products (re/im parts of the fragments).
+template <typename T> struct BlockAcc16;
+template <> struct BlockAcc16<double> {
+  double c[2][2][2];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+  }
+  __device__ __forceinline__ void mma(const double* A, const double* B, int lane) {
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4) {
+      const int kk = k4 * 4 + (lane & 3);
+      double a[2], b[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        a[t] = A[t * 8 + (lane >> 2) + (kk << 4)];
+        b[t] = B[kk + ((t * 8 + (lane >> 2)) << 4)];
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma884(c[i][j][0], c[i][j][1], a[i], b[j]);
+    }
+  }
+  // C -> block (neg: store -C)
+  __device__ __forceinline__ void store(double* C, int lane, bool neg) const {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          C[i * 8 + (lane >> 2) + ((j * 8 + 2 * (lane & 3) + e) << 4)] = neg ? -c[i][j][e] : c[i][j][e];
+  }
+};
+template <> struct BlockAcc16<double2> {
+  double cr[2][2][2], ci[2][2][2];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+  }
+  __device__ __forceinline__ void mma(const double2* A, const double2* B, int lane) {
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4) {
+      const int kk = k4 * 4 + (lane & 3);
+      double2 a[2], b[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        a[t] = A[t * 8 + (lane >> 2) + (kk << 4)];
+        b[t] = B[kk + ((t * 8 + (lane >> 2)) << 4)];
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma884(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
+          dmma884(cr[i][j][0], cr[i][j][1], -a[i].y, b[j].y);
+          dmma884(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
+          dmma884(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
+        }
+    }
+  }
+  __device__ __forceinline__ void store(double2* C, int lane, bool neg) const {
+    const double sg = neg ? -1.0 : 1.0;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          C[i * 8 + (lane >> 2) + ((j * 8 + 2 * (lane & 3) + e) << 4)] = make_double2(sg * cr[i][j][e], sg * ci[i][j][e]);
+  }
+};
+
 // X = L^{-1} for a lower-triangular L (unit or not) of order 16*nblk, both block-packed in smem.
-// Tb: scratch for (nblk - 1) 16x16 blocks.  All NT threads participate (NT a multiple of 256: each
-// group of 256 threads owns one 16x16 block of a level).
+// Tb: scratch for (nblk - 1) 16x16 blocks.  All NT threads participate.
 template <typename T, bool UNIT, int NT>
 __device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NWARPS = NT / 32, NGRP = NT / 256;
+  constexpr int NWARPS = NT / 32;
   // diagonal blocks: warp w inverts block w (lane c < 16 forms column c by forward substitution)
   for (int I = warp; I < nblk; I += NWARPS) {
     if (lane < 16) {
@@ -78,41 +158,28 @@ __device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
       for (int i = 0; i < 16; ++i) Xblk[i + (c << 4)] = x[i];
     }
   }
-  const int r = tid & 15, c = (tid >> 4) & 15, grp = tid >> 8;
-  for (int d = 1; d < nblk; ++d) {
-    __syncthreads();
-    // T_q = sum_{K=J}^{I-1} L_{IK} X_{KJ}   for (I, J) = (d + q, q)
-    for (int q = grp; q + d < nblk; q += NGRP) {
-      const int I = d + q, J = q;
-      T s0 = zero<T>(), s1 = zero<T>(), s2 = zero<T>(), s3 = zero<T>();  // 4 chains for ILP
-      for (int K = J; K < I; ++K) {
-        const T* Lblk = Lb + ((I * (I + 1) / 2 + K) << 8);
-        const T* Xblk = Xb + ((K * (K + 1) / 2 + J) << 8);
-#pragma unroll
-        for (int k = 0; k < 16; k += 4) {
-          s0 = madd(s0, Lblk[r + (k << 4)], Xblk[k + (c << 4)]);
-          s1 = madd(s1, Lblk[r + ((k + 1) << 4)], Xblk[k + 1 + (c << 4)]);
-          s2 = madd(s2, Lblk[r + ((k + 2) << 4)], Xblk[k + 2 + (c << 4)]);
-          s3 = madd(s3, Lblk[r + ((k + 3) << 4)], Xblk[k + 3 + (c << 4)]);
-        }
-      }
-      Tb[(q << 8) + r + (c << 4)] = add(add(s0, s1), add(s2, s3));
-    }
-    __syncthreads();
-    // X_{IJ} = -X_{II} T_q
-    for (int q = grp; q + d < nblk; q += NGRP) {
-      const int I = d + q, J = q;
-      const T* Xii = Xb + ((I * (I + 1) / 2 + I) << 8);
-      T s0 = zero<T>(), s1 = zero<T>();
-#pragma unroll
-      for (int l = 0; l < 16; l += 2) {
-        s0 = madd(s0, Xii[r + (l << 4)], Tb[(q << 8) + l + (c << 4)]);
-        s1 = madd(s1, Xii[r + ((l + 1) << 4)], Tb[(q << 8) + l + 1 + (c << 4)]);
-      }
-      Xb[((I * (I + 1) / 2 + J) << 8) + r + (c << 4)] = neg(add(s0, s1));
-    }
-  }
   __syncthreads();
+  // off-diagonal blocks, by block diagonals d = I - J (Listing-free: plain triangular inversion):
+  //   X_IJ = -X_II sum_{K=J}^{I-1} L_IK X_KJ
+  // one warp per block, both 16x16x16 products on the FP64 tensor pipe (DMMA.8x8x4)
+  for (int d = 1; d < nblk; ++d) {
+    for (int q = warp; q + d < nblk; q += NWARPS) {
+      const int I = d + q, J = q;
+      BlockAcc16<T> acc;
+      acc.zero();
+      for (int K = J; K < I; ++K)
+        acc.mma(Lb + ((I * (I + 1) / 2 + K) << 8), Xb + ((K * (K + 1) / 2 + J) << 8), lane);
+      T* Tq = Tb + (q << 8);
+      acc.store(Tq, lane, false);
+      __syncwarp();
+      BlockAcc16<T> acc2;
+      acc2.zero();
+      acc2.mma(Xb + ((I * (I + 1) / 2 + I) << 8), Tq, lane);
+      acc2.store(Xb + ((I * (I + 1) / 2 + J) << 8), lane, true);
+      __syncwarp();
+    }
+    __syncthreads();
+  }
 }
 
 template <typename T, bool HERM, int NB, int NT>
