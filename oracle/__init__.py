@@ -21,6 +21,9 @@ Pinned by ``tests/test_oracle_*.py`` (-m "not gpu"):
   * fp32 (reading R19): diag(p) closed form in fp32, brute-force law of the
                fp32 kernel, agreement with the fp64 oracle within fp32 rounding, UST and
                Aztec structure (tests/test_oracle_fp32.py).
+  * elementary sampler (Listing 2, reading R20; tests/test_oracle_elementary.py): cardinality k,
+               loglik = ln det(K_Y) (slogdet), factor = Cholesky of K_Y, brute-force law,
+               marginals, UST trees.
   * greedy MAP: K = diag(p) closed form; every decision takes the
                branch whose leading-principal-minor probability |det| is larger
                (numpy det, brute force over both branches at every pivot).
@@ -95,6 +98,9 @@ def lib():
             f = getattr(_lib, name)
             f.restype = ctypes.c_int
             f.argtypes = [ctypes.c_int64, P, ctypes.c_int64, P, ctypes.c_double, ctypes.c_double, P, P, P]
+        _lib.oracle_elementary_herm_d.restype = ctypes.c_int
+        _lib.oracle_elementary_herm_d.argtypes = [ctypes.c_int64, ctypes.c_int64, P, ctypes.c_int64, ctypes.c_uint64,
+                                                  ctypes.c_uint64, ctypes.c_double, P, P, P, P, P]
         _lib.oracle_uniform.restype = ctypes.c_double
         _lib.oracle_uniform.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64]
         _lib.oracle_philox4x32_10.restype = None
@@ -169,6 +175,36 @@ def greedy_map(kind: int, K: np.ndarray, forced=None, tie_tol: float = TIE_TOL,
         raise RuntimeError(f"oracle returned {rc}")
     return OracleResult(mask[:n].copy(), ll.value, A, info.n_kept, info.n_ties, info.first_tie,
                         info.n_out_of_range, info.min_abs_pivot, info.max_abs_imag_pivot)
+
+
+@dataclass
+class ElementaryResult:
+    order: np.ndarray      # int64[k]: chosen items (original indices) in pivot order
+    loglik: float          # sum_j ln d_{t_j} = ln det(K_Y)
+    L: np.ndarray          # n x k factor, rows by original index (L_Y = Cholesky factor of K_Y)
+    n_ties: int
+    first_tie: int
+
+    @property
+    def mask(self):
+        m = np.zeros(self.L.shape[0], dtype=np.uint8)
+        m[self.order] = 1
+        return m
+
+
+def elementary_herm_d(K: np.ndarray, k: int, seed: int = 0, b: int = 0, tie_tol: float = 1e-12) -> ElementaryResult:
+    """Listing 2 for a real rank-k projection K, reading R20."""
+    A = np.array(K, dtype=np.float64, order="F", copy=True)
+    n = A.shape[0]
+    order = np.zeros(max(k, 1), dtype=np.int64)
+    L = np.zeros((n, max(k, 1)), dtype=np.float64, order="F")
+    ll = ctypes.c_double(0.0)
+    nt, ft = ctypes.c_int32(0), ctypes.c_int32(-1)
+    rc = lib().oracle_elementary_herm_d(n, k, A.ctypes.data, max(n, 1), seed, b, tie_tol, order.ctypes.data,
+                                        L.ctypes.data, ctypes.byref(ll), ctypes.byref(nt), ctypes.byref(ft))
+    if rc != 0:
+        raise RuntimeError(f"oracle returned {rc}")
+    return ElementaryResult(order[:k].copy(), ll.value, L[:, :k], nt.value, ft.value)
 
 
 def sample_herm_d(K, seed=0, b=0, forced=None, **kw):

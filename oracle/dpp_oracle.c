@@ -328,6 +328,84 @@ int oracle_sample_lu_c(int64_t n, float* A, int64_t ld, uint64_t seed, uint64_t 
   return run_lu_c(0, n, A, ld, seed, b, forced, tie_tol, range_tol, mask, loglik, info);
 }
 
+
+/* ------------------------------------------------------------------------ */
+/* Elementary (projection) DPP sampler: Listing 2,        */
+/* Theorem "Factorization-based elementary DPP sampling": */
+/* k steps of a left-looking, diagonally pivoted Cholesky factorization of a */
+/* rank-k orthogonal projection K, each pivot drawn from the current         */
+/* diagonal with probability d_t / (k - j).                                  */
+/*                                                                            */
+/* Reading R20 (the listing permutes A and d after every draw; the law of    */
+/* the draw does not depend on the order of the candidates): no physical    */
+/* swap -- the candidates are the items not yet chosen, in ORIGINAL index    */
+/* order; with u_j the Philox uniform of pivot j (R2) and S the sum of their */
+/* d (= k - j in exact arithmetic), t is the first candidate whose running   */
+/* sum of d exceeds u_j S (if rounding leaves none, the last candidate with  */
+/* d > 0).  A draw is a tie when u_j S lies within tie_tol * S of the        */
+/* running sum just before or at t.  L is stored by original row: column j   */
+/* of the n x k array Lf holds the j-th factor column, L(t_j, j) = sqrt(d).  */
+/* The likelihood is ln prod_j A_j^2 = sum_j ln d_{t_j}.  */
+/* ------------------------------------------------------------------------ */
+int oracle_elementary_herm_d(int64_t n, int64_t k, const double* K, int64_t ld, uint64_t seed, uint64_t b,
+                             double tie_tol, int64_t* order, double* Lf, double* loglik, int32_t* n_ties,
+                             int32_t* first_tie) {
+  if (n < 0 || k < 0 || k > n || ld < (n > 1 ? n : 1)) return -1;
+  double* d = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  uint8_t* chosen = (uint8_t*)calloc((size_t)(n > 0 ? n : 1), 1);
+  if (!d || !chosen) { free(d); free(chosen); return -2; }
+#define K_(i, l) K[(size_t)(l) * (size_t)ld + (size_t)(i)]
+#define L_(i, j) Lf[(size_t)(j) * (size_t)n + (size_t)(i)]
+  for (int64_t i = 0; i < n; ++i) d[i] = K_(i, i);            /* d := diag(K) */
+  for (size_t e = 0; e < (size_t)n * (size_t)k; ++e) Lf[e] = 0.0;
+  double ll = 0.0;
+  int32_t ties = 0, ftie = -1;
+  for (int64_t j = 0; j < k; ++j) {
+    /* draw t with probability d_t / (k - j) among the candidates (R20) */
+    double S = 0.0;
+    for (int64_t i = 0; i < n; ++i)
+      if (!chosen[i]) S += d[i];
+    const double target = oracle_uniform(seed, (uint64_t)j, b) * S;
+    int64_t t = -1, last = -1;
+    double run = 0.0, before = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      if (chosen[i]) continue;
+      if (d[i] > 0.0) last = i;
+      before = run;
+      run += d[i];
+      if (run > target) { t = i; break; }
+    }
+    if (t < 0) { t = last; before = run; }
+    if (fabs(target - before) <= tie_tol * S || fabs(run - target) <= tie_tol * S) {
+      if (ties == 0) ftie = (int32_t)j;
+      ties++;
+    }
+    order[j] = t;
+    chosen[t] = 1;
+    const double Aj = sqrt(d[t]);                              /* A_j := sqrt(d_j) */
+    ll += log(d[t]);                                           /* ln A_j^2 */
+    L_(t, j) = Aj;
+    if (j == k - 1) break;
+    /* new column: A_[j+1:n], j -= A_[j+1:n], [0:j] A_j, [0:j]^H ; then / A_j; d -= |.|^2 */
+    for (int64_t i = 0; i < n; ++i) {
+      if (chosen[i]) continue;
+      double c = K_(i, t);
+      for (int64_t m = 0; m < j; ++m) c -= L_(i, m) * L_(t, m);
+      c /= Aj;
+      L_(i, j) = c;
+      d[i] -= c * c;
+    }
+  }
+#undef K_
+#undef L_
+  free(d);
+  free(chosen);
+  *loglik = ll;
+  if (n_ties) *n_ties = ties;
+  if (first_tie) *first_tie = ftie;
+  return 0;
+}
+
 /*
  * Many independent samples b = b0 .. b0+batch-1 of ONE kernel K (read-only),
  * each on a fresh copy of K.  A plain loop over the single-sample routines
