@@ -39,6 +39,7 @@ UNIT = "GFLOP/s"
 # MEASURED_PEAKS.json has no FP64 entry.  For reference: bf16 measured 1647.4 x nominal ratio
 # (37.2 / 2250) = 27.2 TF/s would be a LOWER (more flattering) denominator; we use the measured 37.1.
 FP64_PEAK_TFLOPS = 37.1
+FP32_SIMT_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4: FFMA on all SMs at the max SM clock
 PEAK_SOURCE = "measured DMMA.8x8x4 loop, profiles/r01_fp64_peak.jsonl (MEASURED_PEAKS.json has no fp64 entry)"
 
 
@@ -137,14 +138,16 @@ def main():
     ap.add_argument("--n", type=int, default=N)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="c4", choices=["c4", "ust", "dist", "dist_z", "herm_z", "lu_z", "aztec"],
+    ap.add_argument("--workload", default="c4", choices=["c4", "ust", "dist", "dist_z", "herm_z", "lu_z", "aztec", "herm_s", "aztec_c"],
                     help="c4 (default, BASELINE configs[3]); ust: configs[1] batch of UST samples per GPU; "
                          "dist / dist_z: configs[4] 1D block-column-cyclic single sample over all ranks (real n=65536 / "
                          "complex n=32768); "
                          "herm_z / lu_z: complex128 Hermitian / non-Hermitian kernels (throughput of the "
-                         "complex paths); aztec: configs[2], order-80 Aztec diamond LU sampler")
+                         "complex paths); aztec: configs[2], order-80 Aztec diamond LU sampler; herm_s / aztec_c: the "
+                         "single-precision samplers (n=16384 real; order-80 Aztec consistency, PAPER.md:1164-1169)")
     ap.add_argument("--batch", type=int, default=1024, help="ust: samples per GPU per step")
     ap.add_argument("--batch-chunk", type=int, default=256, help="ust: samples factored concurrently")
+    ap.add_argument("--aztec-d", type=int, default=80, help="aztec_c: diamond order")
     args = ap.parse_args()
     if args.workload != "c4" and args.impl == "ours":
         return extra_workload(args)
@@ -414,6 +417,68 @@ def extra_workload(args):
                     stages={k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                                 "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3)} for k, v in prof.items()},
                     pct_fp64_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), 2), clocks=clocks)
+    elif args.workload == "herm_s":
+        n = args.n
+        Kc = W.haar_kernel_torch(n, seed=KSEED, spectrum="beta").to(torch.float32)
+        opts = dpp.make_opts(nb=128, lookahead=1)
+        op = dpp.DPP_OP_HERM_S | dpp.DPP_OP_BATCHED
+        work = torch.empty(dpp.dpp_workspace_bytes(op, 1, n, opts), dtype=torch.uint8, device="cuda")
+        mask = torch.empty((1, n), dtype=torch.uint8, device="cuda")
+        ll = torch.empty(1, dtype=torch.float64, device="cuda")
+
+        def step(i):
+            dpp.dpp_sample_herm_s_batched(1, n, Kc, n, 0, SEED, rank * 1000 + i, mask, ll, None, opts, work)
+        dpp.dpp_profile_begin()
+        ms, clocks = _timed(step, args.steps, args.warmup, world, dist)
+        prof = dpp.dpp_profile_end()
+        flops = model_flops(n) * args.steps * world
+        up = prof["update_trailing"]
+        ach = up["flops"] / max(up["ms"], 1e-9) / 1e9
+        line.update(value=round(flops / (ms / 1e3) / 1e9, 2), ms_per_step=round(ms / args.steps, 3), scaling="weak",
+                    dtype="f32", samples_per_s=round(args.steps * world / (ms / 1e3), 3),
+                    config={"workload": f"single-precision real symmetric sampler on the configs[3] kernel (n={n}, "
+                                        f"Beta(1/2,1/2), rounded to fp32), one sample per GPU per step",
+                            "n": n, "nb": 128, "global_batch": world, "seq_len": None, "parallelism": f"dp{world}"},
+                    kept_last_sample=int(mask.sum()),
+                    roofline={"bound": "alu", "kernel": "update_simt_kernel<float> trailing update (b)",
+                              "achieved": round(ach, 3), "peak": FP32_SIMT_PEAK_TFLOPS, "unit": "TFLOP/s",
+                              "frac": round(ach / FP32_SIMT_PEAK_TFLOPS, 4), "traffic": None,
+                              "peak_source": "148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz (no exact-fp32 tensor MMA)"},
+                    stages={k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                                "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3)} for k, v in prof.items()},
+                    gpu_launches=int(sum(v["launches"] for v in prof.values())),
+                    pct_fp32_simt_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP32_SIMT_PEAK_TFLOPS * world), 2),
+                    clocks=clocks)
+    elif args.workload == "aztec_c":
+        # single-precision Kenyon-formula sampling "essentially always
+        # inconsistent once the diamond size exceeds 60".  Here on the balanced gauge (R13).
+        d = args.aztec_d
+        n = 4 * d * d
+        Kc = W.aztec_kernel_balanced(d, device="cuda").to(torch.complex64)
+        torch.cuda.synchronize()
+        B = args.batch if args.batch != 1024 else 8
+        opts = dpp.make_opts(nb=64, lookahead=1, batch_chunk=1)
+        op = dpp.DPP_OP_LU_C | dpp.DPP_OP_BATCHED
+        work = torch.empty(dpp.dpp_workspace_bytes(op, B, n, opts), dtype=torch.uint8, device="cuda")
+        mask = torch.empty((B, n), dtype=torch.uint8, device="cuda")
+        ll = torch.empty(B, dtype=torch.float64, device="cuda")
+
+        def step(i):
+            dpp.dpp_sample_lu_c_batched(B, n, Kc, n, 0, SEED, (rank * 1000 + i) * B, mask, ll, None, opts, work)
+        ms, clocks = _timed(step, args.steps, args.warmup, world, dist)
+        masks = mask.cpu().numpy()
+        good = sum(W.is_aztec_tiling(d, masks[b]) for b in range(B))
+        want = -d * (d + 1) / 2 * float(np.log(2.0))
+        flops = 8.0 * n ** 3 / 3.0 * B * args.steps * world
+        line.update(value=round(flops / (ms / 1e3) / 1e9, 2), ms_per_step=round(ms / args.steps, 3), scaling="weak",
+                    dtype="c64", samples_per_s=round(B * args.steps * world / (ms / 1e3), 4),
+                    config={"workload": f"single-precision (complex64) LU sampler, order-{d} Aztec diamond (n={n}), "
+                                        f"balanced-gauge Kenyon kernel, {B} samples per GPU per step",
+                            "n": n, "nb": 64, "global_batch": B * world, "seq_len": None, "parallelism": f"dp{world}"},
+                    perfect_tilings_last_step=f"{good}/{B}",
+                    max_abs_loglik_error_last_step=float(np.max(np.abs(ll.cpu().numpy() - want))),
+                    pct_fp32_simt_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP32_SIMT_PEAK_TFLOPS * world), 2),
+                    clocks=clocks)
     elif args.workload in ("herm_z", "lu_z"):
         n = args.n if args.n != N else 8192
         Kc = W.haar_kernel_torch(n, seed=KSEED, spectrum="uniform", complex_=True)

@@ -59,6 +59,7 @@ extern "C" {
 #define DPP_EUNSUPPORTED (-5)/* device is not sm_100 */
 
 typedef struct { double re, im; } dpp_complex_t;
+typedef struct { float re, im; } dpp_complex64_t;
 typedef struct CUstream_st* dpp_stream_t; /* == cudaStream_t */
 
 /* Options; pass NULL for the defaults. */
@@ -87,6 +88,8 @@ typedef struct {
 #define DPP_OP_HERM_D 0
 #define DPP_OP_HERM_Z 1
 #define DPP_OP_LU_Z 2
+#define DPP_OP_HERM_S 3     /* single precision: real symmetric (float) */
+#define DPP_OP_LU_C 4       /* single precision: complex non-Hermitian (complex64) */
 #define DPP_OP_BATCHED 0x10 /* OR-ed: batched entry point (K copied into work) */
 #define DPP_OP_HOST 0x20    /* OR-ed: _host entry point (implies a K copy in work) */
 
@@ -111,6 +114,51 @@ int dpp_sample_herm_z(int64_t n, dpp_complex_t* K, int64_t ld, uint64_t seed, ui
 int dpp_sample_lu_z(int64_t n, dpp_complex_t* K, int64_t ld, uint64_t seed, uint8_t* mask,
                     double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
                     size_t work_bytes, dpp_stream_t stream);
+
+/* ---- single precision (the paper's single-precision
+ * runs) ------------------------------------------------
+ * Same arguments, layout and semantics as dpp_sample_herm_d / dpp_sample_lu_z
+ * with float / complex64 matrices, factored in fp32 (FP32 SIMT pipe: sm_100a
+ * has no exact-fp32 tensor-core MMA).  Reading R19: the decision compares the
+ * fp64 uniform with the fp32 pivot promoted to fp64; loglik is accumulated in
+ * fp64 from the fp32 pivots.  K must be 4- (herm_s) / 8-byte (lu_c) aligned. */
+int dpp_sample_herm_s(int64_t n, float* K, int64_t ld, uint64_t seed, uint8_t* mask,
+                      double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
+                      size_t work_bytes, dpp_stream_t stream);
+int dpp_sample_lu_c(int64_t n, dpp_complex64_t* K, int64_t ld, uint64_t seed, uint8_t* mask,
+                    double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
+                    size_t work_bytes, dpp_stream_t stream);
+int dpp_sample_herm_s_batched(int64_t batch, int64_t n, const float* K, int64_t ld,
+                              int64_t strideK, uint64_t seed, uint64_t b0, uint8_t* mask,
+                              double* loglik, dpp_info_t* info, const dpp_opts_t* opts,
+                              void* work, size_t work_bytes, dpp_stream_t stream);
+int dpp_sample_lu_c_batched(int64_t batch, int64_t n, const dpp_complex64_t* K, int64_t ld,
+                            int64_t strideK, uint64_t seed, uint64_t b0, uint8_t* mask,
+                            double* loglik, dpp_info_t* info, const dpp_opts_t* opts,
+                            void* work, size_t work_bytes, dpp_stream_t stream);
+
+/* ---- elementary (projection) DPP sampler -----------------------------------
+ * Listing 2, Theorem "Factorization-based elementary DPP
+ * sampling": for K an orthogonal projection of rank k, k
+ * steps of a left-looking, diagonally pivoted Cholesky factorization whose
+ * pivot j is drawn from the current diagonal with probability d_t / (k - j);
+ * O(n k^2) instead of O(n^3).  Reading R20: candidates are the unchosen items
+ * in original index order; t_j is the first whose running sum of d exceeds
+ * u_j * sum(d) (u_j: the Philox uniform of pivot j, sample b, R2).
+ * batch independent samples b = b0 .. b0+batch-1 of ONE kernel K (DEVICE,
+ * n x n column-major, ld >= n, read-only, real symmetric; only the diagonal
+ * and the columns of the drawn items are read).
+ * order:  DEVICE int64[batch x k]: items in pivot order (row s at order + s*k)
+ * loglik: DEVICE double[batch]: sum_j ln d_{t_j} = ln det(K_Y)
+ * ties:   DEVICE int32[batch x 2] (n_ties, first_tie) or NULL: draws whose
+ *         target lay within 1e-12 * sum(d) of a candidate boundary
+ * work:   DEVICE, >= dpp_elementary_workspace_bytes(batch, n, k) (holds the
+ *         n x k factor of every sample).  k * 8 bytes <= 200 KB.
+ * Stream-ordered; 2k kernel launches. */
+size_t dpp_elementary_workspace_bytes(int64_t batch, int64_t n, int64_t k);
+int dpp_elementary_herm_d(int64_t batch, int64_t n, int64_t k, const double* K, int64_t ld,
+                          uint64_t seed, uint64_t b0, int64_t* order, double* loglik,
+                          int32_t* ties, void* work, size_t work_bytes, dpp_stream_t stream);
 
 /* ---- greedy MAP inference (in place) ----------------------------------------
  * "By replacing the Bernoulli samples of algorithm [Listing 1]

@@ -21,7 +21,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdpp_b200.so")
 
-DPP_OP_HERM_D, DPP_OP_HERM_Z, DPP_OP_LU_Z = 0, 1, 2
+DPP_OP_HERM_D, DPP_OP_HERM_Z, DPP_OP_LU_Z, DPP_OP_HERM_S, DPP_OP_LU_C = 0, 1, 2, 3, 4
 DPP_OP_BATCHED, DPP_OP_HOST = 0x10, 0x20
 INFO_BYTES = 32
 
@@ -53,13 +53,17 @@ def _sig(name, res, args):
 
 
 _sig("dpp_workspace_bytes", _SZ, [ctypes.c_int, _I64, _I64, _P])
-for _n in ("dpp_sample_herm_d", "dpp_sample_herm_z", "dpp_sample_lu_z"):
+for _n in ("dpp_sample_herm_d", "dpp_sample_herm_z", "dpp_sample_lu_z", "dpp_sample_herm_s", "dpp_sample_lu_c"):
     _sig(_n, ctypes.c_int, [_I64, _P, _I64, _U64, _P, _P, _P, _P, _P, _SZ, _P])
 for _n in ("dpp_map_herm_d", "dpp_map_herm_z", "dpp_map_lu_z"):
     _sig(_n, ctypes.c_int, [_I64, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P])
 for _n in ("dpp_sample_herm_d_batched", "dpp_sample_herm_z_batched", "dpp_sample_lu_z_batched",
+           "dpp_sample_herm_s_batched", "dpp_sample_lu_c_batched", "dpp_elementary_workspace_bytes",
+           "dpp_elementary_herm_d",
            "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host"):
     _sig(_n, ctypes.c_int, [_I64, _I64, _P, _I64, _I64, _U64, _U64, _P, _P, _P, _P, _P, _SZ, _P])
+_sig("dpp_elementary_workspace_bytes", _SZ, [_I64, _I64, _I64])
+_sig("dpp_elementary_herm_d", ctypes.c_int, [_I64, _I64, _I64, _P, _I64, _U64, _U64, _P, _P, _P, _P, _SZ, _P])
 _sig("dpp_philox_uniforms", ctypes.c_int, [_U64, _U64, _U64, _I64, _P, _P])
 _sig("dpp_comm_init", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)])
 _sig("dpp_comm_destroy", ctypes.c_int, [_P])
@@ -77,7 +81,9 @@ _sig("dpp_strerror", ctypes.c_char_p, [ctypes.c_int])
 _sig("dpp_version", ctypes.c_char_p, [])
 
 EXPORTS = ["dpp_workspace_bytes", "dpp_sample_herm_d", "dpp_sample_herm_z", "dpp_sample_lu_z",
-           "dpp_map_herm_d", "dpp_map_herm_z", "dpp_map_lu_z",
+           "dpp_map_herm_d", "dpp_map_herm_z", "dpp_map_lu_z", "dpp_sample_herm_s", "dpp_sample_lu_c",
+           "dpp_sample_herm_s_batched", "dpp_sample_lu_c_batched", "dpp_elementary_workspace_bytes",
+           "dpp_elementary_herm_d",
            "dpp_sample_herm_d_batched", "dpp_sample_herm_z_batched", "dpp_sample_lu_z_batched",
            "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host",
            "dpp_philox_uniforms", "dpp_comm_init", "dpp_comm_destroy", "dpp_bcc_local_cols",
@@ -157,6 +163,16 @@ dpp_map_herm_z = _map("dpp_map_herm_z")
 dpp_map_lu_z = _map("dpp_map_lu_z")
 
 
+def dpp_sample_herm_s(n, K, ld, seed, mask, loglik, info=None, opts=None, work=None, work_bytes=None, stream=None):
+    _check(_lib.dpp_sample_herm_s(n, _ptr(K), ld, seed, _ptr(mask), _ptr(loglik), _ptr(info), _optp(opts),
+                                  _ptr(work), work_bytes if work_bytes is not None else work.numel(), _stream(stream)))
+
+
+def dpp_sample_lu_c(n, K, ld, seed, mask, loglik, info=None, opts=None, work=None, work_bytes=None, stream=None):
+    _check(_lib.dpp_sample_lu_c(n, _ptr(K), ld, seed, _ptr(mask), _ptr(loglik), _ptr(info), _optp(opts),
+                                _ptr(work), work_bytes if work_bytes is not None else work.numel(), _stream(stream)))
+
+
 def _batched(name):
     fn = getattr(_lib, name)
 
@@ -174,6 +190,33 @@ dpp_sample_lu_z_batched = _batched("dpp_sample_lu_z_batched")
 dpp_sample_herm_d_host = _batched("dpp_sample_herm_d_host")
 dpp_sample_herm_z_host = _batched("dpp_sample_herm_z_host")
 dpp_sample_lu_z_host = _batched("dpp_sample_lu_z_host")
+dpp_sample_herm_s_batched = _batched("dpp_sample_herm_s_batched")
+dpp_sample_lu_c_batched = _batched("dpp_sample_lu_c_batched")
+
+
+def dpp_elementary_workspace_bytes(batch, n, k) -> int:
+    return int(_lib.dpp_elementary_workspace_bytes(batch, n, k))
+
+
+def dpp_elementary_herm_d(batch, n, k, K, ld, seed, b0, order, loglik, ties=None, work=None, work_bytes=None,
+                          stream=None):
+    _check(_lib.dpp_elementary_herm_d(batch, n, k, _ptr(K), ld, seed, b0, _ptr(order), _ptr(loglik), _ptr(ties),
+                                      _ptr(work), work_bytes if work_bytes is not None else work.numel(),
+                                      _stream(stream)))
+
+
+def elementary(Kc: torch.Tensor, k: int, batch: int = 1, seed: int = 0, b0: int = 0, work=None, stream=None):
+    """Elementary DPP sampler (Listing 2) for a rank-k projection kernel in column-major storage
+    Kc (n, ld): returns (order [batch, k] int64, loglik [batch], ties [batch, 2] int32)."""
+    n, ld = Kc.shape[0], Kc.shape[1]
+    dev = Kc.device
+    order = torch.empty((batch, max(k, 1)), dtype=torch.int64, device=dev)
+    ll = torch.empty(batch, dtype=torch.float64, device=dev)
+    ties = torch.empty((batch, 2), dtype=torch.int32, device=dev)
+    if work is None:
+        work = torch.empty(max(dpp_elementary_workspace_bytes(batch, n, k), 256), dtype=torch.uint8, device=dev)
+    dpp_elementary_herm_d(batch, n, k, Kc, ld, seed, b0, order, ll, ties, work, stream=stream)
+    return order[:, :k], ll, ties
 
 
 def dpp_philox_uniforms(seed, j0, b, count, u, stream=None):
@@ -255,10 +298,12 @@ def colmajor(K: torch.Tensor) -> torch.Tensor:
     return K.transpose(0, 1).contiguous()
 
 
-_OPS = {"herm_d": DPP_OP_HERM_D, "herm_z": DPP_OP_HERM_Z, "lu_z": DPP_OP_LU_Z}
-_INPLACE = {"herm_d": dpp_sample_herm_d, "herm_z": dpp_sample_herm_z, "lu_z": dpp_sample_lu_z}
+_OPS = {"herm_d": DPP_OP_HERM_D, "herm_z": DPP_OP_HERM_Z, "lu_z": DPP_OP_LU_Z, "herm_s": DPP_OP_HERM_S,
+        "lu_c": DPP_OP_LU_C}
+_INPLACE = {"herm_d": dpp_sample_herm_d, "herm_z": dpp_sample_herm_z, "lu_z": dpp_sample_lu_z,
+            "herm_s": dpp_sample_herm_s, "lu_c": dpp_sample_lu_c}
 _BATCHED = {"herm_d": dpp_sample_herm_d_batched, "herm_z": dpp_sample_herm_z_batched,
-            "lu_z": dpp_sample_lu_z_batched}
+            "lu_z": dpp_sample_lu_z_batched, "herm_s": dpp_sample_herm_s_batched, "lu_c": dpp_sample_lu_c_batched}
 
 
 def workspace(kind: str, n: int, batch: int = 1, batched: bool = False, opts=None, device="cuda"):

@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -46,6 +47,16 @@ __device__ __forceinline__ double add(double a, double b) { return a + b; }
 __device__ __forceinline__ double2 add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double neg(double a) { return -a; }
 __device__ __forceinline__ double2 neg(double2 a) { return make_double2(-a.x, -a.y); }
+__device__ __forceinline__ float madd(float c, float a, float b) { return fmaf(a, b, c); }
+__device__ __forceinline__ float2 madd(float2 c, float2 a, float2 b) {
+  float rx = fmaf(a.x, b.x, c.x);
+  rx = fmaf(-a.y, b.y, rx);
+  float ry = fmaf(a.x, b.y, c.y);
+  ry = fmaf(a.y, b.x, ry);
+  return make_float2(rx, ry);
+}
+__device__ __forceinline__ float neg(float a) { return -a; }
+__device__ __forceinline__ float2 neg(float2 a) { return make_float2(-a.x, -a.y); }
 
 // block-packed lower-triangular storage: 16x16 blocks (I >= J), column-major inside a block
 __device__ __forceinline__ int bp(int i, int k) {
@@ -134,24 +145,62 @@ template <> struct BlockAcc16<double2> {
   }
 };
 
+// Single precision has no exact tensor-core path: the same block product on the FP32 pipe, each
+// lane computing the 8 outputs it would hold as DMMA accumulators.
+template <typename T> struct BlockAccSimt {
+  T c[2][2][2];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) c[i][j][0] = c[i][j][1] = dpp::zero<T>();
+  }
+  __device__ __forceinline__ void mma(const T* A, const T* B, int lane) {
+#pragma unroll 4
+    for (int k = 0; k < 16; ++k)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const T a = A[i * 8 + (lane >> 2) + (k << 4)];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) c[i][j][e] = madd(c[i][j][e], a, B[k + ((j * 8 + 2 * (lane & 3) + e) << 4)]);
+      }
+  }
+  __device__ __forceinline__ void store(T* C, int lane, bool ng) const {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          C[i * 8 + (lane >> 2) + ((j * 8 + 2 * (lane & 3) + e) << 4)] = ng ? neg(c[i][j][e]) : c[i][j][e];
+  }
+};
+template <> struct BlockAcc16<float> : BlockAccSimt<float> {};
+template <> struct BlockAcc16<float2> : BlockAccSimt<float2> {};
+
 // X = L^{-1} for a lower-triangular L (unit or not) of order 16*nblk, both block-packed in smem.
 // Tb: scratch for (nblk - 1) 16x16 blocks.  All NT threads participate.
 template <typename T, bool UNIT, int NT>
 __device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NWARPS = NT / 32;
-  // diagonal blocks: warp w inverts block w (lane c < 16 forms column c by forward substitution)
+  // diagonal blocks: warp w inverts block w; lane c < 16 forms column c of the inverse by forward
+  // substitution in column (axpy) order -- after x[l] is final it is eliminated from all later
+  // rows at once, so the dependent chain is 16 steps long, not 120
   for (int I = warp; I < nblk; I += NWARPS) {
     if (lane < 16) {
       const int c = lane;
       const T* Lblk = Lb + ((I * (I + 1) / 2 + I) << 8);
       T x[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        T s = (i == c) ? make_real(1.0, zero<T>()) : zero<T>();
+      for (int i = 0; i < 16; ++i) x[i] = (i == c) ? make_real(1.0, zero<T>()) : zero<T>();
 #pragma unroll
-        for (int l = 0; l < i; ++l) s = fms(s, Lblk[i + (l << 4)], x[l]);
-        x[i] = UNIT ? s : mul(s, recip(Lblk[i + (i << 4)]));
+      for (int l = 0; l < 16; ++l) {
+        if (!UNIT) x[l] = mul(x[l], recip(Lblk[l + (l << 4)]));
+#pragma unroll
+        for (int i = l + 1; i < 16; ++i) x[i] = fms(x[i], Lblk[i + (l << 4)], x[l]);
       }
       T* Xblk = Xb + ((I * (I + 1) / 2 + I) << 8);
 #pragma unroll
@@ -261,7 +310,13 @@ __global__ void __launch_bounds__(NT, 1) diag_kernel(const DiagArgs a) {
   // columns, and applies the two rank-1 updates (line 439) in pivot order -- the same arithmetic,
   // operation for operation, as two single-pivot steps.  Rows/columns at or above the pivot carry
   // zeros (tile entries beyond jb are zero too), so only row/column k+1 needs a predicate.
-  for (int k = 0; k < jb; k += 2) {
+  // The pivot loop runs in phases of 16 pivots: in phase P (pivots 16P .. 16P+15) every row and
+  // column of the tile below 16P is final, so register blocks holding only such rows (ia < IA0) or
+  // columns (ib < IB0) are skipped at compile time -- each phase is its own instantiation of the
+  // step, selected by a warp-uniform switch.
+  auto step = [&](auto PC, int k) {
+    constexpr int P = decltype(PC)::value;
+    constexpr int IA0 = (16 * P) / TR, IB0 = (16 * P) / TC;
     const int cur = (k >> 1) & 1, nxt = cur ^ 1;
     const bool two = k + 1 < jb;
     const T* c0 = colbuf[cur][0];
@@ -294,7 +349,7 @@ __global__ void __launch_bounds__(NT, 1) diag_kernel(const DiagArgs a) {
     // multipliers L(i,k), L(i,k+1) (line 438) for my rows
     T L0[RA], L1[RA];
 #pragma unroll
-    for (int ia = 0; ia < RA; ++ia) {
+    for (int ia = IA0; ia < RA; ++ia) {
       const int i = tr + TR * ia;
       const T l0 = mul(c0[i], r0);
       L0[ia] = l0;
@@ -303,7 +358,7 @@ __global__ void __launch_bounds__(NT, 1) diag_kernel(const DiagArgs a) {
     // update rows for my columns: conj(w_l) or U(k, l), U(k+1, l)
     T W0[CB], W1[CB];
 #pragma unroll
-    for (int ib = 0; ib < CB; ++ib) {
+    for (int ib = IB0; ib < CB; ++ib) {
       const int l = tc + TC * ib;
       if (HERM) {
         const T w0 = c0[l];
@@ -315,17 +370,30 @@ __global__ void __launch_bounds__(NT, 1) diag_kernel(const DiagArgs a) {
         W1[ib] = (l == k + 1) ? zero<T>() : fms(rowbuf[HERM ? 0 : cur][1][l], mul(a10, r0), w0);
       }
     }
-    // two rank-1 updates (line 439), branch-free, pivot order
+    // two rank-1 updates (line 439), branch-free within the live blocks, pivot order
 #pragma unroll
-    for (int ia = 0; ia < RA; ++ia)
+    for (int ia = IA0; ia < RA; ++ia)
 #pragma unroll
-      for (int ib = 0; ib < CB; ++ib)
+      for (int ib = IB0; ib < CB; ++ib)
         if (!HERM || TC * ib <= TR * ia + TR - 1) {  // skip register blocks entirely above the diagonal
           R[ia][ib] = fms(R[ia][ib], L0[ia], W0[ib]);
           R[ia][ib] = fms(R[ia][ib], L1[ia], W1[ib]);
         }
     if (k + 2 < jb) publish(k + 2, nxt);
     __syncthreads();
+  };
+  using std::integral_constant;
+  for (int k = 0; k < jb; k += 2) {
+    switch (k >> 4) {
+      case 0: step(integral_constant<int, 0>{}, k); break;
+      case 1: if constexpr (NB > 16) step(integral_constant<int, 1>{}, k); break;
+      case 2: if constexpr (NB > 32) step(integral_constant<int, 2>{}, k); break;
+      case 3: if constexpr (NB > 48) step(integral_constant<int, 3>{}, k); break;
+      case 4: if constexpr (NB > 64) step(integral_constant<int, 4>{}, k); break;
+      case 5: if constexpr (NB > 80) step(integral_constant<int, 5>{}, k); break;
+      case 6: if constexpr (NB > 96) step(integral_constant<int, 6>{}, k); break;
+      default: if constexpr (NB > 112) step(integral_constant<int, 7>{}, k); break;
+    }
   }
 
   // ---- finalize the factor: L = (unscaled column) * (1/p), diagonal = final pivot; also stage
@@ -351,7 +419,7 @@ __global__ void __launch_bounds__(NT, 1) diag_kernel(const DiagArgs a) {
   //      shuffles; the log-likelihood terms are summed by one lane IN PIVOT ORDER
   for (int k = tid; k < jb; k += NT) {
     a.mask[(int64_t)s * a.n + a.j0 + k] = keepv[k];
-    lg[k] = log(absval(pv[k]));
+    lg[k] = log((double)absval(pv[k]));
   }
   __syncthreads();
   if (tid < 32) {
@@ -369,7 +437,7 @@ __global__ void __launch_bounds__(NT, 1) diag_kernel(const DiagArgs a) {
       noor += __popc(__ballot_sync(0xffffffffu, in && (d < -a.range_tol || d > 1.0 + a.range_tol)));
       nkept += __popc(__ballot_sync(0xffffffffu, in && keepv[k]));
       if (in) {
-        minabs = fmin(minabs, absval(pv[k]));
+        minabs = fmin(minabs, (double)absval(pv[k]));
         if (!HERM) maximag = fmax(maximag, fabs(imv[k]));
       }
     }
@@ -411,35 +479,33 @@ __global__ void __launch_bounds__(NT, 1) diag_kernel(const DiagArgs a) {
   if (HERM) {
     double* dvec = a.dvec + (int64_t)s * a.ldm;  // D1 of sample s (stride nb)
     for (int k = tid; k < jb; k += NT) dvec[k] = re(pv[k]);
-    // Bm(j,k) = delta_jk - conj(Linv(j,k)) / D(j)  (j >= k), 0 above
-    for (int idx = tid; idx < jb * jb; idx += NT) {
-      const int k = idx / jb, j = idx % jb;
-      T v = zero<T>();
-      if (j >= k) {
-        v = neg(mul(cj(Xb[bp(j, k)]), make_real(re(rv[j]), zero<T>())));
-        if (j == k) v = make_real(re(v) + 1.0, v);
+    // Bm(j,k) = delta_jk - conj(Linv(j,k)) / D(j)  (j >= k), 0 above  (column k per warp, coalesced)
+    for (int k = tid >> 5; k < jb; k += NT / 32)
+      for (int j = tid & 31; j < jb; j += 32) {
+        T v = zero<T>();
+        if (j >= k) {
+          v = neg(mul(cj(Xb[bp(j, k)]), make_real(re(rv[j]), zero<T>())));
+          if (j == k) v = make_real(re(v) + 1.0, v);
+        }
+        Bm[j + (int64_t)k * a.ldm] = v;
       }
-      Bm[j + (int64_t)k * a.ldm] = v;
-    }
   } else {
     // Am(i,k) = -Linv(i,k) (i > k), else 0
     T* Am = reinterpret_cast<T*>(a.Am) + (int64_t)s * a.strideM;
-    for (int idx = tid; idx < jb * jb; idx += NT) {
-      const int k = idx / jb, i = idx % jb;
-      Am[i + (int64_t)k * a.ldm] = (i > k) ? neg(Xb[bp(i, k)]) : zero<T>();
-    }
+    for (int k = tid >> 5; k < jb; k += NT / 32)
+      for (int i = tid & 31; i < jb; i += 32) Am[i + (int64_t)k * a.ldm] = (i > k) ? neg(Xb[bp(i, k)]) : zero<T>();
     __syncthreads();
     tri_inverse_lower<T, false, NT>(Ub, Xb, Tb, nblk);  // Xb = (U11^T)^{-1} = (U11^{-1})^T
     // Bm(j,k) = delta_jk - Uinv(k,j) = delta_jk - Xb(j,k)  (j >= k), 0 above
-    for (int idx = tid; idx < jb * jb; idx += NT) {
-      const int k = idx / jb, j = idx % jb;
-      T v = zero<T>();
-      if (j >= k) {
-        v = neg(Xb[bp(j, k)]);
-        if (j == k) v = make_real(re(v) + 1.0, v);
+    for (int k = tid >> 5; k < jb; k += NT / 32)
+      for (int j = tid & 31; j < jb; j += 32) {
+        T v = zero<T>();
+        if (j >= k) {
+          v = neg(Xb[bp(j, k)]);
+          if (j == k) v = make_real(re(v) + 1.0, v);
+        }
+        Bm[j + (int64_t)k * a.ldm] = v;
       }
-      Bm[j + (int64_t)k * a.ldm] = v;
-    }
   }
 }
 
@@ -491,6 +557,13 @@ cudaError_t launch_diag(Kind kind, int nb, const DiagArgs& a, cudaStream_t s) {
     case LU_Z:
       if (nb <= 32) return launch_diag_t<double2, false, 32>(a, s);
       return launch_diag_t<double2, false, 64>(a, s);
+    case HERM_S:
+      if (nb <= 32) return launch_diag_t<float, true, 32>(a, s);
+      if (nb <= 64) return launch_diag_t<float, true, 64>(a, s);
+      return launch_diag_t<float, true, 128>(a, s);
+    case LU_C:
+      if (nb <= 32) return launch_diag_t<float2, false, 32>(a, s);
+      return launch_diag_t<float2, false, 64>(a, s);
   }
   return cudaErrorInvalidValue;
 }

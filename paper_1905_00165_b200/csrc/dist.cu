@@ -221,7 +221,7 @@ int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* K_local, int64_t ld_lo
     }
     // every rank: W21 = L21 D1 (the update's A operand; the DMMA loop then needs no scaling)
     if (m2 > 0)
-      CK(launch_scale_cols(kind == HERM_Z, msg + M.w_off, W.ldw, 0, w + W.w_off[k & 1], W.ldw, 0,
+      CK(launch_scale_cols(kind, msg + M.w_off, W.ldw, 0, w + W.w_off[k & 1], W.ldw, 0,
                            reinterpret_cast<const double*>(msg + M.d_off), 0, (int)m2, jb, 1, s));
     return DPP_OK;
   };

@@ -41,20 +41,20 @@ struct Opts {
 };
 
 int resolve_opts(Kind kind, const dpp_opts_t* o, Opts* r) {
-  r->nb = (o && o->nb) ? o->nb : (kind == HERM_D ? 128 : 64);
+  r->nb = (o && o->nb) ? o->nb : (kind_cplx(kind) ? 64 : 128);
   r->lookahead = o ? o->lookahead : 1;
   r->tie_tol = (o && o->tie_tol > 0) ? o->tie_tol : 1e-9;
   r->range_tol = (o && o->range_tol > 0) ? o->range_tol : 1e-8;
   r->forced = o ? o->forced : nullptr;
   r->batch_chunk = o ? o->batch_chunk : 0;
   if (r->nb != 32 && r->nb != 64 && r->nb != 128) return DPP_EINVAL;
-  if (kind != HERM_D && r->nb > 64) return DPP_EINVAL;  // complex tile must fit the diag kernel
+  if (kind_cplx(kind) && r->nb > 64) return DPP_EINVAL;  // complex tile must fit the diag kernel
   if (r->lookahead < 0 || r->lookahead > 1) return DPP_EINVAL;
   if (r->batch_chunk < 0) return DPP_EINVAL;
   return DPP_OK;
 }
 
-size_t esize(Kind k) { return k == HERM_D ? 8 : 16; }
+size_t esize(Kind k) { return kind_esize(k); }
 
 // Workspace layout (all regions 256-byte aligned):
 //   [SampleState x chunk]
@@ -79,9 +79,9 @@ WsLayout layout(Kind kind, int64_t chunk, int64_t n, int nb, bool copies, bool h
   L.state_off = off; off = align_up(off + sizeof(SampleState) * (size_t)chunk);
   L.bm_off = off; off = align_up(off + (size_t)chunk * L.strideM * es);
   L.am_off = off;
-  if (kind == LU_Z) off = align_up(off + (size_t)chunk * L.strideM * es);
+  if (!kind_herm(kind)) off = align_up(off + (size_t)chunk * L.strideM * es);
   L.d_off = off;
-  if (kind != LU_Z) off = align_up(off + 2 * (size_t)chunk * nb * 8);
+  if (kind_herm(kind)) off = align_up(off + 2 * (size_t)chunk * nb * 8);
   L.ut_off = off;  // LU: U12^T; Hermitian: W21 (same shape)
   off = align_up(off + 2 * (size_t)chunk * (size_t)L.strideU * es);
   L.k_off = off;
@@ -160,11 +160,11 @@ struct ProfScope {  // brackets one launch with events on its stream
   ~ProfScope() { if (e1) cudaEventRecord(e1, s); }
 };
 
-double cplx_mult(Kind k) { return k == HERM_D ? 1.0 : 4.0; }
+double cplx_mult(Kind k) { return kind_cplx(k) ? 4.0 : 1.0; }
 // algorithmic flops of a Hermitian update region (lower elements only) or an LU rectangle
 double region_flops(Kind kind, int64_t row0, int64_t col0, int64_t rows, int64_t cols, int K) {
   double elems;
-  if (kind == LU_Z) {
+  if (!kind_herm(kind)) {
     elems = (double)rows * (double)cols;
   } else {
     elems = 0;  // count (i, j) with i >= j, i in [row0, row0+rows), j in [col0, col0+cols)
@@ -230,10 +230,11 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     CK(cudaStreamWaitEvent(s2, ds->ev_start, 0));
   }
   const size_t es = esize(kind);
-  const bool herm = kind != LU_Z;
+  const bool herm = kind_herm(kind);
   char* Ab = reinterpret_cast<char*>(A);
-  const bool vec = kind != HERM_D || ((ld % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
-                                      (strideA % 2 == 0));
+  // 16-byte aligned columns: the TMA / cp.async 16-byte operand paths
+  const bool vec = ((size_t)ld * es) % 16 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0 &&
+                   ((size_t)strideA * es) % 16 == 0;
   void* Bm = work + L.bm_off;
   void* Am = work + L.am_off;
   int step = 0;
@@ -274,7 +275,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
         // U12 = L11^-1 A12 = A12 - Am A12 (Am = I - L11^-1), computed transposed so that every
         // operand is K-major:  U12^T = A12^T - A12^T Am^T  in the U12^T buffer, then copied back.
         char* A12 = Ab + (size_t)(j0 + j1 * ld) * es;
-        { ProfScope pa(4, 0.0, s1); CK(launch_transpose_z(A12, ld, strideA, UT, L.ldk, strideU, jb, (int)m2, batch, s1)); }
+        { ProfScope pa(4, 0.0, s1); CK(launch_transpose(es, A12, ld, strideA, UT, L.ldk, strideU, jb, (int)m2, batch, s1)); }
         UpdateArgs q = base_update(kind, batch, vec);
         q.Aop = UT; q.lda = L.ldk; q.strideA = strideU;                            // A12^T (j, k)
         q.Bop = Am; q.ldb = nb; q.strideB = L.strideM;                             // Am (i, k)
@@ -283,7 +284,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
         q.row0 = 0; q.col0 = 0; q.rows = (int)m2; q.cols = jb;
         CK(launch_update(kind, q, s1));
         ProfScope pa(4, 0.0, s1);
-        CK(launch_transpose_z(UT, L.ldk, strideU, A12, ld, strideA, (int)m2, jb, batch, s1));  // U12 -> K
+        CK(launch_transpose(es, UT, L.ldk, strideU, A12, ld, strideA, (int)m2, jb, batch, s1));  // U12 -> K
       }
     }
     // ---- stage 3 operands
@@ -292,7 +293,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     if (herm) {
       // A22 -= W21 L21^H with W21 = L21 D1 (pre-scaled copy; the DMMA loop does no scaling)
       ProfScope pa(4, 0.0, s1);
-      CK(launch_scale_cols(kind == HERM_Z, Ab + (size_t)(j1 + j0 * ld) * es, ld, strideA, UT, L.ldk, strideU, dvec,
+      CK(launch_scale_cols(kind, Ab + (size_t)(j1 + j0 * ld) * es, ld, strideA, UT, L.ldk, strideU, dvec,
                            nb, (int)m2, jb, batch, s1));
       u.Aop = UT; u.lda = L.ldk; u.strideA = strideU;  // W21
       u.Bop = Ab + (size_t)(j1 + j0 * ld) * es; u.ldb = ld; u.strideB = strideA;  // L21 (conjugated on load)
@@ -331,7 +332,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       UpdateArgs ub = u;
       ub.row0 = jn; ub.col0 = jn; ub.rows = (int)(m2 - jn); ub.cols = (int)(m2 - jn);
       ub.tri = herm;
-      if (vec) ub.grid_limit = sms - reserve_sms(m2, jn, sms, batch, kind == HERM_D ? 128 : 64, herm);
+      if (vec) ub.grid_limit = sms - reserve_sms(m2, jn, sms, batch, kind_cplx(kind) ? 64 : 128, herm);
       {
         ProfScope ps(3, region_flops(kind, jn, jn, m2 - jn, m2 - jn, jb) * batch, s2);
         CK(launch_update(kind, ub, s2));
@@ -367,7 +368,7 @@ int sample_inplace(Kind kind, int64_t n, void* K, int64_t ld, uint64_t seed, uin
   if ((rc = check_device())) return rc;
   WsLayout L = layout(kind, 1, n, o.nb, false, false);
   if (!work || work_bytes < L.total || reinterpret_cast<uintptr_t>(work) % ALIGN) return DPP_EWORKSPACE;
-  if (kind != HERM_D && reinterpret_cast<uintptr_t>(K) % 16) return DPP_EINVAL;
+  if (reinterpret_cast<uintptr_t>(K) % esize(kind)) return DPP_EINVAL;
   return run_blocked(kind, o, n, K, ld, 0, 1, seed, 0, mask, o.forced, loglik, info, reinterpret_cast<char*>(work),
                      L, st, map);
 }
@@ -395,7 +396,7 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
   // triangle, so only it is moved: device sources with one batched copy kernel, host sources with
   // one 2-D DMA copy per 128-column block of rows [c, n) -- about half the bytes of the full
   // matrix (this halves the host->device time of the _host entry points).
-  const bool lower = kind != LU_Z;
+  const bool lower = kind_herm(kind);
   auto h2d = [&](char* dst, const char* src) -> int {
     if (!lower) {
       CK(cudaMemcpy2DAsync(dst, (size_t)L.ldk * es, src, (size_t)ld * es, (size_t)n * es, (size_t)n, ck, st));
@@ -417,7 +418,7 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
         if ((rc = h2d(Kc, reinterpret_cast<const char*>(K)))) return rc;
         ProfScope pa(4, 0.0, st);
         if (cb > 1)
-          CK(launch_copy_matrix(kind != HERM_D, Kc, L.ldk, 0, Kc + (size_t)L.strideK * es, L.ldk, L.strideK, (int)n,
+          CK(launch_copy_matrix(es, Kc, L.ldk, 0, Kc + (size_t)L.strideK * es, L.ldk, L.strideK, (int)n,
                                 cb - 1, lower, st));
       } else if (host) {
         for (int s = 0; s < cb; ++s)
@@ -425,7 +426,7 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
                         reinterpret_cast<const char*>(K) + (size_t)(strideK * (c0 + s)) * es))) return rc;
       } else {
         ProfScope pa(4, 0.0, st);
-        CK(launch_copy_matrix(kind != HERM_D, reinterpret_cast<const char*>(K) + (size_t)(strideK * c0) * es, ld,
+        CK(launch_copy_matrix(es, reinterpret_cast<const char*>(K) + (size_t)(strideK * c0) * es, ld,
                               strideK, Kc, L.ldk, L.strideK, (int)n, cb, lower, st));
       }
     }
@@ -450,8 +451,8 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
 extern "C" {
 
 size_t dpp_workspace_bytes(int op, int64_t batch, int64_t n, const dpp_opts_t* opts) {
-  const Kind kind = (Kind)(op & 0x3);
-  if ((op & 0x3) == 3 || n < 0 || batch < 0) return 0;
+  if ((op & 0x7) > 4 || n < 0 || batch < 0) return 0;
+  const Kind kind = (Kind)(op & 0x7);
   Opts o;
   if (resolve_opts(kind, opts, &o)) return 0;
   const bool batched = (op & (DPP_OP_BATCHED | DPP_OP_HOST)) != 0;
@@ -473,6 +474,16 @@ int dpp_sample_herm_z(int64_t n, dpp_complex_t* K, int64_t ld, uint64_t seed, ui
 int dpp_sample_lu_z(int64_t n, dpp_complex_t* K, int64_t ld, uint64_t seed, uint8_t* mask, double* loglik,
                     dpp_info_t* info, const dpp_opts_t* opts, void* work, size_t work_bytes, dpp_stream_t stream) {
   return sample_inplace(LU_Z, n, K, ld, seed, mask, loglik, info, opts, work, work_bytes, (cudaStream_t)stream);
+}
+
+// single precision (reading R19)
+int dpp_sample_herm_s(int64_t n, float* K, int64_t ld, uint64_t seed, uint8_t* mask, double* loglik,
+                      dpp_info_t* info, const dpp_opts_t* opts, void* work, size_t work_bytes, dpp_stream_t stream) {
+  return sample_inplace(HERM_S, n, K, ld, seed, mask, loglik, info, opts, work, work_bytes, (cudaStream_t)stream);
+}
+int dpp_sample_lu_c(int64_t n, dpp_complex64_t* K, int64_t ld, uint64_t seed, uint8_t* mask, double* loglik,
+                    dpp_info_t* info, const dpp_opts_t* opts, void* work, size_t work_bytes, dpp_stream_t stream) {
+  return sample_inplace(LU_C, n, K, ld, seed, mask, loglik, info, opts, work, work_bytes, (cudaStream_t)stream);
 }
 
 // greedy MAP inference: the same blocked factorization, decisions Re p >= 1/2
@@ -502,6 +513,8 @@ BATCHED(dpp_sample_lu_z_batched, LU_Z, dpp_complex_t, false)
 BATCHED(dpp_sample_herm_d_host, HERM_D, double, true)
 BATCHED(dpp_sample_herm_z_host, HERM_Z, dpp_complex_t, true)
 BATCHED(dpp_sample_lu_z_host, LU_Z, dpp_complex_t, true)
+BATCHED(dpp_sample_herm_s_batched, HERM_S, float, false)
+BATCHED(dpp_sample_lu_c_batched, LU_C, dpp_complex64_t, false)
 #undef BATCHED
 
 int dpp_philox_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, double* u, dpp_stream_t stream) {

@@ -1,11 +1,15 @@
 // kernels.h -- internal launch interface between the host driver and the kernels.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace dpp {
 
-enum Kind { HERM_D = 0, HERM_Z = 1, LU_Z = 2 };
+enum Kind { HERM_D = 0, HERM_Z = 1, LU_Z = 2, HERM_S = 3, LU_C = 4 };  // _S/_C: single precision
+inline bool kind_herm(Kind k) { return k == HERM_D || k == HERM_Z || k == HERM_S; }
+inline bool kind_cplx(Kind k) { return k == HERM_Z || k == LU_Z || k == LU_C; }
+inline size_t kind_esize(Kind k) { return k == HERM_S ? 4 : (k == HERM_D || k == LU_C) ? 8 : 16; }
 
 // Stage 1: sequential sample-and-factor of the jb x jb diagonal tile at (j0, j0)
 // (Listing 4 line "subsample, A_J1 = unblocked_dpp(A_J1)"), followed by the
@@ -72,16 +76,18 @@ struct UpdateArgs {
 
 cudaError_t launch_diag(Kind kind, int nb, const DiagArgs& a, cudaStream_t s);
 cudaError_t launch_update(Kind kind, UpdateArgs a, cudaStream_t s);
-// dst(j, k) = src(k, j) for k < rows, j < cols (complex128), `batch` matrices at the given strides:
-// the LU row panel A12 / U12 (jb x m2, N-major as a GEMM operand) <-> its K-major transpose.
-cudaError_t launch_transpose_z(const void* src, int64_t lds, int64_t strideS, void* dst, int64_t ldd,
-                               int64_t strideD, int rows, int cols, int batch, cudaStream_t s);
-// W(i, k) = L(i, k) d[k] (i < rows, k < cols), real or complex, `batch` panels at the given strides
-cudaError_t launch_scale_cols(bool cplx, const void* L, int64_t ldl, int64_t strideL, void* W, int64_t ldw,
+cudaError_t launch_update_simt(Kind kind, UpdateArgs a, cudaStream_t s);  // single precision
+// dst(j, k) = src(k, j) for k < rows, j < cols (elements of es = 8 or 16 bytes), `batch` matrices at
+// the given strides: the LU row panel A12 / U12 (jb x m2, N-major as a GEMM operand) <-> its K-major
+// transpose.
+cudaError_t launch_transpose(size_t es, const void* src, int64_t lds, int64_t strideS, void* dst, int64_t ldd,
+                             int64_t strideD, int rows, int cols, int batch, cudaStream_t s);
+// W(i, k) = L(i, k) d[k] (i < rows, k < cols), any kind's element type, `batch` panels at the given strides
+cudaError_t launch_scale_cols(Kind kind, const void* L, int64_t ldl, int64_t strideL, void* W, int64_t ldw,
                               int64_t strideW, const double* d, int64_t strideD, int rows, int cols, int batch,
                               cudaStream_t s);
-// dst <- src for `batch` n x n column-major matrices (lower: rows >= column only)
-cudaError_t launch_copy_matrix(bool cplx, const void* src, int64_t lds, int64_t strideS, void* dst, int64_t ldd,
+// dst <- src for `batch` n x n column-major matrices of es-byte elements (lower: rows >= column only)
+cudaError_t launch_copy_matrix(size_t es, const void* src, int64_t lds, int64_t strideS, void* dst, int64_t ldd,
                                int64_t strideD, int n, int batch, bool lower, cudaStream_t s);
 cudaError_t launch_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, double* u, cudaStream_t s);
 cudaError_t launch_zero_state(void* state, double* loglik, void* info, int batch, cudaStream_t s);

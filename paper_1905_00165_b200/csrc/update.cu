@@ -192,17 +192,20 @@ __global__ void __launch_bounds__(256) scale_cols_kernel(const T* L, int64_t ldl
   for (int i = blockIdx.x * 256 + threadIdx.x; i < rows; i += gridDim.x * 256) dst[i] = scal(src[i], dk);
 }
 
-cudaError_t launch_scale_cols(bool cplx, const void* L, int64_t ldl, int64_t strideL, void* W, int64_t ldw,
+cudaError_t launch_scale_cols(Kind kind, const void* L, int64_t ldl, int64_t strideL, void* W, int64_t ldw,
                               int64_t strideW, const double* d, int64_t strideD, int rows, int cols, int batch,
                               cudaStream_t s) {
   if (rows <= 0 || cols <= 0 || batch <= 0) return cudaSuccess;
   dim3 grid((unsigned)std::min<int64_t>((rows + 255) / 256, 16), cols, batch);
-  if (cplx)
-    scale_cols_kernel<double2><<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(L), ldl, strideL,
-                                                    reinterpret_cast<double2*>(W), ldw, strideW, d, strideD, rows, cols);
-  else
-    scale_cols_kernel<double><<<grid, 256, 0, s>>>(reinterpret_cast<const double*>(L), ldl, strideL,
-                                                   reinterpret_cast<double*>(W), ldw, strideW, d, strideD, rows, cols);
+#define DPP_SC(T) scale_cols_kernel<T><<<grid, 256, 0, s>>>(reinterpret_cast<const T*>(L), ldl, strideL, \
+      reinterpret_cast<T*>(W), ldw, strideW, d, strideD, rows, cols)
+  switch (kind) {
+    case HERM_D: DPP_SC(double); break;
+    case HERM_Z: case LU_Z: DPP_SC(double2); break;
+    case HERM_S: DPP_SC(float); break;
+    case LU_C: DPP_SC(float2); break;
+  }
+#undef DPP_SC
   return cudaGetLastError();
 }
 
@@ -217,28 +220,28 @@ __global__ void __launch_bounds__(256) copy_matrix_kernel(const T* src, int64_t 
   for (int i = (lower ? (int)j : 0) + threadIdx.x; i < n; i += 256) b[i] = a[i];
 }
 
-cudaError_t launch_copy_matrix(bool cplx, const void* src, int64_t lds, int64_t strideS, void* dst, int64_t ldd,
+cudaError_t launch_copy_matrix(size_t es, const void* src, int64_t lds, int64_t strideS, void* dst, int64_t ldd,
                                int64_t strideD, int n, int batch, bool lower, cudaStream_t s) {
   if (n <= 0 || batch <= 0) return cudaSuccess;
   dim3 grid(n, batch);
-  if (cplx)
-    copy_matrix_kernel<double2><<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(src), lds, strideS,
-                                                     reinterpret_cast<double2*>(dst), ldd, strideD, n, lower);
-  else
-    copy_matrix_kernel<double><<<grid, 256, 0, s>>>(reinterpret_cast<const double*>(src), lds, strideS,
-                                                    reinterpret_cast<double*>(dst), ldd, strideD, n, lower);
+#define DPP_CP(T) copy_matrix_kernel<T><<<grid, 256, 0, s>>>(reinterpret_cast<const T*>(src), lds, strideS, \
+      reinterpret_cast<T*>(dst), ldd, strideD, n, lower)
+  if (es == 4) DPP_CP(float);
+  else if (es == 8) DPP_CP(double);
+  else DPP_CP(double2);
+#undef DPP_CP
   return cudaGetLastError();
 }
 
 // 32 x 32 tiles through shared memory: coalesced 16-byte reads of src columns and dst columns.
-__global__ void __launch_bounds__(256) transpose_z_kernel(const double2* src, int64_t lds, int64_t strideS,
-                                                          double2* dst, int64_t ldd, int64_t strideD, int rows,
-                                                          int cols) {
-  __shared__ double2 t[32][33];
+template <typename T>
+__global__ void __launch_bounds__(256) transpose_kernel(const T* src, int64_t lds, int64_t strideS, T* dst,
+                                                        int64_t ldd, int64_t strideD, int rows, int cols) {
+  __shared__ T t[32][33];
   const int s = blockIdx.z;
   const int k0 = blockIdx.x * 32, j0 = blockIdx.y * 32;  // src rows k (< rows), src cols j (< cols)
-  const double2* S = src + (int64_t)s * strideS;
-  double2* D = dst + (int64_t)s * strideD;
+  const T* S = src + (int64_t)s * strideS;
+  T* D = dst + (int64_t)s * strideD;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   for (int jj = ty; jj < 32; jj += 8) {
     const int k = k0 + tx, j = j0 + jj;
@@ -251,12 +254,16 @@ __global__ void __launch_bounds__(256) transpose_z_kernel(const double2* src, in
   }
 }
 
-cudaError_t launch_transpose_z(const void* src, int64_t lds, int64_t strideS, void* dst, int64_t ldd,
-                               int64_t strideD, int rows, int cols, int batch, cudaStream_t s) {
+cudaError_t launch_transpose(size_t es, const void* src, int64_t lds, int64_t strideS, void* dst, int64_t ldd,
+                             int64_t strideD, int rows, int cols, int batch, cudaStream_t s) {
   if (rows <= 0 || cols <= 0 || batch <= 0) return cudaSuccess;
   dim3 grid((rows + 31) / 32, (cols + 31) / 32, batch);
-  transpose_z_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(src), lds, strideS,
-                                          reinterpret_cast<double2*>(dst), ldd, strideD, rows, cols);
+  if (es == 16)
+    transpose_kernel<double2><<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(src), lds, strideS,
+                                                   reinterpret_cast<double2*>(dst), ldd, strideD, rows, cols);
+  else
+    transpose_kernel<float2><<<grid, 256, 0, s>>>(reinterpret_cast<const float2*>(src), lds, strideS,
+                                                  reinterpret_cast<float2*>(dst), ldd, strideD, rows, cols);
   return cudaGetLastError();
 }
 
@@ -265,6 +272,7 @@ cudaError_t launch_transpose_z(const void* src, int64_t lds, int64_t strideS, vo
 static int g_force_generic = -1;
 cudaError_t launch_update(Kind kind, UpdateArgs a, cudaStream_t s) {
   if (a.rows <= 0 || a.cols <= 0 || a.K <= 0) return cudaSuccess;
+  if (kind == HERM_S || kind == LU_C) return launch_update_simt(kind, a, s);
   if (g_force_generic < 0) {
     const char* e = getenv("DPP_UPDATE_GENERIC");  // test hook: exercise the generic kernel
     g_force_generic = (e && e[0] == '1') ? 1 : 0;

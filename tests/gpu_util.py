@@ -5,7 +5,8 @@ import numpy as np
 import torch
 
 KIND_DT = {"herm_d": (np.float64, torch.float64), "herm_z": (np.complex128, torch.complex128),
-           "lu_z": (np.complex128, torch.complex128)}
+           "lu_z": (np.complex128, torch.complex128), "herm_s": (np.float32, torch.float32),
+           "lu_c": (np.complex64, torch.complex64)}
 FACTOR_TOL = 1e-9     # north_star: factor entries within 1e-9 relative to max|K|
 LOGLIK_TOL = 1e-10    # north_star: log-likelihood within 1e-10 relative
 
@@ -38,7 +39,7 @@ def compare_masks(gpu_mask: np.ndarray, o) -> int:
 
 def factor_part(F: np.ndarray, kind: str) -> np.ndarray:
     """The entries the sampler owns: lower triangle for Hermitian kinds, all for LU."""
-    if kind == "lu_z":
+    if kind in ("lu_z", "lu_c"):
         return F
     return np.tril(F)
 
