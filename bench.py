@@ -138,16 +138,18 @@ def main():
     ap.add_argument("--n", type=int, default=N)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="c4", choices=["c4", "ust", "dist", "dist_z", "herm_z", "lu_z", "aztec", "herm_s", "aztec_c"],
+    ap.add_argument("--workload", default="c4", choices=["c4", "ust", "dist", "dist_z", "herm_z", "lu_z", "aztec", "herm_s", "aztec_c", "elementary"],
                     help="c4 (default, BASELINE configs[3]); ust: configs[1] batch of UST samples per GPU; "
                          "dist / dist_z: configs[4] 1D block-column-cyclic single sample over all ranks (real n=65536 / "
                          "complex n=32768); "
                          "herm_z / lu_z: complex128 Hermitian / non-Hermitian kernels (throughput of the "
                          "complex paths); aztec: configs[2], order-80 Aztec diamond LU sampler; herm_s / aztec_c: the "
-                         "single-precision samplers (n=16384 real; order-80 Aztec consistency, PAPER.md:1164-1169)")
+                         "single-precision samplers (n=16384 real; order-80 Aztec consistency, PAPER.md:1164-1169); "
+                         "elementary: Listing 2 on a rank-k projection, n=5000 (the paper's Fig. setting)")
     ap.add_argument("--batch", type=int, default=1024, help="ust: samples per GPU per step")
     ap.add_argument("--batch-chunk", type=int, default=256, help="ust: samples factored concurrently")
     ap.add_argument("--aztec-d", type=int, default=80, help="aztec_c: diamond order")
+    ap.add_argument("--rank", type=int, default=500, help="elementary: projection rank k")
     args = ap.parse_args()
     if args.workload != "c4" and args.impl == "ours":
         return extra_workload(args)
@@ -479,6 +481,40 @@ def extra_workload(args):
                     max_abs_loglik_error_last_step=float(np.max(np.abs(ll.cpu().numpy() - want))),
                     pct_fp32_simt_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP32_SIMT_PEAK_TFLOPS * world), 2),
                     clocks=clocks)
+    elif args.workload == "elementary":
+        # Listing 2: rank-k projection of order n = 5000 (the paper's elementary
+        # sampler figure: ranks 10..500), a batch of independent samples per GPU per step
+        n = args.n if args.n != N else 5000
+        k = args.rank
+        B = args.batch if args.batch != 1024 else 64
+        g = torch.Generator(device="cuda"); g.manual_seed(KSEED)
+        G = torch.randn(n, k, generator=g, device="cuda", dtype=torch.float64)
+        Q, _ = torch.linalg.qr(G)
+        Kc = (Q @ Q.T).contiguous()  # symmetric: column-major storage == row-major
+        del G, Q
+        order = torch.empty((B, k), dtype=torch.int64, device="cuda")
+        ll = torch.empty(B, dtype=torch.float64, device="cuda")
+        work = torch.empty(dpp.dpp_elementary_workspace_bytes(B, n, k), dtype=torch.uint8, device="cuda")
+
+        def step(i):
+            dpp.dpp_elementary_herm_d(B, n, k, Kc, n, SEED, (rank * 1000 + i) * B, order, ll, None, work)
+        ms, clocks = _timed(step, args.steps, args.warmup, world, dist)
+        flops = n * k * k / 3.0 * B * args.steps * world  # the paper's elementary count (n k^2 / 3)
+        # algorithmic bytes: the factor reads of every column step, sum_j 8 (n - j) j, + K columns
+        byts = sum(8.0 * (n - j) * j + 8.0 * n for j in range(k)) * B * args.steps * world
+        gbs = byts / (ms / 1e3) / 1e9
+        peak_hbm = _hbm_peak()
+        line.update(value=round(flops / (ms / 1e3) / 1e9, 2), ms_per_step=round(ms / args.steps, 3), scaling="weak",
+                    dtype="f64", samples_per_s=round(B * args.steps * world / (ms / 1e3), 2),
+                    config={"workload": f"elementary DPP sampler (Listing 2) on a rank-{k} projection kernel, "
+                                        f"n={n}, {B} samples per GPU per step", "n": n, "rank": k,
+                            "global_batch": B * world, "seq_len": None, "parallelism": f"dp{world}"},
+                    roofline={"bound": "hbm", "kernel": "elem_column_kernel (factor-column GEMVs)",
+                              "achieved": round(gbs, 1), "peak": peak_hbm, "unit": "GB/s",
+                              "frac": round(gbs / peak_hbm, 4), "traffic": None,
+                              "note": "the per-sample factor (n x k x 8 B) is L2-resident for small k"},
+                    gpu_launches=int(2 * k * args.steps),
+                    clocks=clocks)
     elif args.workload in ("herm_z", "lu_z"):
         n = args.n if args.n != N else 8192
         Kc = W.haar_kernel_torch(n, seed=KSEED, spectrum="uniform", complex_=True)
@@ -551,6 +587,13 @@ def extra_workload(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6541.8
 
 
 def _shared_uid(dist, rank):
