@@ -24,6 +24,9 @@ Pinned by ``tests/test_oracle_*.py`` (-m "not gpu"):
   * elementary sampler (Listing 2, reading R20; tests/test_oracle_elementary.py): cardinality k,
                loglik = ln det(K_Y) (slogdet), factor = Cholesky of K_Y, brute-force law,
                marginals, UST trees.
+  * L-ensemble conversion K = I - (L+I)^{-1} (tests/test_oracle_lensemble.py):
+               eigenvalue map lambda / (1 + lambda), special cases, and the DPP law of the
+               converted kernel vs the L-ensemble's det(L_S) / det(L + I) by brute force.
   * greedy MAP: K = diag(p) closed form; every decision takes the
                branch whose leading-principal-minor probability |det| is larger
                (numpy det, brute force over both branches at every pivot).
@@ -205,6 +208,18 @@ def elementary_herm_d(K: np.ndarray, k: int, seed: int = 0, b: int = 0, tie_tol:
     if rc != 0:
         raise RuntimeError(f"oracle returned {rc}")
     return ElementaryResult(order[:k].copy(), ll.value, L[:, :k], nt.value, ft.value)
+
+
+def lensemble_to_marginal(L: np.ndarray):
+    """K = I - (L + I)^{-1} (Gillenwater 2014) for a Hermitian PSD L-ensemble
+    kernel -- the plain definition with a library inverse (fp64), plus ln det(L + I).  Not the
+    paper's algorithm (which the GPU path follows: factorization, triangular inverse, product)."""
+    L = np.asarray(L)
+    n = L.shape[0]
+    M = L + np.eye(n, dtype=L.dtype)
+    K = np.eye(n, dtype=L.dtype) - np.linalg.inv(M)
+    sign, logdet = np.linalg.slogdet(M)
+    return K, float(logdet)
 
 
 def sample_herm_d(K, seed=0, b=0, forced=None, **kw):
