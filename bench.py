@@ -138,18 +138,20 @@ def main():
     ap.add_argument("--n", type=int, default=N)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="c4", choices=["c4", "ust", "dist", "dist_z", "herm_z", "lu_z", "aztec", "herm_s", "aztec_c", "elementary"],
+    ap.add_argument("--workload", default="c4", choices=["c4", "ust", "dist", "dist_z", "herm_z", "lu_z", "aztec", "herm_s", "aztec_c", "elementary", "lensemble"],
                     help="c4 (default, BASELINE configs[3]); ust: configs[1] batch of UST samples per GPU; "
                          "dist / dist_z: configs[4] 1D block-column-cyclic single sample over all ranks (real n=65536 / "
                          "complex n=32768); "
                          "herm_z / lu_z: complex128 Hermitian / non-Hermitian kernels (throughput of the "
                          "complex paths); aztec: configs[2], order-80 Aztec diamond LU sampler; herm_s / aztec_c: the "
                          "single-precision samplers (n=16384 real; order-80 Aztec consistency, PAPER.md:1164-1169); "
-                         "elementary: Listing 2 on a rank-k projection, n=5000 (the paper's Fig. setting)")
+                         "elementary: Listing 2 on a rank-k projection, n=5000 (the paper's Fig. setting); lensemble: "
+                         "K = I - (L+I)^{-1} at n=16384")
     ap.add_argument("--batch", type=int, default=1024, help="ust: samples per GPU per step")
     ap.add_argument("--batch-chunk", type=int, default=256, help="ust: samples factored concurrently")
     ap.add_argument("--aztec-d", type=int, default=80, help="aztec_c: diamond order")
     ap.add_argument("--rank", type=int, default=500, help="elementary: projection rank k")
+    ap.add_argument("--lookahead", type=int, default=1, help="ust: 0 = single stream")
     args = ap.parse_args()
     if args.workload != "c4" and args.impl == "ours":
         return extra_workload(args)
@@ -365,7 +367,7 @@ def extra_workload(args):
         K = W.ust_kernel(40, 40)
         Kc = torch.from_numpy(np.ascontiguousarray(K.T)).cuda()
         B = args.batch
-        opts = dpp.make_opts(nb=128, lookahead=1, batch_chunk=min(B, args.batch_chunk))
+        opts = dpp.make_opts(nb=128, lookahead=args.lookahead, batch_chunk=min(B, args.batch_chunk))
         op = dpp.DPP_OP_HERM_D | dpp.DPP_OP_BATCHED
         work = torch.empty(dpp.dpp_workspace_bytes(op, B, n, opts), dtype=torch.uint8, device="cuda")
         mask = torch.empty((B, n), dtype=torch.uint8, device="cuda")
@@ -381,7 +383,7 @@ def extra_workload(args):
                     dtype="f64", samples_per_s=round(B * args.steps * world / (ms / 1e3), 2),
                     config={"workload": f"BASELINE configs[1]: UST of the 40x40 grid (n=3120, rank 1599), {B} "
                                         f"independent samples per GPU per step", "n": n, "global_batch": B * world,
-                            "nb": 128, "batch_chunk": min(B, args.batch_chunk), "seq_len": None,
+                            "nb": 128, "batch_chunk": min(B, args.batch_chunk), "lookahead": args.lookahead, "seq_len": None,
                             "parallelism": f"dp{world} (independent samples)"},
                     all_samples_are_spanning_trees_with_1599_edges=ok,
                     pct_fp64_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), 2), clocks=clocks)
@@ -514,6 +516,36 @@ def extra_workload(args):
                               "frac": round(gbs / peak_hbm, 4), "traffic": None,
                               "note": "the per-sample factor (n x k x 8 B) is L2-resident for small k"},
                     gpu_launches=int(2 * k * args.steps),
+                    clocks=clocks)
+    elif args.workload == "lensemble":
+        # L-ensemble -> marginal conversion, "3 samples worth of time"
+        n = args.n
+        Lc0 = W.haar_kernel_torch(n, seed=KSEED, spectrum="uniform") * 10.0  # PSD L, eigenvalues in [0, 10)
+        Lc = torch.empty_like(Lc0)
+        logdet = torch.empty((), dtype=torch.float64, device="cuda")
+        work = torch.empty(dpp.dpp_lensemble_workspace_bytes(n), dtype=torch.uint8, device="cuda")
+        copy_ms = 0.0
+
+        def step(i):
+            Lc.copy_(Lc0)
+            dpp.dpp_lensemble_to_marginal_d(n, Lc, n, logdet, work)
+        ms, clocks = _timed(step, args.steps, args.warmup, world, dist)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            Lc.copy_(Lc0)
+        e1.record()
+        torch.cuda.synchronize()
+        copy_ms = e0.elapsed_time(e1)
+        flops = float(n) ** 3 * args.steps * world  # LDL^T + triangular inverse + product: 3 x n^3/3
+        line.update(value=round(flops / ((ms - copy_ms) / 1e3) / 1e9, 2), ms_per_step=round(ms / args.steps, 3),
+                    scaling="weak", dtype="f64",
+                    config={"workload": f"L-ensemble -> marginal kernel K = I - (L+I)^-1, n={n} real symmetric, "
+                                        f"L = Q diag(10 u) Q^T; value excludes the per-step restore copy",
+                            "n": n, "global_batch": world, "seq_len": None, "parallelism": f"dp{world}"},
+                    restore_copy_ms_per_step=round(copy_ms / args.steps, 3),
+                    conversion_ms=round((ms - copy_ms) / args.steps, 3),
+                    pct_fp64_peak=round(100 * flops / ((ms - copy_ms) / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), 2),
                     clocks=clocks)
     elif args.workload in ("herm_z", "lu_z"):
         n = args.n if args.n != N else 8192

@@ -59,10 +59,12 @@ for _n in ("dpp_map_herm_d", "dpp_map_herm_z", "dpp_map_lu_z"):
     _sig(_n, ctypes.c_int, [_I64, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P])
 for _n in ("dpp_sample_herm_d_batched", "dpp_sample_herm_z_batched", "dpp_sample_lu_z_batched",
            "dpp_sample_herm_s_batched", "dpp_sample_lu_c_batched", "dpp_elementary_workspace_bytes",
-           "dpp_elementary_herm_d",
+           "dpp_elementary_herm_d", "dpp_lensemble_workspace_bytes", "dpp_lensemble_to_marginal_d",
            "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host"):
     _sig(_n, ctypes.c_int, [_I64, _I64, _P, _I64, _I64, _U64, _U64, _P, _P, _P, _P, _P, _SZ, _P])
 _sig("dpp_elementary_workspace_bytes", _SZ, [_I64, _I64, _I64])
+_sig("dpp_lensemble_workspace_bytes", _SZ, [_I64])
+_sig("dpp_lensemble_to_marginal_d", ctypes.c_int, [_I64, _P, _I64, _P, _P, _SZ, _P])
 _sig("dpp_elementary_herm_d", ctypes.c_int, [_I64, _I64, _I64, _P, _I64, _U64, _U64, _P, _P, _P, _P, _SZ, _P])
 _sig("dpp_philox_uniforms", ctypes.c_int, [_U64, _U64, _U64, _I64, _P, _P])
 _sig("dpp_comm_init", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)])
@@ -83,7 +85,7 @@ _sig("dpp_version", ctypes.c_char_p, [])
 EXPORTS = ["dpp_workspace_bytes", "dpp_sample_herm_d", "dpp_sample_herm_z", "dpp_sample_lu_z",
            "dpp_map_herm_d", "dpp_map_herm_z", "dpp_map_lu_z", "dpp_sample_herm_s", "dpp_sample_lu_c",
            "dpp_sample_herm_s_batched", "dpp_sample_lu_c_batched", "dpp_elementary_workspace_bytes",
-           "dpp_elementary_herm_d",
+           "dpp_elementary_herm_d", "dpp_lensemble_workspace_bytes", "dpp_lensemble_to_marginal_d",
            "dpp_sample_herm_d_batched", "dpp_sample_herm_z_batched", "dpp_sample_lu_z_batched",
            "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host",
            "dpp_philox_uniforms", "dpp_comm_init", "dpp_comm_destroy", "dpp_bcc_local_cols",
@@ -217,6 +219,26 @@ def elementary(Kc: torch.Tensor, k: int, batch: int = 1, seed: int = 0, b0: int 
         work = torch.empty(max(dpp_elementary_workspace_bytes(batch, n, k), 256), dtype=torch.uint8, device=dev)
     dpp_elementary_herm_d(batch, n, k, Kc, ld, seed, b0, order, ll, ties, work, stream=stream)
     return order[:, :k], ll, ties
+
+
+def dpp_lensemble_workspace_bytes(n) -> int:
+    return int(_lib.dpp_lensemble_workspace_bytes(n))
+
+
+def dpp_lensemble_to_marginal_d(n, A, ld, logdet=None, work=None, work_bytes=None, stream=None):
+    _check(_lib.dpp_lensemble_to_marginal_d(n, _ptr(A), ld, _ptr(logdet), _ptr(work),
+                                            work_bytes if work_bytes is not None else work.numel(), _stream(stream)))
+
+
+def lensemble_to_marginal(Lc: torch.Tensor, work=None, stream=None):
+    """K = I - (L + I)^{-1} in place on the lower triangle of the column-major storage Lc (n, ld);
+    returns ln det(L + I) as a 0-d device tensor."""
+    n, ld = Lc.shape[0], Lc.shape[1]
+    logdet = torch.empty((), dtype=torch.float64, device=Lc.device)
+    if work is None:
+        work = torch.empty(max(dpp_lensemble_workspace_bytes(n), 256), dtype=torch.uint8, device=Lc.device)
+    dpp_lensemble_to_marginal_d(n, Lc, ld, logdet, work, stream=stream)
+    return logdet
 
 
 def dpp_philox_uniforms(seed, j0, b, count, u, stream=None):

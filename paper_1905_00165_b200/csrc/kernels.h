@@ -65,6 +65,8 @@ struct UpdateArgs {
   int mask, conj, bnmajor;
   const double* dscale; // per-k scale of B (Hermitian trailing update: D1), stride dstride per sample
   int64_t dstride;
+  int ktri;             // 1: A(i, k) = 0 for k < i (upper-triangular A): a tile starts its K loop at
+                        //    its first row (fast kernel only; the others just multiply the zeros)
   int grid_limit;       // > 0: persistent launch with at most this many CTAs (SMs left to the
                         //      lookahead stream); 0: short-lived CTAs (<= 4 tiles each)
   // 1D block-column-cyclic mode (bcc_P > 0, BN == nb): tile column tj is local block

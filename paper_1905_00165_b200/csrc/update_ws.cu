@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
       const int arows = min(C::BM, a.a_rows - ti.grow0);   // operand rows that exist
       const int bcols = min(C::BN, a.b_rows - ti.gcol0);
       const int abulk = CPLX ? arows : (arows & ~1), bbulk = CPLX ? bcols : (bcols & ~1);
-      for (int kc = 0; kc < nchunks; ++kc) {
+      for (int kc = a.ktri ? ti.grow0 / C::KC : 0; kc < nchunks; ++kc) {
         mbar_wait(&empty[stage], phase ^ 1);
         T* As = ring + stage * LY::STAGE_ELEMS;
         T* Bs = As + LY::A_ELEMS;
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
     if (!ti.valid) continue;
     MmaAcc<CPLX, MI, NI> acc;
     acc.zero();
-    for (int kc = 0; kc < nchunks; ++kc) {
+    for (int kc = a.ktri ? ti.grow0 / C::KC : 0; kc < nchunks; ++kc) {
       mbar_wait(&full[stage], phase);
       const T* As = ring + stage * LY::STAGE_ELEMS;
       mma_chunk<CPLX, BNMAJ, SCALE, CONJ, C::KC, MI, NI, LY::LDA, LY::LDBK, LY::LDBN>(
