@@ -194,8 +194,7 @@ int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile, bool herm) {
   int best = 8;
   double best_t = 1e300;
   for (int R = 4; R <= sms / 2; R += 2) {
-    // the batch's diag tiles (one CTA each, ~5 tile times) share the R SMs with (a) and the panel
-    const double t1 = diag_tiles * (double)((batch + R - 1) / R) + (ta + tp) / R;
+    const double t1 = diag_tiles + (ta + tp) / R;
     const double t2 = tb / (sms - R);
     const double t = t1 > t2 ? t1 : t2;
     if (t < best_t) { best_t = t; best = R; }
