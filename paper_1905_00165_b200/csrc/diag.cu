@@ -352,7 +352,13 @@ static cudaError_t launch_diag_t(const DiagArgs& a, cudaStream_t s) {
   return launch_diag_nt<T, HERM, NB, 256>(a, s);
 }
 
+cudaError_t launch_diag_herm_blocked(Kind kind, int nb, const DiagArgs& a, cudaStream_t s);
+
 cudaError_t launch_diag(Kind kind, int nb, const DiagArgs& a, cudaStream_t s) {
+  if (kind == HERM_D || kind == HERM_Z) {
+    const cudaError_t e = launch_diag_herm_blocked(kind, nb, a, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   switch (kind) {
     case HERM_D:
       if (nb <= 32) return launch_diag_t<double, true, 32>(a, s);

@@ -50,14 +50,14 @@ template <> struct BlockAcc16<double> {
 #pragma unroll
       for (int j = 0; j < 2; ++j) c[i][j][0] = c[i][j][1] = 0.0;
   }
-  __device__ __forceinline__ void mma(const double* A, const double* B, int lane) {
+  __device__ __forceinline__ void mma(const double* A, const double* B, int lane, int lda = 16) {
 #pragma unroll
     for (int k4 = 0; k4 < 4; ++k4) {
       const int kk = k4 * 4 + (lane & 3);
       double a[2], b[2];
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        a[t] = A[t * 8 + (lane >> 2) + (kk << 4)];
+        a[t] = A[t * 8 + (lane >> 2) + kk * lda];
         b[t] = B[kk + ((t * 8 + (lane >> 2)) << 4)];
       }
 #pragma unroll
@@ -85,14 +85,14 @@ template <> struct BlockAcc16<double2> {
 #pragma unroll
       for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
   }
-  __device__ __forceinline__ void mma(const double2* A, const double2* B, int lane) {
+  __device__ __forceinline__ void mma(const double2* A, const double2* B, int lane, int lda = 16) {
 #pragma unroll
     for (int k4 = 0; k4 < 4; ++k4) {
       const int kk = k4 * 4 + (lane & 3);
       double2 a[2], b[2];
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        a[t] = A[t * 8 + (lane >> 2) + (kk << 4)];
+        a[t] = A[t * 8 + (lane >> 2) + kk * lda];
         b[t] = B[kk + ((t * 8 + (lane >> 2)) << 4)];
       }
 #pragma unroll
@@ -128,12 +128,12 @@ template <typename T> struct BlockAccSimt {
 #pragma unroll
       for (int j = 0; j < 2; ++j) c[i][j][0] = c[i][j][1] = dpp::zero<T>();
   }
-  __device__ __forceinline__ void mma(const T* A, const T* B, int lane) {
+  __device__ __forceinline__ void mma(const T* A, const T* B, int lane, int lda = 16) {
 #pragma unroll 4
     for (int k = 0; k < 16; ++k)
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const T a = A[i * 8 + (lane >> 2) + (k << 4)];
+        const T a = A[i * 8 + (lane >> 2) + k * lda];
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -153,10 +153,11 @@ template <typename T> struct BlockAccSimt {
 template <> struct BlockAcc16<float> : BlockAccSimt<float> {};
 template <> struct BlockAcc16<float2> : BlockAccSimt<float2> {};
 
-// X = L^{-1} for a lower-triangular L (unit or not) of order 16*nblk, both block-packed in smem.
-// Tb: scratch for (nblk - 1) 16x16 blocks.  All NT threads participate.
-template <typename T, bool UNIT, int NT>
-__device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
+// X = L^{-1} for a lower-triangular L (unit or not) of order 16*nblk; X block-packed in smem, L
+// given by a block accessor Lblk(I, K) -> pointer to its 16x16 block (I >= K), element (i, k) at
+// [i + k * ldl].  Tb: scratch for (nblk - 1) 16x16 blocks.  All NT threads participate.
+template <typename T, bool UNIT, int NT, class LBlk>
+__device__ void tri_inverse_lower_g(LBlk Lblk_of, int ldl, T* Xb, T* Tb, int nblk) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NWARPS = NT / 32;
   // diagonal blocks: warp w inverts block w; lane c < 16 forms column c of the inverse by forward
@@ -165,15 +166,15 @@ __device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
   for (int I = warp; I < nblk; I += NWARPS) {
     if (lane < 16) {
       const int c = lane;
-      const T* Lblk = Lb + ((I * (I + 1) / 2 + I) << 8);
+      const T* Lblk = Lblk_of(I, I);
       T x[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) x[i] = (i == c) ? make_real(1.0, zero<T>()) : zero<T>();
 #pragma unroll
       for (int l = 0; l < 16; ++l) {
-        if (!UNIT) x[l] = mul(x[l], recip(Lblk[l + (l << 4)]));
+        if (!UNIT) x[l] = mul(x[l], recip(Lblk[l + l * ldl]));
 #pragma unroll
-        for (int i = l + 1; i < 16; ++i) x[i] = fms(x[i], Lblk[i + (l << 4)], x[l]);
+        for (int i = l + 1; i < 16; ++i) x[i] = fms(x[i], Lblk[i + l * ldl], x[l]);
       }
       T* Xblk = Xb + ((I * (I + 1) / 2 + I) << 8);
 #pragma unroll
@@ -181,7 +182,7 @@ __device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
     }
   }
   __syncthreads();
-  // off-diagonal blocks, by block diagonals d = I - J (Listing-free: plain triangular inversion):
+  // off-diagonal blocks, by block diagonals d = I - J (plain triangular inversion):
   //   X_IJ = -X_II sum_{K=J}^{I-1} L_IK X_KJ
   // one warp per block, both 16x16x16 products on the FP64 tensor pipe (DMMA.8x8x4)
   for (int d = 1; d < nblk; ++d) {
@@ -189,8 +190,7 @@ __device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
       const int I = d + q, J = q;
       BlockAcc16<T> acc;
       acc.zero();
-      for (int K = J; K < I; ++K)
-        acc.mma(Lb + ((I * (I + 1) / 2 + K) << 8), Xb + ((K * (K + 1) / 2 + J) << 8), lane);
+      for (int K = J; K < I; ++K) acc.mma(Lblk_of(I, K), Xb + ((K * (K + 1) / 2 + J) << 8), lane, ldl);
       T* Tq = Tb + (q << 8);
       acc.store(Tq, lane, false);
       __syncwarp();
@@ -202,6 +202,13 @@ __device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
     }
     __syncthreads();
   }
+}
+
+// the same with L block-packed in smem
+template <typename T, bool UNIT, int NT>
+__device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
+  tri_inverse_lower_g<T, UNIT, NT>([=](int I, int K) { return Lb + ((I * (I + 1) / 2 + K) << 8); }, 16, Xb, Tb,
+                                   nblk);
 }
 
 }  // namespace dpp

@@ -210,12 +210,13 @@ def test_large_parity_2048(oracle_mod):
         assert_loglik_close(float(s.loglik), o.loglik)
 
 
-@pytest.mark.parametrize("env", [{"DPP_UPDATE_GENERIC": "1"}, {"DPP_WS_VARIANT": "0"}, {"DPP_DIAG_NT": "256"},
-                                 {"DPP_DIAG_NT": "512"}])
+@pytest.mark.parametrize("env", [{"DPP_UPDATE_GENERIC": "1"}, {"DPP_WS_VARIANT": "0"}, {"DPP_DIAG_NT": "512"},
+                                 {"DPP_DIAG_BLOCKED": "1"}])
 def test_alternate_update_kernels_subprocess(env):
-    """The cp.async fallback update kernel (forced with DPP_UPDATE_GENERIC=1) and the 8-consumer-
-    warp layout of the warp-specialized kernel (DPP_WS_VARIANT=0) give the same samples and
-    factors as the oracle for all three kinds (each run in a fresh process)."""
+    """The cp.async fallback update kernel (DPP_UPDATE_GENERIC=1), the 8-consumer-warp layout of
+    the warp-specialized kernel (DPP_WS_VARIANT=0), the 512-thread register-tile diag kernel
+    (DPP_DIAG_NT=512) and the 32-column-blocked Hermitian diag kernel (DPP_DIAG_BLOCKED=1) give the same
+    samples and factors as the oracle for all three kinds (each run in a fresh process)."""
     import os
     import subprocess
     import sys
