@@ -30,6 +30,9 @@ template <> struct WsCfg<false, 0> {  // real: 128x128 tile, consumer warps 2(M)
 template <> struct WsCfg<false, 1> {  // real: 128x128 tile, 16 consumer warps 4 x 4 of 32x32
   static constexpr int BM = 128, BN = 128, WM = 4, WN = 4, KC = 8, STAGES = 5;
 };
+template <> struct WsCfg<false, 2> {  // real: 64x128 tile, 8 consumer warps 2 x 4 of 32x32, 2 CTAs per SM
+  static constexpr int BM = 64, BN = 128, WM = 2, WN = 4, KC = 8, STAGES = 3;
+};
 template <> struct WsCfg<true, 0> {   // complex: 64x64 tile, consumer warps 2 x 4 of 32x16
   static constexpr int BM = 64, BN = 64, WM = 2, WN = 4, KC = 8, STAGES = 4;
 };
@@ -65,7 +68,7 @@ __device__ __forceinline__ void consumer_sync(int nthreads) {
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
 template <bool CPLX, bool BNMAJ, bool MASK, bool SCALE, bool CONJ, int V>
-__global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_kernel(const UpdateArgs a) {
+__global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, (V == 2) ? 2 : 1) update_ws_kernel(const UpdateArgs a) {
   using LY = WsLayoutT<CPLX, BNMAJ, V>;
   using C = WsCfg<CPLX, V>;
   using T = typename LY::T;
@@ -258,6 +261,8 @@ cudaError_t launch_update_ws_v(UpdateArgs a, cudaStream_t s) {
   using C = WsCfg<CPLX, V>;
   using LY = WsLayoutT<CPLX, BNMAJ, V>;
   if (a.rows <= 0 || a.cols <= 0 || a.K <= 0) return cudaSuccess;
+  constexpr int CPS = (C::BM == C::BN) ? 1 : 2;  // CTAs per SM (rectangular tiles: 2)
+  if (C::BM != C::BN) a.tri = 0;                 // rectangular tiles: rectangular enumeration, masked
   a.tiles_m = (a.rows + C::BM - 1) / C::BM;
   if (a.bcc_P == 0) a.tiles_n = (a.cols + C::BN - 1) / C::BN;
   const long long per = a.tri ? (long long)a.tiles_m * (a.tiles_m + 1) / 2 : (long long)a.tiles_m * a.tiles_n;
@@ -271,10 +276,11 @@ cudaError_t launch_update_ws_v(UpdateArgs a, cudaStream_t s) {
   }
   long long g;
   if (a.grid_limit > 0) {
-    g = total < a.grid_limit ? total : a.grid_limit;  // persistent over the CTAs granted
+    const long long lim = (long long)a.grid_limit * CPS;
+    g = total < lim ? total : lim;  // persistent over the CTAs granted
   } else {
     g = (total + TPC - 1) / TPC;
-    if (g < num_sms()) g = total < num_sms() ? total : num_sms();
+    if (g < num_sms() * CPS) g = total < num_sms() * CPS ? total : num_sms() * CPS;
   }
   auto* fn = update_ws_kernel<CPLX, BNMAJ, MASK, SCALE, CONJ, V>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LY::SMEM);
@@ -289,7 +295,7 @@ static int ws_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("DPP_WS_VARIANT");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '0') ? 0 : (e && e[0] == '2') ? 2 : 1;
   }
   return v;
 }
@@ -298,6 +304,7 @@ template <bool CPLX, bool BNMAJ, bool MASK, bool SCALE, bool CONJ>
 cudaError_t launch_update_ws_t(UpdateArgs a, cudaStream_t s) {
   if constexpr (!CPLX) {
     if (ws_variant() == 1) return launch_update_ws_v<CPLX, BNMAJ, MASK, SCALE, CONJ, 1>(a, s);
+    if (ws_variant() == 2) return launch_update_ws_v<CPLX, BNMAJ, MASK, SCALE, CONJ, 2>(a, s);
   }
   return launch_update_ws_v<CPLX, BNMAJ, MASK, SCALE, CONJ, 0>(a, s);
 }
