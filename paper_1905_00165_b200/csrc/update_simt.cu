@@ -9,7 +9,7 @@
 //   * one CTA of 512 threads (4 warps per SM sub-partition) per 256x128 (real) / 128x64 (complex)
 //     tile, 8x8 (4x4 complex) outputs per thread in registers, split in two halves so the fragment
 //     loads are 16-byte vector loads;
-//   * persistent CTAs (one per SM, the SMs of the lookahead stream left free); K-chunks of 16 (8
+//   * persistent CTAs (one per SM, the SMs of the lookahead stream left free); K-chunks of 32 (16
 //     complex) double-buffered in shared memory with cp.async, the first chunk of the next tile
 //     prefetched while the last one of the current tile is consumed;
 //   * epilogue: read-modify-write of C straight from the registers with 16-byte accesses (masked to
@@ -24,8 +24,8 @@ namespace dpp {
 
 // 512 threads = 32 (rows) x 16 (columns); each thread TM x TN outputs in two halves of HM x HN.
 template <typename T> struct SimtCfg;
-template <> struct SimtCfg<float> { static constexpr int BM = 256, BN = 128, TM = 8, TN = 8, KC = 16; };
-template <> struct SimtCfg<float2> { static constexpr int BM = 128, BN = 64, TM = 4, TN = 4, KC = 8; };
+template <> struct SimtCfg<float> { static constexpr int BM = 256, BN = 128, TM = 8, TN = 8, KC = 32; };
+template <> struct SimtCfg<float2> { static constexpr int BM = 128, BN = 64, TM = 4, TN = 4, KC = 16; };
 constexpr int SIMT_NT = 512;
 
 __device__ __forceinline__ void cfma(float& c, float a, float b) { c = fmaf(a, b, c); }

@@ -44,3 +44,20 @@ def test_elementary_ust_gpu(oracle_mod):
         mask[order[s].cpu().numpy()] = 1
         assert W.is_spanning_tree(400, edges, mask)
         assert abs(float(ll[s]) - want) <= 1e-9 * abs(want)
+
+
+def test_elementary_edge_cases(oracle_mod):
+    """k = n (K = I: every item, loglik 0), k = 0 (empty sample), batch = 0 (no work)."""
+    n = 37
+    K = np.eye(n)
+    order, ll, ties = dpp.elementary(to_device(K, "herm_d"), n, batch=2, seed=0)
+    for s in range(2):
+        assert sorted(order[s].cpu().numpy().tolist()) == list(range(n))
+        assert abs(float(ll[s])) <= 1e-14
+    order, ll, _ = dpp.elementary(to_device(W.projection_kernel(20, 5, seed=1), "herm_d"), 0, batch=3)
+    assert order.shape == (3, 0) and np.all(ll.cpu().numpy() == 0.0)
+    work = torch.empty(256, dtype=torch.uint8, device="cuda")
+    dpp.dpp_elementary_herm_d(0, 10, 3, to_device(np.eye(10), "herm_d"), 10, 0, 0, None, None, None, work)
+    with pytest.raises(dpp.DppError):  # k > n
+        dpp.dpp_elementary_workspace_bytes(1, 4, 5) or dpp.dpp_elementary_herm_d(
+            1, 4, 5, to_device(np.eye(4), "herm_d"), 4, 0, 0, None, None, None, work)

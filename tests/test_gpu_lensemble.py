@@ -48,3 +48,19 @@ def test_lensemble_then_sample(oracle_mod):
     o = oracle_mod.sample_herm_d(K, 3, 0)
     k = o.first_tie if o.n_ties else n
     assert np.array_equal(s.mask.cpu().numpy()[:k], o.mask[:k])
+
+
+def test_lensemble_edge_cases(oracle_mod):
+    """n = 0 gives logdet 0; L = 0 gives K = 0 and logdet 0; L = c I gives c / (1 + c) I."""
+    work = torch.empty(max(dpp.dpp_lensemble_workspace_bytes(0), 256), dtype=torch.uint8, device="cuda")
+    logdet = torch.full((), 5.0, dtype=torch.float64, device="cuda")
+    A = torch.empty((1, 1), dtype=torch.float64, device="cuda")
+    dpp.dpp_lensemble_to_marginal_d(0, A, 1, logdet, work)
+    assert float(logdet) == 0.0
+    for c in (0.0, 3.0):
+        n = 200
+        Lc = to_device(c * np.eye(n), "herm_d")
+        ld = dpp.lensemble_to_marginal(Lc)
+        K = from_device(Lc, n)
+        assert np.max(np.abs(np.tril(K) - c / (1 + c) * np.eye(n))) <= 1e-14
+        assert abs(float(ld) - n * np.log1p(c)) <= 1e-10 * max(1.0, n * np.log1p(c))
