@@ -523,7 +523,7 @@ def extra_workload(args):
         Lc0 = W.haar_kernel_torch(n, seed=KSEED, spectrum="uniform") * 10.0  # PSD L, eigenvalues in [0, 10)
         Lc = torch.empty_like(Lc0)
         logdet = torch.empty((), dtype=torch.float64, device="cuda")
-        work = torch.empty(dpp.dpp_lensemble_workspace_bytes(n), dtype=torch.uint8, device="cuda")
+        work = torch.empty(dpp.dpp_lensemble_workspace_bytes(dpp.DPP_OP_HERM_D, n), dtype=torch.uint8, device="cuda")
         copy_ms = 0.0
 
         def step(i):

@@ -163,17 +163,20 @@ int dpp_elementary_herm_d(int64_t batch, int64_t n, int64_t k, const double* K, 
 /* ---- L-ensemble -> marginal kernel: K = I - (L + I)^{-1} --------------------
  * PAPER.md:1494-1498 ("converting a Hermitian L-ensemble kernel into a
  * marginal kernel via K = I - (L + I)^{-1} ... the equivalent of 3 samples
- * worth of time").  Real symmetric PSD L (DEVICE, n x n column-major, ld >= n;
- * 16-byte aligned columns take the fast kernels); the LOWER triangle of L is read and OVERWRITTEN by
- * the lower triangle of K (the strict upper triangle is not touched).
+ * worth of time").  Hermitian PSD L (DEVICE, n x n column-major, ld >= n; real
+ * fp64 (_d) or complex128 (_z, 16-byte aligned); 16-byte aligned columns take
+ * the fast kernels); the LOWER triangle of L is read and OVERWRITTEN by the
+ * lower triangle of K (the strict upper triangle is not touched).
  * Method: LDL^T of L + I with the sampler's kernels (every decision forced to
  * "keep"), inverse of the unit-lower factor by block forward substitution on
  * DMMA GEMMs, then K = I - Y D^{-1} Y^T, Y = Lf^{-T} (3 x n^3/3 flops).
  * logdet: DEVICE double[1] or NULL: ln det(L + I) (the L-ensemble's
  * normaliser).  work: DEVICE, >= dpp_lensemble_workspace_bytes(n) (~8 n^2
- * bytes).  Stream-ordered. */
-size_t dpp_lensemble_workspace_bytes(int64_t n);
+ * bytes; op = DPP_OP_HERM_D or DPP_OP_HERM_Z, 0 otherwise).  Stream-ordered. */
+size_t dpp_lensemble_workspace_bytes(int op, int64_t n);
 int dpp_lensemble_to_marginal_d(int64_t n, double* A, int64_t ld, double* logdet, void* work,
+                                size_t work_bytes, dpp_stream_t stream);
+int dpp_lensemble_to_marginal_z(int64_t n, dpp_complex_t* A, int64_t ld, double* logdet, void* work,
                                 size_t work_bytes, dpp_stream_t stream);
 
 /* ---- greedy MAP inference (in place) ----------------------------------------

@@ -60,11 +60,13 @@ for _n in ("dpp_map_herm_d", "dpp_map_herm_z", "dpp_map_lu_z"):
 for _n in ("dpp_sample_herm_d_batched", "dpp_sample_herm_z_batched", "dpp_sample_lu_z_batched",
            "dpp_sample_herm_s_batched", "dpp_sample_lu_c_batched", "dpp_elementary_workspace_bytes",
            "dpp_elementary_herm_d", "dpp_lensemble_workspace_bytes", "dpp_lensemble_to_marginal_d",
+           "dpp_lensemble_to_marginal_z",
            "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host"):
     _sig(_n, ctypes.c_int, [_I64, _I64, _P, _I64, _I64, _U64, _U64, _P, _P, _P, _P, _P, _SZ, _P])
 _sig("dpp_elementary_workspace_bytes", _SZ, [_I64, _I64, _I64])
-_sig("dpp_lensemble_workspace_bytes", _SZ, [_I64])
-_sig("dpp_lensemble_to_marginal_d", ctypes.c_int, [_I64, _P, _I64, _P, _P, _SZ, _P])
+_sig("dpp_lensemble_workspace_bytes", _SZ, [ctypes.c_int, _I64])
+for _n in ("dpp_lensemble_to_marginal_d", "dpp_lensemble_to_marginal_z"):
+    _sig(_n, ctypes.c_int, [_I64, _P, _I64, _P, _P, _SZ, _P])
 _sig("dpp_elementary_herm_d", ctypes.c_int, [_I64, _I64, _I64, _P, _I64, _U64, _U64, _P, _P, _P, _P, _SZ, _P])
 _sig("dpp_philox_uniforms", ctypes.c_int, [_U64, _U64, _U64, _I64, _P, _P])
 _sig("dpp_comm_init", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)])
@@ -86,6 +88,7 @@ EXPORTS = ["dpp_workspace_bytes", "dpp_sample_herm_d", "dpp_sample_herm_z", "dpp
            "dpp_map_herm_d", "dpp_map_herm_z", "dpp_map_lu_z", "dpp_sample_herm_s", "dpp_sample_lu_c",
            "dpp_sample_herm_s_batched", "dpp_sample_lu_c_batched", "dpp_elementary_workspace_bytes",
            "dpp_elementary_herm_d", "dpp_lensemble_workspace_bytes", "dpp_lensemble_to_marginal_d",
+           "dpp_lensemble_to_marginal_z",
            "dpp_sample_herm_d_batched", "dpp_sample_herm_z_batched", "dpp_sample_lu_z_batched",
            "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host",
            "dpp_philox_uniforms", "dpp_comm_init", "dpp_comm_destroy", "dpp_bcc_local_cols",
@@ -221,8 +224,8 @@ def elementary(Kc: torch.Tensor, k: int, batch: int = 1, seed: int = 0, b0: int 
     return order[:, :k], ll, ties
 
 
-def dpp_lensemble_workspace_bytes(n) -> int:
-    return int(_lib.dpp_lensemble_workspace_bytes(n))
+def dpp_lensemble_workspace_bytes(op, n) -> int:
+    return int(_lib.dpp_lensemble_workspace_bytes(op, n))
 
 
 def dpp_lensemble_to_marginal_d(n, A, ld, logdet=None, work=None, work_bytes=None, stream=None):
@@ -230,14 +233,21 @@ def dpp_lensemble_to_marginal_d(n, A, ld, logdet=None, work=None, work_bytes=Non
                                             work_bytes if work_bytes is not None else work.numel(), _stream(stream)))
 
 
+def dpp_lensemble_to_marginal_z(n, A, ld, logdet=None, work=None, work_bytes=None, stream=None):
+    _check(_lib.dpp_lensemble_to_marginal_z(n, _ptr(A), ld, _ptr(logdet), _ptr(work),
+                                            work_bytes if work_bytes is not None else work.numel(), _stream(stream)))
+
+
 def lensemble_to_marginal(Lc: torch.Tensor, work=None, stream=None):
-    """K = I - (L + I)^{-1} in place on the lower triangle of the column-major storage Lc (n, ld);
-    returns ln det(L + I) as a 0-d device tensor."""
+    """K = I - (L + I)^{-1} in place on the lower triangle of the column-major storage Lc (n, ld),
+    real (float64) or complex Hermitian (complex128); returns ln det(L + I) as a 0-d device tensor."""
     n, ld = Lc.shape[0], Lc.shape[1]
+    cplx = Lc.dtype == torch.complex128
+    op = DPP_OP_HERM_Z if cplx else DPP_OP_HERM_D
     logdet = torch.empty((), dtype=torch.float64, device=Lc.device)
     if work is None:
-        work = torch.empty(max(dpp_lensemble_workspace_bytes(n), 256), dtype=torch.uint8, device=Lc.device)
-    dpp_lensemble_to_marginal_d(n, Lc, ld, logdet, work, stream=stream)
+        work = torch.empty(max(dpp_lensemble_workspace_bytes(op, n), 256), dtype=torch.uint8, device=Lc.device)
+    (dpp_lensemble_to_marginal_z if cplx else dpp_lensemble_to_marginal_d)(n, Lc, ld, logdet, work, stream=stream)
     return logdet
 
 

@@ -292,6 +292,7 @@ cudaError_t launch_update(Kind kind, UpdateArgs a, cudaStream_t s) {
     if (a.bnmajor) return cudaErrorInvalidValue;
     if (a.mask && scale && a.conj) DPP_GO(true, false, true, true, true);
     if (a.mask && !scale && a.conj) DPP_GO(true, false, true, false, true);
+    if (!a.mask && !scale && a.conj) DPP_GO(true, false, false, false, true);  // L-ensemble: B conjugated
     if (!a.mask && !scale && !a.conj) DPP_GO(true, false, false, false, false);
   } else {
     if (a.mask || scale || a.conj) return cudaErrorInvalidValue;

@@ -317,5 +317,6 @@ template cudaError_t launch_update_ws_t<true, true, false, false, false>(UpdateA
 // Hermitian trailing update with a pre-scaled A operand (W21 = L21 D1): no per-k scaling
 template cudaError_t launch_update_ws_t<false, false, true, false, false>(UpdateArgs, cudaStream_t);
 template cudaError_t launch_update_ws_t<true, false, true, false, true>(UpdateArgs, cudaStream_t);
+template cudaError_t launch_update_ws_t<true, false, false, false, true>(UpdateArgs, cudaStream_t);
 
 }  // namespace dpp

@@ -14,19 +14,25 @@ if not torch.cuda.is_available():
 import paper_1905_00165_b200 as dpp  # noqa: E402
 
 
-def _lens(n, seed, scale):
+def _lens(n, seed, scale, complex_=False):
     rng = np.random.default_rng(seed)
-    V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    G = rng.standard_normal((n, n)) + (1j * rng.standard_normal((n, n)) if complex_ else 0.0)
+    V, _ = np.linalg.qr(G)
     lam = rng.uniform(0, scale, n)
-    L = (V * lam) @ V.T
-    return 0.5 * (L + L.T), lam
+    L = (V * lam) @ V.conj().T
+    L = 0.5 * (L + L.conj().T)
+    if complex_:
+        L[np.diag_indices(n)] = L.diagonal().real
+    return L, lam
 
 
-@pytest.mark.parametrize("n,scale", [(1, 3.0), (100, 10.0), (300, 10.0), (1000, 50.0), (2049, 10.0)])
-def test_lensemble_matches_oracle(oracle_mod, n, scale):
-    L, lam = _lens(n, n, scale)
+@pytest.mark.parametrize("n,scale,cplx", [(1, 3.0, False), (100, 10.0, False), (300, 10.0, False),
+                                           (1000, 50.0, False), (2049, 10.0, False), (1, 2.0, True),
+                                           (200, 10.0, True), (777, 20.0, True)])
+def test_lensemble_matches_oracle(oracle_mod, n, scale, cplx):
+    L, lam = _lens(n, n, scale, cplx)
     K, ld = oracle_mod.lensemble_to_marginal(L)
-    Lc = to_device(L, "herm_d")
+    Lc = to_device(L, "herm_z" if cplx else "herm_d")
     logdet = dpp.lensemble_to_marginal(Lc)
     torch.cuda.synchronize()
     Kg = from_device(Lc, n)
@@ -52,7 +58,7 @@ def test_lensemble_then_sample(oracle_mod):
 
 def test_lensemble_edge_cases(oracle_mod):
     """n = 0 gives logdet 0; L = 0 gives K = 0 and logdet 0; L = c I gives c / (1 + c) I."""
-    work = torch.empty(max(dpp.dpp_lensemble_workspace_bytes(0), 256), dtype=torch.uint8, device="cuda")
+    work = torch.empty(max(dpp.dpp_lensemble_workspace_bytes(dpp.DPP_OP_HERM_D, 0), 256), dtype=torch.uint8, device="cuda")
     logdet = torch.full((), 5.0, dtype=torch.float64, device="cuda")
     A = torch.empty((1, 1), dtype=torch.float64, device="cuda")
     dpp.dpp_lensemble_to_marginal_d(0, A, 1, logdet, work)
