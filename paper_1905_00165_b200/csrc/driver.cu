@@ -64,7 +64,7 @@ size_t esize(Kind k) { return kind_esize(k); }
 //   [W21 double buffer (Hermitian): 2 x chunk x ldk x nb -- the pre-scaled panel L21 D1]
 //   [K copies: chunk x ldk x n (batched / host)][host staging: mask, loglik, info (host)]
 struct WsLayout {
-  size_t state_off, bm_off, am_off, d_off, ut_off, k_off, mask_off, ll_off, info_off, total;
+  size_t state_off, bm_off, am_off, d_off, ut_off, dh_off, k_off, mask_off, ll_off, info_off, total;
   int64_t ldk, strideK, strideM, strideU;
 };
 
@@ -84,6 +84,8 @@ WsLayout layout(Kind kind, int64_t chunk, int64_t n, int nb, bool copies, bool h
   if (kind_herm(kind)) off = align_up(off + 2 * (size_t)chunk * nb * 8);
   L.ut_off = off;  // LU: U12^T; Hermitian: W21 (same shape)
   off = align_up(off + 2 * (size_t)chunk * (size_t)L.strideU * es);
+  L.dh_off = off;  // Hermitian: D of every pivot so far (chunk x n), the column-chunked schedule
+  if (kind_herm(kind)) off = align_up(off + (size_t)chunk * (size_t)std::max<int64_t>(n, 1) * 8);
   L.k_off = off;
   if (copies) off = align_up(off + (size_t)chunk * (size_t)L.strideK * es);
   L.mask_off = off;
@@ -97,10 +99,12 @@ WsLayout layout(Kind kind, int64_t chunk, int64_t n, int nb, bool copies, bool h
 }
 
 // ---------------------------------------------------------------- stream pair per device
+constexpr int MAX_CHUNKS = 64;
 struct DeviceStreams {
-  cudaStream_t s1 = nullptr, s2 = nullptr;
-  cudaEvent_t ev_start, ev_panel, ev_rest, ev_done1, ev_done2;
-  std::mutex mu;
+  cudaStream_t s1 = nullptr, s2 = nullptr, s3 = nullptr;  // s3: host->device copies of the _host path
+  cudaEvent_t ev_start, ev_panel, ev_rest, ev_done1, ev_done2, ev_delay, ev_copy_start;
+  cudaEvent_t ev_chunk[MAX_CHUNKS];
+  std::recursive_mutex mu;
   bool init = false;
 };
 DeviceStreams g_streams[64];
@@ -116,8 +120,11 @@ int get_streams(DeviceStreams** out) {
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return DPP_ECUDA;
     if (cudaStreamCreateWithPriority(&d.s1, cudaStreamNonBlocking, hi) != cudaSuccess) return DPP_ECUDA;
     if (cudaStreamCreateWithPriority(&d.s2, cudaStreamNonBlocking, lo) != cudaSuccess) return DPP_ECUDA;
-    for (cudaEvent_t* e : {&d.ev_start, &d.ev_panel, &d.ev_rest, &d.ev_done1, &d.ev_done2})
+    if (cudaStreamCreateWithPriority(&d.s3, cudaStreamNonBlocking, lo) != cudaSuccess) return DPP_ECUDA;
+    for (cudaEvent_t* e : {&d.ev_start, &d.ev_panel, &d.ev_rest, &d.ev_done1, &d.ev_done2, &d.ev_delay, &d.ev_copy_start})
       if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return DPP_ECUDA;
+    for (cudaEvent_t& e : d.ev_chunk)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return DPP_ECUDA;
     d.init = true;
   }
   *out = &d;
@@ -212,15 +219,39 @@ UpdateArgs base_update(Kind kind, int batch, bool vec) {
 
 // ---------------------------------------------------------------- the blocked factorization
 // Factors `batch` matrices A + s*strideA (in place), samples b0 + s.
+// Column-chunked schedule (Hermitian kinds, lookahead on): the factorization proceeds over column
+// chunks of cw columns; inside a chunk it is the right-looking loop below with its trailing
+// updates restricted to the chunk's columns, and each new chunk first receives every earlier
+// panel at once (one DMMA GEMM with K = c0, B scaled by the saved pivots) -- Prop. 5's exactness
+// does not depend on the update order.  A chunk can start as soon as its columns are resident:
+// the _host path copies chunk by chunk on a third stream and the chunk events gate the compute.
+struct Chunking {
+  int64_t cw = 0;               // 0: off
+  const cudaEvent_t* ev = nullptr;  // per chunk: its columns are resident (nullable)
+};
+
+// DPP_CHUNK_COLS overrides the chunk width (0 = off) of both paths; defaults: the _host path
+// pipelines its copy in chunks of 2048 columns (n >= 4096), the device paths are not chunked.
+int chunk_cols(bool host, int64_t n) {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("DPP_CHUNK_COLS");
+    v = e ? atoi(e) : -1;
+  }
+  if (v >= 0) return v;
+  return (host && n >= 4096) ? 2048 : 0;
+}
+
 int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_t strideA, int batch,
                 uint64_t seed, uint64_t b0, uint8_t* mask, const uint8_t* forced, double* loglik,
-                dpp_info_t* info, char* work, const WsLayout& L, cudaStream_t caller, bool map = false) {
+                dpp_info_t* info, char* work, const WsLayout& L, cudaStream_t caller, bool map = false,
+                Chunking ch = Chunking{}) {
   void* state = work + L.state_off;
   if (n == 0) { CK(launch_zero_state(state, loglik, info, batch, caller)); return DPP_OK; }
   DeviceStreams* ds = nullptr;
   int rc = get_streams(&ds);
   if (rc) return rc;
-  std::lock_guard<std::mutex> lk(ds->mu);
+  std::lock_guard<std::recursive_mutex> lk(ds->mu);
   const int nb = o.nb;
   const bool la = o.lookahead > 0;
   cudaStream_t s1 = la ? ds->s1 : caller, s2 = la ? ds->s2 : caller;
@@ -240,9 +271,38 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
   int step = 0;
   bool have_rest = false;
   const int sms = device_sms();
+  if (!herm || !la || ch.cw < nb || ch.cw % nb) ch.cw = 0;
+  if (ch.cw && (n + ch.cw - 1) / ch.cw > MAX_CHUNKS) ch.cw = (n + MAX_CHUNKS - 1) / MAX_CHUNKS / nb * nb + nb;
+  double* dhist = herm ? reinterpret_cast<double*>(work + L.dh_off) : nullptr;
   for (int64_t j0 = 0; j0 < n; j0 += nb, ++step) {
     const int jb = (int)std::min<int64_t>(nb, n - j0);
     const int64_t j1 = j0 + jb, m2 = n - j1;
+    const int64_t c0 = ch.cw ? (j0 / ch.cw) * ch.cw : 0;
+    const int64_t ce = ch.cw ? std::min<int64_t>(n, c0 + ch.cw) : n;  // the chunk's columns: [c0, ce)
+    if (ch.cw && j0 == c0) {
+      if (ch.ev) {
+        CK(cudaStreamWaitEvent(s1, ch.ev[j0 / ch.cw], 0));
+        CK(cudaStreamWaitEvent(s2, ch.ev[j0 / ch.cw], 0));
+      }
+      if (c0 > 0) {
+        // every earlier panel into the new chunk: A(c0:n, c0:ce) -= L(c0:n, 0:c0) D L(c0:ce, 0:c0)^H
+        CK(cudaEventRecord(ds->ev_panel, s1));
+        CK(cudaStreamWaitEvent(s2, ds->ev_panel, 0));
+        UpdateArgs dl = base_update(kind, batch, vec);
+        dl.Aop = Ab + (size_t)c0 * es; dl.lda = ld; dl.strideA = strideA;
+        dl.Bop = Ab + (size_t)c0 * es; dl.ldb = ld; dl.strideB = strideA;
+        dl.dscale = dhist; dl.dstride = n; dl.mask = 1; dl.conj = (kind == HERM_Z);
+        dl.C = Ab + (size_t)(c0 + c0 * ld) * es; dl.ldc = ld; dl.strideC = strideA;
+        dl.a_rows = (int)(n - c0); dl.b_rows = (int)(ce - c0); dl.K = (int)c0;
+        dl.row0 = 0; dl.col0 = 0; dl.rows = (int)(n - c0); dl.cols = (int)(ce - c0); dl.tri = 0;
+        {
+          ProfScope ps(3, region_flops(kind, c0, c0, n - c0, ce - c0, (int)c0) * batch, s2);
+          CK(launch_update(kind, dl, s2));
+        }
+        CK(cudaEventRecord(ds->ev_delay, s2));
+        CK(cudaStreamWaitEvent(s1, ds->ev_delay, 0));
+      }
+    }
     double* dvec = herm ? reinterpret_cast<double*>(work + L.d_off) + (size_t)(step & 1) * batch * nb : nullptr;
     // LU: U12^T (m2 x jb, ld = ldk, K-major GEMM operand); Hermitian: W21 = L21 D1 (same shape);
     // double-buffered like D1
@@ -260,6 +320,9 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       CK(launch_diag(kind, nb, d, s1));
     }
     if (m2 <= 0) break;
+    if (ch.cw && herm)  // this block's pivots, for the later chunks' catch-up updates
+      CK(cudaMemcpy2DAsync(dhist + j0, (size_t)n * 8, dvec, (size_t)nb * 8, (size_t)jb * 8, (size_t)batch,
+                           cudaMemcpyDeviceToDevice, s1));
     // ---- stage 2: panel GEMMs with the tile operators (in place)
     {
       const double fl = (herm ? 1.0 : 2.0) * (double)m2 * jb * jb * cplx_mult(kind) * batch;  // TRSM count
@@ -311,9 +374,10 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       continue;
     }
     CK(cudaEventRecord(ds->ev_panel, s1));
-    // (a) next block column [0, jn) x rows [0, m2)  (+ LU: next block row [0, jn) x cols [jn, m2))
+    // (a) next block column [0, jn) x rows [0, m2)  (+ LU: next block row [0, jn) x cols [jn, m2));
+    // chunked: only while the next block is in this chunk (else the catch-up update covers it)
     if (have_rest) CK(cudaStreamWaitEvent(s1, ds->ev_rest, 0));
-    {
+    if (j1 < ce) {
       UpdateArgs ua = u;
       ua.row0 = 0; ua.col0 = 0; ua.rows = (int)m2; ua.cols = jn; ua.tri = 0;
       double fl = region_flops(kind, 0, 0, m2, jn, jb);
@@ -326,15 +390,16 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
         CK(launch_update(kind, ur, s1));
       }
     }
-    // (b) the rest [jn, m2)^2 on S2
-    if (m2 > jn) {
+    // (b) the rest [jn, m2)^2 on S2 (chunked: its columns restricted to the chunk)
+    const int64_t colsb = std::min<int64_t>(m2, ce - j1) - jn;
+    if (m2 > jn && colsb > 0) {
       CK(cudaStreamWaitEvent(s2, ds->ev_panel, 0));
       UpdateArgs ub = u;
-      ub.row0 = jn; ub.col0 = jn; ub.rows = (int)(m2 - jn); ub.cols = (int)(m2 - jn);
-      ub.tri = herm;
+      ub.row0 = jn; ub.col0 = jn; ub.rows = (int)(m2 - jn); ub.cols = (int)colsb;
+      ub.tri = herm && colsb == m2 - jn;
       if (vec) ub.grid_limit = sms - reserve_sms(m2, jn, sms, batch, kind_cplx(kind) ? 64 : 128, herm);
       {
-        ProfScope ps(3, region_flops(kind, jn, jn, m2 - jn, m2 - jn, jb) * batch, s2);
+        ProfScope ps(3, region_flops(kind, jn, jn, m2 - jn, colsb, jb) * batch, s2);
         CK(launch_update(kind, ub, s2));
       }
       CK(cudaEventRecord(ds->ev_rest, s2));
@@ -369,8 +434,10 @@ int sample_inplace(Kind kind, int64_t n, void* K, int64_t ld, uint64_t seed, uin
   WsLayout L = layout(kind, 1, n, o.nb, false, false);
   if (!work || work_bytes < L.total || reinterpret_cast<uintptr_t>(work) % ALIGN) return DPP_EWORKSPACE;
   if (reinterpret_cast<uintptr_t>(K) % esize(kind)) return DPP_EINVAL;
+  Chunking chk;
+  chk.cw = kind_herm(kind) ? chunk_cols(false, n) : 0;
   return run_blocked(kind, o, n, K, ld, 0, 1, seed, 0, mask, o.forced, loglik, info, reinterpret_cast<char*>(work),
-                     L, st, map);
+                     L, st, map, chk);
 }
 
 int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t ld, int64_t strideK, uint64_t seed,
@@ -412,6 +479,40 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
   };
   for (int64_t c0 = 0; c0 < batch; c0 += chunk) {
     const int cb = (int)std::min<int64_t>(chunk, batch - c0);
+    const int64_t cw = (lower && cb == 1 && o.lookahead > 0) ? chunk_cols(host, n) : 0;
+    if (host && cw > 0 && n > 0) {
+      // pipelined: the copy of column chunk c (on s3) gates only chunk c of the factorization
+      DeviceStreams* ds = nullptr;
+      if ((rc = get_streams(&ds))) return rc;
+      std::lock_guard<std::recursive_mutex> lk(ds->mu);
+      CK(cudaEventRecord(ds->ev_copy_start, st));
+      CK(cudaStreamWaitEvent(ds->s3, ds->ev_copy_start, 0));
+      const char* src = reinterpret_cast<const char*>(K) + (size_t)(strideK * c0) * es;
+      int64_t cwe = cw;
+      if ((n + cwe - 1) / cwe > MAX_CHUNKS) cwe = (n + MAX_CHUNKS - 1) / MAX_CHUNKS / o.nb * o.nb + o.nb;
+      for (int64_t q0 = 0, ci = 0; q0 < n; q0 += cwe, ++ci) {
+        for (int64_t c = q0; c < std::min<int64_t>(n, q0 + cwe); c += 128) {
+          const int64_t w_ = std::min<int64_t>({(int64_t)128, n - c, q0 + cwe - c});
+          CK(cudaMemcpy2DAsync(Kc + (size_t)(c + c * L.ldk) * es, (size_t)L.ldk * es, src + (size_t)(c + c * ld) * es,
+                               (size_t)ld * es, (size_t)(n - c) * es, (size_t)w_, ck, ds->s3));
+        }
+        CK(cudaEventRecord(ds->ev_chunk[ci], ds->s3));
+      }
+      uint8_t* mk = reinterpret_cast<uint8_t*>(w + L.mask_off);
+      double* llk = reinterpret_cast<double*>(w + L.ll_off);
+      dpp_info_t* ifo = info ? reinterpret_cast<dpp_info_t*>(w + L.info_off) : nullptr;
+      const uint8_t* fz = o.forced ? o.forced + c0 * n : nullptr;
+      Chunking chk;
+      chk.cw = cwe;
+      chk.ev = ds->ev_chunk;
+      rc = run_blocked(kind, o, n, Kc, L.ldk, L.strideK, cb, seed, b0 + (uint64_t)c0, mk, fz, llk, ifo, w, L, st,
+                       false, chk);
+      if (rc) return rc;
+      CK(cudaMemcpyAsync(mask + c0 * n, mk, (size_t)cb * n, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(loglik + c0, llk, 8 * (size_t)cb, cudaMemcpyDeviceToHost, st));
+      if (info) CK(cudaMemcpyAsync(info + c0, ifo, sizeof(dpp_info_t) * (size_t)cb, cudaMemcpyDeviceToHost, st));
+      continue;
+    }
     if (n > 0) {
       if (host && strideK == 0) {
         // one host->device transfer of the shared kernel, then device-side replication
@@ -434,7 +535,10 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
     double* llk = host ? reinterpret_cast<double*>(w + L.ll_off) : loglik + c0;
     dpp_info_t* ifo = host ? (info ? reinterpret_cast<dpp_info_t*>(w + L.info_off) : nullptr) : (info ? info + c0 : nullptr);
     const uint8_t* fz = o.forced ? o.forced + c0 * n : nullptr;
-    rc = run_blocked(kind, o, n, Kc, L.ldk, L.strideK, cb, seed, b0 + (uint64_t)c0, mk, fz, llk, ifo, w, L, st);
+    Chunking chk;
+    chk.cw = cw;
+    rc = run_blocked(kind, o, n, Kc, L.ldk, L.strideK, cb, seed, b0 + (uint64_t)c0, mk, fz, llk, ifo, w, L, st, false,
+                     chk);
     if (rc) return rc;
     if (host) {
       if (n > 0) CK(cudaMemcpyAsync(mask + c0 * n, mk, (size_t)cb * n, cudaMemcpyDeviceToHost, st));

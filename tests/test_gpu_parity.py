@@ -241,3 +241,45 @@ print("GENERIC_OK")
     env = dict(os.environ, PYTHONPATH=root, **env)
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert "GENERIC_OK" in r.stdout, r.stdout + r.stderr
+
+
+def test_column_chunked_schedule_subprocess():
+    """The column-chunked schedule (DPP_CHUNK_COLS=256: right-looking inside 256-column chunks, a
+    K = c0 catch-up GEMM per chunk, and for the _host entry point the copy pipelined chunk by chunk
+    on its own stream) gives the oracle's samples and factors -- in place, batched and host
+    entry points, real and complex Hermitian (run in a fresh process)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, oracle, workloads as W, paper_1905_00165_b200 as dpp
+from tests.gpu_util import to_device, from_device, compare_masks, assert_factor_close, assert_loglik_close
+for kind, n in (("herm_d", 1000), ("herm_d", 1311), ("herm_z", 700)):
+    K = W.haar_kernel(n, seed=n, complex_=(kind != "herm_d"))
+    fn = oracle.sample_herm_d if kind == "herm_d" else oracle.sample_herm_z
+    o = fn(K, 9, 0)
+    Kc = to_device(K, kind)
+    s = dpp.sample(kind, Kc, 9)
+    torch.cuda.synchronize()
+    compare_masks(s.mask.cpu().numpy(), o)
+    if o.n_ties == 0:
+        assert_factor_close(from_device(Kc, n), o.factor, K, kind)
+        assert_loglik_close(float(s.loglik), o.loglik)
+    sb = dpp.sample_batched(kind, to_device(K, kind), 2, seed=9, b0=0)
+    compare_masks(sb.mask[0].cpu().numpy(), o)
+    if kind == "herm_d":
+        Kh = torch.from_numpy(np.ascontiguousarray(K.T)).pin_memory()
+        mh = torch.empty((1, n), dtype=torch.uint8).pin_memory()
+        lh = torch.empty(1, dtype=torch.float64).pin_memory()
+        op = dpp.DPP_OP_HERM_D | dpp.DPP_OP_HOST
+        work = torch.empty(dpp.dpp_workspace_bytes(op, 1, n), dtype=torch.uint8, device="cuda")
+        dpp.dpp_sample_herm_d_host(1, n, Kh, n, 0, 9, 0, mh, lh, None, None, work)
+        compare_masks(mh[0].numpy(), o)
+        if o.n_ties == 0:
+            assert_loglik_close(float(lh[0]), o.loglik)
+print("CHUNK_OK")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PYTHONPATH=root, DPP_CHUNK_COLS="256")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert "CHUNK_OK" in r.stdout, r.stdout + r.stderr
