@@ -228,18 +228,39 @@ UpdateArgs base_update(Kind kind, int batch, bool vec) {
 struct Chunking {
   int64_t cw = 0;               // 0: off
   const cudaEvent_t* ev = nullptr;  // per chunk: its columns are resident (nullable)
+  // copy-gated mode (the _host path's default): the factorization is NOT restricted; the copy
+  // arrives in chunks of copy_cw columns (events ev), each step's diag/panel/lookahead waits for
+  // the chunk holding its next block column, and the trailing updates of the first split_steps
+  // steps are launched per copy chunk, each waiting only for its own chunk
+  int64_t copy_cw = 0;
+  int split_steps = 0;
 };
 
-// DPP_CHUNK_COLS overrides the chunk width (0 = off) of both paths; defaults: the _host path
-// pipelines its copy in chunks of 2048 columns (n >= 4096), the device paths are not chunked.
+// DPP_CHUNK_COLS > 0 selects the column-chunked factorization (both paths; measured slower: 19.9
+// vs 25.8 TF/s at n = 16384 with 2048-column chunks -- the restricted trailing updates leave the
+// sequential chain exposed in every chunk).
 int chunk_cols(bool host, int64_t n) {
   static int v = -2;
   if (v == -2) {
     const char* e = getenv("DPP_CHUNK_COLS");
-    v = e ? atoi(e) : -1;
+    v = e ? atoi(e) : 0;
   }
-  if (v >= 0) return v;
-  return (host && n >= 4096) ? 2048 : 0;
+  (void)host;
+  (void)n;
+  return v;
+}
+
+// DPP_COPY_GATED=1: the _host path's copy-gated mode.  Off by default: measured slower (e2e 18.3
+// vs 19.3 TF/s at n = 16384) -- the right-looking order needs every column before the first
+// trailing update completes, and the work a left-looking order could do on the first columns is
+// small, so little of the copy can hide behind compute.
+bool copy_gated() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPP_COPY_GATED");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
 }
 
 int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_t strideA, int batch,
@@ -279,6 +300,14 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     const int64_t j1 = j0 + jb, m2 = n - j1;
     const int64_t c0 = ch.cw ? (j0 / ch.cw) * ch.cw : 0;
     const int64_t ce = ch.cw ? std::min<int64_t>(n, c0 + ch.cw) : n;  // the chunk's columns: [c0, ce)
+    if (ch.copy_cw && ch.ev) {
+      // copy-gated: this step's tile, panel and lookahead column need the chunk of block column
+      // j0 + 1 (and all before it -- the copies are issued in order on one stream)
+      const int64_t need = std::min<int64_t>(n - 1, j1 + nb - 1);
+      CK(cudaStreamWaitEvent(s1, ch.ev[need / ch.copy_cw], 0));
+      // past the split steps the trailing updates are single launches: the whole copy must be in
+      if (step == ch.split_steps) CK(cudaStreamWaitEvent(s2, ch.ev[(n - 1) / ch.copy_cw], 0));
+    }
     if (ch.cw && j0 == c0) {
       if (ch.ev) {
         CK(cudaStreamWaitEvent(s1, ch.ev[j0 / ch.cw], 0));
@@ -398,7 +427,18 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       ub.row0 = jn; ub.col0 = jn; ub.rows = (int)(m2 - jn); ub.cols = (int)colsb;
       ub.tri = herm && colsb == m2 - jn;
       if (vec) ub.grid_limit = sms - reserve_sms(m2, jn, sms, batch, kind_cplx(kind) ? 64 : 128, herm);
-      {
+      if (ch.copy_cw && ch.ev && step < ch.split_steps) {
+        // one launch per copy chunk of the trailing columns, each gated by its own chunk
+        for (int64_t g0 = j1 + jn; g0 < j1 + jn + colsb;) {
+          const int64_t g1 = std::min<int64_t>(j1 + jn + colsb, (g0 / ch.copy_cw + 1) * ch.copy_cw);
+          CK(cudaStreamWaitEvent(s2, ch.ev[(g1 - 1) / ch.copy_cw], 0));
+          UpdateArgs up = ub;
+          up.col0 = (int)(g0 - j1); up.cols = (int)(g1 - g0); up.tri = 0;
+          ProfScope ps(3, region_flops(kind, jn, g0 - j1, m2 - jn, g1 - g0, jb) * batch, s2);
+          CK(launch_update(kind, up, s2));
+          g0 = g1;
+        }
+      } else {
         ProfScope ps(3, region_flops(kind, jn, jn, m2 - jn, colsb, jb) * batch, s2);
         CK(launch_update(kind, ub, s2));
       }
@@ -480,7 +520,8 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
   for (int64_t c0 = 0; c0 < batch; c0 += chunk) {
     const int cb = (int)std::min<int64_t>(chunk, batch - c0);
     const int64_t cw = (lower && cb == 1 && o.lookahead > 0) ? chunk_cols(host, n) : 0;
-    if (host && cw > 0 && n > 0) {
+    const bool gated = host && lower && cb == 1 && o.lookahead > 0 && n >= 4096 && copy_gated();
+    if (host && (cw > 0 || gated) && n > 0) {
       // pipelined: the copy of column chunk c (on s3) gates only chunk c of the factorization
       DeviceStreams* ds = nullptr;
       if ((rc = get_streams(&ds))) return rc;
@@ -488,7 +529,7 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
       CK(cudaEventRecord(ds->ev_copy_start, st));
       CK(cudaStreamWaitEvent(ds->s3, ds->ev_copy_start, 0));
       const char* src = reinterpret_cast<const char*>(K) + (size_t)(strideK * c0) * es;
-      int64_t cwe = cw;
+      int64_t cwe = cw > 0 ? cw : 2048;
       if ((n + cwe - 1) / cwe > MAX_CHUNKS) cwe = (n + MAX_CHUNKS - 1) / MAX_CHUNKS / o.nb * o.nb + o.nb;
       for (int64_t q0 = 0, ci = 0; q0 < n; q0 += cwe, ++ci) {
         for (int64_t c = q0; c < std::min<int64_t>(n, q0 + cwe); c += 128) {
@@ -503,8 +544,23 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
       dpp_info_t* ifo = info ? reinterpret_cast<dpp_info_t*>(w + L.info_off) : nullptr;
       const uint8_t* fz = o.forced ? o.forced + c0 * n : nullptr;
       Chunking chk;
-      chk.cw = cwe;
       chk.ev = ds->ev_chunk;
+      if (cw > 0) {
+        chk.cw = cwe;
+      } else {
+        // copy-gated: split the trailing updates of the steps that can start before the copy is
+        // over (estimate: copy at ~50 GB/s, trailing updates at ~25 TF/s)
+        chk.copy_cw = cwe;
+        double t_copy = 0.0;
+        for (int64_t c = 0; c < n; c += 128) t_copy += (double)(n - c) * std::min<int64_t>(128, n - c) * es / 50e9;
+        double t = 0.0;
+        int k = 0;
+        for (int64_t j = 0; j < n && t < t_copy; j += o.nb, ++k) {
+          const double m = (double)(n - j - o.nb);
+          t += m > 0 ? m * m * o.nb * cplx_mult(kind) / 25e12 : 0.0;
+        }
+        chk.split_steps = k + 1;
+      }
       rc = run_blocked(kind, o, n, Kc, L.ldk, L.strideK, cb, seed, b0 + (uint64_t)c0, mk, fz, llk, ifo, w, L, st,
                        false, chk);
       if (rc) return rc;

@@ -283,3 +283,37 @@ print("CHUNK_OK")
     env = dict(os.environ, PYTHONPATH=root, DPP_CHUNK_COLS="256")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert "CHUNK_OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("n", [4500, 8192])
+def test_host_equals_device_path(oracle_mod, n):
+    """The _host entry point (with DPP_COPY_GATED=1 in the environment: its copy pipelined, the
+    trailing updates of the first steps launched per arrived column chunk) sees the same operations
+    per element as the device path, so mask and loglik equal the batched call's bit for bit; the
+    leading block also matches the oracle (prefix property)."""
+    Kc = W.haar_kernel_torch(n, seed=3, spectrum="beta")
+    sb = dpp.sample_batched("herm_d", Kc, 1, seed=4, b0=0)
+    Kh = Kc.cpu().pin_memory()
+    mh = torch.empty((1, n), dtype=torch.uint8).pin_memory()
+    lh = torch.empty(1, dtype=torch.float64).pin_memory()
+    work = torch.empty(dpp.dpp_workspace_bytes(dpp.DPP_OP_HERM_D | dpp.DPP_OP_HOST, 1, n), dtype=torch.uint8,
+                       device="cuda")
+    dpp.dpp_sample_herm_d_host(1, n, Kh, n, 0, 4, 0, mh, lh, None, None, work)
+    assert np.array_equal(mh[0].numpy(), sb.mask[0].cpu().numpy())
+    assert float(lh[0]) == float(sb.loglik[0])
+    m = 600
+    o = oracle_mod.sample_herm_d(Kc[:m, :m].cpu().numpy().T.copy(), 4, 0)
+    compare_masks(mh[0].numpy()[:m], o)
+
+
+def test_host_copy_gated_subprocess():
+    """The copy-gated _host schedule (DPP_COPY_GATED=1) equals the device path bit for bit."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PYTHONPATH=root, DPP_COPY_GATED="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-k", "test_host_equals_device_path",
+                        os.path.join(root, "tests", "test_gpu_parity.py")], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
