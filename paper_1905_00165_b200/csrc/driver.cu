@@ -82,8 +82,8 @@ WsLayout layout(Kind kind, int64_t chunk, int64_t n, int nb, bool copies, bool h
   if (!kind_herm(kind)) off = align_up(off + (size_t)chunk * L.strideM * es);
   L.d_off = off;
   if (kind_herm(kind)) off = align_up(off + 2 * (size_t)chunk * nb * 8);
-  L.ut_off = off;  // LU: U12^T; Hermitian: W21 (same shape)
-  off = align_up(off + 2 * (size_t)chunk * (size_t)L.strideU * es);
+  L.ut_off = off;  // LU: U12^T (double-buffered); Hermitian: W21, as two pair buffers of 2 panels each
+  off = align_up(off + (kind_herm(kind) ? 4 : 2) * (size_t)chunk * (size_t)L.strideU * es);
   L.dh_off = off;  // Hermitian: D of every pivot so far (chunk x n), the column-chunked schedule
   if (kind_herm(kind)) off = align_up(off + (size_t)chunk * (size_t)std::max<int64_t>(n, 1) * 8);
   L.k_off = off;
@@ -254,6 +254,20 @@ int chunk_cols(bool host, int64_t n) {
 // vs 19.3 TF/s at n = 16384) -- the right-looking order needs every column before the first
 // trailing update completes, and the work a left-looking order could do on the first columns is
 // small, so little of the copy can hide behind compute.
+// Paired trailing updates (Hermitian, lookahead on): the trailing update of an even step is
+// deferred and applied together with the next step's, one DMMA pass with K = 2 nb (the two panels
+// are adjacent columns of the factor; their pre-scaled copies W21 are stacked in one buffer), so
+// the update kernel's per-tile epilogue and the C read/write are amortized over twice the work.
+// DPP_PAIR=0 turns it off.
+bool pair_updates() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPP_PAIR");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 bool copy_gated() {
   static int v = -1;
   if (v < 0) {
@@ -291,6 +305,8 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
   void* Am = work + L.am_off;
   int step = 0;
   bool have_rest = false;
+  bool pair_open = false;  // the previous step deferred its trailing update to this one
+  bool prev_psecond = false;  // the previous step was the second of a pair
   const int sms = device_sms();
   if (!herm || !la || ch.cw < nb || ch.cw % nb) ch.cw = 0;
   if (ch.cw && (n + ch.cw - 1) / ch.cw > MAX_CHUNKS) ch.cw = (n + MAX_CHUNKS - 1) / MAX_CHUNKS / nb * nb + nb;
@@ -337,6 +353,10 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     // double-buffered like D1
     const int64_t strideU = L.strideU;
     char* UT = work + L.ut_off + (size_t)(step & 1) * batch * strideU * es;
+    // pairing: steps (2p, 2p+1) share the pair buffer (p & 1) of 2 panels per sample
+    const bool pairing = herm && la && !ch.cw && !ch.copy_cw && pair_updates() && nb == (int)std::min<int64_t>(nb, n);
+    const int64_t strideW = 2 * strideU;
+    char* WP = work + L.ut_off + (size_t)((step >> 1) & 1) * batch * strideW * es;
     // ---- stage 1
     DiagArgs d{};
     d.A = A; d.ld = ld; d.strideA = strideA; d.n = n; d.j0 = j0; d.tcol = j0; d.jb = jb; d.seed = seed; d.b0 = b0;
@@ -382,7 +402,23 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     // ---- stage 3 operands
     UpdateArgs u = base_update(kind, batch, vec);
     u.Aop = Ab + (size_t)(j1 + j0 * ld) * es; u.lda = ld; u.strideA = strideA;  // L21
-    if (herm) {
+    const int jn0 = (int)std::min<int64_t>(nb, m2);
+    // pair roles: the first step of a pair defers its trailing update when the second step has a
+    // trailing region of its own; the second applies both panels
+    const bool pfirst = pairing && !(step & 1) && jb == nb && m2 - jn0 > 0;
+    const bool psecond = pairing && (step & 1) && pair_open;
+    if (herm && pairing) {
+      // W21 of this step into its half of the pair buffer, rows aligned with the first step's
+      ProfScope pa(4, 0.0, s1);
+      // (second of a pair: half 1, shifted down by the first step's nb rows so that row r of both
+      // halves is the same row of the matrix; the K = 2 nb operand then starts at row nb of half 0)
+      char* dst = WP + (size_t)(psecond ? strideU + nb : ((step & 1) ? strideU : 0)) * es;
+      CK(launch_scale_cols(kind, Ab + (size_t)(j1 + j0 * ld) * es, ld, strideA, dst, L.ldk, strideW, dvec,
+                           nb, (int)m2, jb, batch, s1));
+      u.Aop = psecond ? WP + (size_t)nb * es : dst; u.lda = L.ldk; u.strideA = strideW;  // W21 (both panels if 2nd)
+      u.Bop = Ab + (size_t)(j1 + (psecond ? j0 - nb : j0) * ld) * es; u.ldb = ld; u.strideB = strideA;
+      u.mask = 1; u.conj = (kind == HERM_Z);
+    } else if (herm) {
       // A22 -= W21 L21^H with W21 = L21 D1 (pre-scaled copy; the DMMA loop does no scaling)
       ProfScope pa(4, 0.0, s1);
       CK(launch_scale_cols(kind, Ab + (size_t)(j1 + j0 * ld) * es, ld, strideA, UT, L.ldk, strideU, dvec,
@@ -394,8 +430,10 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       u.Bop = UT; u.ldb = L.ldk; u.strideB = strideU;  // U12^T (j, k), K-major
     }
     u.C = Ab + (size_t)(j1 + j1 * ld) * es; u.ldc = ld; u.strideC = strideA;
-    u.a_rows = (int)m2; u.b_rows = (int)m2; u.K = jb;
-    const int jn = (int)std::min<int64_t>(nb, m2);  // width of the next block
+    u.a_rows = (int)m2; u.b_rows = (int)m2; u.K = psecond ? nb + jb : jb;
+    // width of the lookahead region: the next block -- or, at the second step of a pair, the next
+    // pair's two blocks, so the next pair's whole diag/panel chain runs under this pair's update
+    const int jn = (int)std::min<int64_t>(psecond ? 2 * nb : nb, m2);
     if (!la) {
       u.row0 = 0; u.col0 = 0; u.rows = (int)m2; u.cols = (int)m2; u.tri = herm;
       ProfScope ps(3, region_flops(kind, 0, 0, m2, m2, jb) * batch, s1);
@@ -405,11 +443,14 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     CK(cudaEventRecord(ds->ev_panel, s1));
     // (a) next block column [0, jn) x rows [0, m2)  (+ LU: next block row [0, jn) x cols [jn, m2));
     // chunked: only while the next block is in this chunk (else the catch-up update covers it)
-    if (have_rest) CK(cudaStreamWaitEvent(s1, ds->ev_rest, 0));
+    // (the first step of a pair needs no wait: its lookahead block was covered by the previous
+    // pair's lookahead update and is not part of the previous trailing update)
+    if (have_rest && !(pfirst && prev_psecond)) CK(cudaStreamWaitEvent(s1, ds->ev_rest, 0));
+    prev_psecond = psecond;
     if (j1 < ce) {
       UpdateArgs ua = u;
       ua.row0 = 0; ua.col0 = 0; ua.rows = (int)m2; ua.cols = jn; ua.tri = 0;
-      double fl = region_flops(kind, 0, 0, m2, jn, jb);
+      double fl = region_flops(kind, 0, 0, m2, jn, ua.K);
       if (!herm && m2 > jn) fl += region_flops(kind, 0, jn, jn, m2 - jn, jb);
       ProfScope ps(2, fl * batch, s1);
       CK(launch_update(kind, ua, s1));
@@ -421,7 +462,8 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     }
     // (b) the rest [jn, m2)^2 on S2 (chunked: its columns restricted to the chunk)
     const int64_t colsb = std::min<int64_t>(m2, ce - j1) - jn;
-    if (m2 > jn && colsb > 0) {
+    pair_open = pfirst;  // the next step applies this step's trailing update with its own
+    if (m2 > jn && colsb > 0 && !pfirst) {
       CK(cudaStreamWaitEvent(s2, ds->ev_panel, 0));
       UpdateArgs ub = u;
       ub.row0 = jn; ub.col0 = jn; ub.rows = (int)(m2 - jn); ub.cols = (int)colsb;
@@ -439,7 +481,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
           g0 = g1;
         }
       } else {
-        ProfScope ps(3, region_flops(kind, jn, jn, m2 - jn, colsb, jb) * batch, s2);
+        ProfScope ps(3, region_flops(kind, jn, jn, m2 - jn, colsb, ub.K) * batch, s2);
         CK(launch_update(kind, ub, s2));
       }
       CK(cudaEventRecord(ds->ev_rest, s2));

@@ -211,11 +211,12 @@ def test_large_parity_2048(oracle_mod):
 
 
 @pytest.mark.parametrize("env", [{"DPP_UPDATE_GENERIC": "1"}, {"DPP_WS_VARIANT": "0"}, {"DPP_DIAG_NT": "512"},
-                                 {"DPP_DIAG_BLOCKED": "1"}])
+                                 {"DPP_DIAG_BLOCKED": "1"}, {"DPP_PAIR": "0"}])
 def test_alternate_update_kernels_subprocess(env):
     """The cp.async fallback update kernel (DPP_UPDATE_GENERIC=1), the 8-consumer-warp layout of
     the warp-specialized kernel (DPP_WS_VARIANT=0), the 512-thread register-tile diag kernel
-    (DPP_DIAG_NT=512) and the 32-column-blocked Hermitian diag kernel (DPP_DIAG_BLOCKED=1) give the same
+    (DPP_DIAG_NT=512), the 32-column-blocked Hermitian diag kernel (DPP_DIAG_BLOCKED=1) and the
+    unpaired trailing updates (DPP_PAIR=0: one K = nb update per step) give the same
     samples and factors as the oracle for all three kinds (each run in a fresh process)."""
     import os
     import subprocess
@@ -312,7 +313,7 @@ def test_host_copy_gated_subprocess():
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PYTHONPATH=root, DPP_COPY_GATED="1")
+    env = dict(os.environ, PYTHONPATH=root, DPP_COPY_GATED="1", DPP_PAIR="0")  # same update grouping on both paths
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-k", "test_host_equals_device_path",
                         os.path.join(root, "tests", "test_gpu_parity.py")], cwd=root, env=env, capture_output=True,
                        text=True, timeout=900)
