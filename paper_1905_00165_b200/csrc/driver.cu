@@ -192,7 +192,9 @@ int device_sms() {
 // SMs to leave to the lookahead stream while the trailing update (b) of this step runs
 // persistently on the rest: minimise max(T1, T2) with T1 = diag latency + (tiles of the next
 // block column's update + next panel) / R, T2 = tiles of (b) / (SMs - R), in units of one tile.
-int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile, bool herm) {
+// g = 2 for the second step of a pair: its trailing update has K = 2nb (twice the tile time) and
+// the chain beside it holds the next pair's two diag tiles and two panels.
+int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile, bool herm, int g = 1) {
   const double diag_tiles = 5.0;  // the diag tile ~ 5 update-tile times (measured ~100 us vs ~20 us)
   const double side = (double)((m2 + tile - 1) / tile), side_b = (double)((m2 - jn + tile - 1) / tile);
   const double ta = (herm ? 1.0 : 2.0) * side * batch;     // (a): next block column (LU: + row)
@@ -201,8 +203,8 @@ int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile, bool herm) {
   int best = 8;
   double best_t = 1e300;
   for (int R = 4; R <= sms / 2; R += 2) {
-    const double t1 = diag_tiles + (ta + tp) / R;
-    const double t2 = tb / (sms - R);
+    const double t1 = g * diag_tiles + (ta + g * tp) / R;
+    const double t2 = g * tb / (sms - R);
     const double t = t1 > t2 ? t1 : t2;
     if (t < best_t) { best_t = t; best = R; }
   }
@@ -268,6 +270,16 @@ bool pair_updates() {
   return v == 1;
 }
 
+// rows below which the real Hermitian sampler switches to half-width blocks (DPP_TAIL_ROWS, 0 = off)
+int64_t tail_rows() {
+  static long long v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPP_TAIL_ROWS");
+    v = e ? atoll(e) : 0;
+  }
+  return (int64_t)v;
+}
+
 bool copy_gated() {
   static int v = -1;
   if (v < 0) {
@@ -311,8 +323,15 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
   if (!herm || !la || ch.cw < nb || ch.cw % nb) ch.cw = 0;
   if (ch.cw && (n + ch.cw - 1) / ch.cw > MAX_CHUNKS) ch.cw = (n + MAX_CHUNKS - 1) / MAX_CHUNKS / nb * nb + nb;
   double* dhist = herm ? reinterpret_cast<double*>(work + L.dh_off) : nullptr;
-  for (int64_t j0 = 0; j0 < n; j0 += nb, ++step) {
-    const int jb = (int)std::min<int64_t>(nb, n - j0);
+  // Tail blocks: once at most `thr` rows remain, the blocks are nb/2 wide -- the sequential chain
+  // (diag tile, panel, lookahead column) is what bounds those steps, and a half-width diag tile
+  // costs far less than half of a full one.  Pivot draws are by global index (R2): the blocking
+  // does not change the sample.
+  const int64_t thr = (nb == 128 && herm && la && !ch.cw && !ch.copy_cw) ? tail_rows() : 0;
+  auto bs_of = [&](int64_t j) -> int { return (thr > 0 && n - j <= thr) ? nb / 2 : nb; };
+  auto blk = [&](int64_t j) -> int64_t { return std::min<int64_t>(bs_of(j), n - j); };
+  for (int64_t j0 = 0; j0 < n; j0 += blk(j0), ++step) {
+    const int jb = (int)blk(j0);
     const int64_t j1 = j0 + jb, m2 = n - j1;
     const int64_t c0 = ch.cw ? (j0 / ch.cw) * ch.cw : 0;
     const int64_t ce = ch.cw ? std::min<int64_t>(n, c0 + ch.cw) : n;  // the chunk's columns: [c0, ce)
@@ -366,7 +385,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     {
       const double fl = (herm ? 1.0 : 2.0) * jb * (double)jb * jb / 3.0 * cplx_mult(kind) * batch;
       ProfScope ps(0, fl, s1);
-      CK(launch_diag(kind, nb, d, s1));
+      CK(launch_diag(kind, bs_of(j0), d, s1));
     }
     if (m2 <= 0) break;
     if (ch.cw && herm)  // this block's pivots, for the later chunks' catch-up updates
@@ -402,10 +421,10 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     // ---- stage 3 operands
     UpdateArgs u = base_update(kind, batch, vec);
     u.Aop = Ab + (size_t)(j1 + j0 * ld) * es; u.lda = ld; u.strideA = strideA;  // L21
-    const int jn0 = (int)std::min<int64_t>(nb, m2);
+    const int jn0 = (int)std::min<int64_t>(bs_of(j1), m2);
     // pair roles: the first step of a pair defers its trailing update when the second step has a
     // trailing region of its own; the second applies both panels
-    const bool pfirst = pairing && !(step & 1) && jb == nb && m2 - jn0 > 0;
+    const bool pfirst = pairing && !(step & 1) && jb == nb && jn0 == nb && m2 - jn0 > 0;
     const bool psecond = pairing && (step & 1) && pair_open;
     if (herm && pairing) {
       // W21 of this step into its half of the pair buffer, rows aligned with the first step's
@@ -433,7 +452,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     u.a_rows = (int)m2; u.b_rows = (int)m2; u.K = psecond ? nb + jb : jb;
     // width of the lookahead region: the next block -- or, at the second step of a pair, the next
     // pair's two blocks, so the next pair's whole diag/panel chain runs under this pair's update
-    const int jn = (int)std::min<int64_t>(psecond ? 2 * nb : nb, m2);
+    const int jn = (int)std::min<int64_t>(psecond ? 2 * nb : bs_of(j1), m2);
     if (!la) {
       u.row0 = 0; u.col0 = 0; u.rows = (int)m2; u.cols = (int)m2; u.tri = herm;
       ProfScope ps(3, region_flops(kind, 0, 0, m2, m2, jb) * batch, s1);
@@ -468,7 +487,8 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       UpdateArgs ub = u;
       ub.row0 = jn; ub.col0 = jn; ub.rows = (int)(m2 - jn); ub.cols = (int)colsb;
       ub.tri = herm && colsb == m2 - jn;
-      if (vec) ub.grid_limit = sms - reserve_sms(m2, jn, sms, batch, kind_cplx(kind) ? 64 : 128, herm);
+      if (vec)
+        ub.grid_limit = sms - reserve_sms(m2, jn, sms, batch, kind_cplx(kind) ? 64 : 128, herm, psecond ? 2 : 1);
       if (ch.copy_cw && ch.ev && step < ch.split_steps) {
         // one launch per copy chunk of the trailing columns, each gated by its own chunk
         for (int64_t g0 = j1 + jn; g0 < j1 + jn + colsb;) {
