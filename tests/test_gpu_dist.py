@@ -63,3 +63,32 @@ def test_dist_rejects_bad_nb():
             dpp.dpp_sample_herm_d_dist(comm, 100, loc, 100, 0, mask, ll, None, dpp.make_opts(nb=64), work)
     finally:
         dpp.dpp_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("kind,n", [("herm_d", 32768), ("herm_z", 16384)])
+def test_dist_full_size_bench_configuration(oracle_mod, kind, n):
+    """configs[4] at (half of) its size in the bench's launch configuration (block-cyclic layout,
+    lookahead, one rank): the leading 1024 x 1024 block's decisions equal the oracle's sample of
+    K[:1024, :1024] (prefix property), loglik = sum ln|D| over the returned factor,
+    and about half of the items are kept (lambda ~ U(0,1))."""
+    cplx = kind == "herm_z"
+    nb = 64 if cplx else 128
+    loc = W.haar_kernel_bcc_torch(n, nb, 1, 0, seed=0, spectrum="uniform", complex_=cplx)
+    m = 1024
+    Kpre = loc[:m, :m].cpu().numpy().T.copy()  # local storage == column-major storage at world size 1
+    comm = dpp.dpp_comm_init(D.unique_id(), 1, 0)
+    try:
+        mask = torch.empty(n, dtype=torch.uint8, device="cuda")
+        ll = torch.empty((), dtype=torch.float64, device="cuda")
+        op = dpp.DPP_OP_HERM_Z if cplx else dpp.DPP_OP_HERM_D
+        work = torch.empty(dpp.dpp_dist_workspace_bytes(op, n, 1), dtype=torch.uint8, device="cuda")
+        fn = dpp.dpp_sample_herm_z_dist if cplx else dpp.dpp_sample_herm_d_dist
+        fn(comm, n, loc, n, 0, mask, ll, None, None, work)
+        torch.cuda.synchronize()
+    finally:
+        dpp.dpp_comm_destroy(comm)
+    o = (oracle_mod.sample_herm_z if cplx else oracle_mod.sample_herm_d)(Kpre, 0, 0)
+    compare_masks(mask[:m].cpu().numpy(), o)
+    d = torch.diagonal(loc[:n, :n]).real if cplx else torch.diagonal(loc[:n, :n])
+    assert abs(float(torch.log(d.abs()).sum()) - float(ll)) <= 1e-10 * abs(float(ll))
+    assert 0.4 * n < int(mask.sum()) < 0.6 * n

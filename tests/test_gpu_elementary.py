@@ -61,3 +61,21 @@ def test_elementary_edge_cases(oracle_mod):
     with pytest.raises(dpp.DppError):  # k > n
         dpp.dpp_elementary_workspace_bytes(1, 4, 5) or dpp.dpp_elementary_herm_d(
             1, 4, 5, to_device(np.eye(4), "herm_d"), 4, 0, 0, None, None, None, work)
+
+
+def test_elementary_bench_configuration(oracle_mod):
+    """The bench's configuration (n = 5000, rank 500, the paper's elementary-sampler figure): the
+    first samples equal the oracle's item for item."""
+    n, k = 5000, 500
+    g = torch.Generator(device="cuda")
+    g.manual_seed(0)
+    Q, _ = torch.linalg.qr(torch.randn(n, k, generator=g, device="cuda", dtype=torch.float64))
+    Kc = (Q @ Q.T).contiguous()
+    order, ll, _ = dpp.elementary(Kc, k, batch=2, seed=0, b0=0)
+    K = Kc.cpu().numpy()
+    for s in range(2):
+        o = oracle_mod.elementary_herm_d(K, k, 0, s)
+        m = o.first_tie if o.n_ties else k
+        assert np.array_equal(order[s].cpu().numpy()[:m], o.order[:m])
+        if o.n_ties == 0:
+            assert abs(float(ll[s]) - o.loglik) <= 1e-9 * abs(o.loglik)

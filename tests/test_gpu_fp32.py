@@ -68,3 +68,17 @@ def test_fp32_batched_and_structure(oracle_mod):
     for b in range(8):
         assert W.is_aztec_tiling(10, s.mask[b].cpu().numpy())
         assert abs(float(s.loglik[b]) + 55 * np.log(2.0)) <= 1e-4 * 55 * np.log(2.0)
+
+
+def test_fp32_bench_configuration_prefix(oracle_mod):
+    """The herm_s bench configuration (n = 16384, the configs[3] kernel rounded to fp32, nb = 128):
+    the leading 1536 x 1536 block's decisions equal the fp32 oracle's (prefix property)."""
+    n, m = 16384, 1536
+    Kc = W.haar_kernel_torch(n, seed=0, spectrum="beta").to(torch.float32)
+    Kpre = Kc[:m, :m].cpu().numpy().T.copy()
+    s = dpp.sample("herm_s", Kc, 0, opts=dpp.make_opts(nb=128, lookahead=1))
+    torch.cuda.synchronize()
+    o = oracle_mod.sample_herm_s(Kpre, 0, 0, tie_tol=TIE32)
+    k = o.first_tie if o.n_ties else m
+    assert np.array_equal(s.mask.cpu().numpy()[:k], o.mask[:k])
+    assert 0.4 * n < int(s.mask.sum()) < 0.6 * n

@@ -70,3 +70,24 @@ def test_lensemble_edge_cases(oracle_mod):
         K = from_device(Lc, n)
         assert np.max(np.abs(np.tril(K) - c / (1 + c) * np.eye(n))) <= 1e-14
         assert abs(float(ld) - n * np.log1p(c)) <= 1e-10 * max(1.0, n * np.log1p(c))
+
+
+def test_lensemble_bench_size_residual():
+    """n = 16384 (the bench's size): (I - K)(L + I) = I checked on random vectors with torch
+    (harness arithmetic), and ln det(L + I) against the spectrum the kernel was built from."""
+    n = 16384
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    Q, _ = torch.linalg.qr(torch.randn(n, n, generator=g, device="cuda", dtype=torch.float64))
+    lam = 10.0 * torch.rand(n, generator=g, device="cuda", dtype=torch.float64)
+    L = (Q * lam[None, :]) @ Q.T
+    del Q
+    L = 0.5 * (L + L.T)
+    Lc = L.clone()  # symmetric: column-major storage == L
+    logdet = dpp.lensemble_to_marginal(Lc)
+    Kl = torch.tril(Lc)
+    K = Kl + torch.tril(Kl, -1).T
+    x = torch.randn(n, 4, generator=g, device="cuda", dtype=torch.float64)
+    y = x - K @ (L @ x + x)  # (I - K)(L + I) x
+    assert float((y - x).abs().max()) <= 1e-9 * float(x.abs().max()) * (1.0 + float(lam.max()))
+    assert abs(float(logdet) - float(torch.log1p(lam).sum())) <= 1e-9 * float(torch.log1p(lam).sum())
