@@ -82,8 +82,8 @@ WsLayout layout(Kind kind, int64_t chunk, int64_t n, int nb, bool copies, bool h
   if (!kind_herm(kind)) off = align_up(off + (size_t)chunk * L.strideM * es);
   L.d_off = off;
   if (kind_herm(kind)) off = align_up(off + 2 * (size_t)chunk * nb * 8);
-  L.ut_off = off;  // LU: U12^T (double-buffered); Hermitian: W21, as two pair buffers of 2 panels each
-  off = align_up(off + (kind_herm(kind) ? 4 : 2) * (size_t)chunk * (size_t)L.strideU * es);
+  L.ut_off = off;  // W21 (Hermitian) or U12^T (LU): two pair buffers of two panels each
+  off = align_up(off + 4 * (size_t)chunk * (size_t)L.strideU * es);
   L.dh_off = off;  // Hermitian: D of every pivot so far (chunk x n), the column-chunked schedule
   if (kind_herm(kind)) off = align_up(off + (size_t)chunk * (size_t)std::max<int64_t>(n, 1) * 8);
   L.k_off = off;
@@ -280,6 +280,20 @@ int64_t tail_rows() {
   return (int64_t)v;
 }
 
+// trailing size below which updates are no longer paired (DPP_PAIR_MIN_ROWS; default 6144 rows for
+// 128-wide blocks, where the 86-us diag tile makes the chain the bound near the end -- measured
+// C4 25.8 -> 26.1 TF/s -- and 0 for 64-wide blocks, whose chain is short: complex Hermitian n =
+// 8192 27.0 vs 26.6 TF/s with 6144)
+int64_t pair_min_rows(int nb) {
+  static long long v = -2;
+  if (v == -2) {
+    const char* e = getenv("DPP_PAIR_MIN_ROWS");
+    v = e ? atoll(e) : -1;
+  }
+  if (v >= 0) return (int64_t)v;
+  return nb >= 128 ? 6144 : 0;
+}
+
 bool copy_gated() {
   static int v = -1;
   if (v < 0) {
@@ -373,9 +387,19 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     const int64_t strideU = L.strideU;
     char* UT = work + L.ut_off + (size_t)(step & 1) * batch * strideU * es;
     // pairing: steps (2p, 2p+1) share the pair buffer (p & 1) of 2 panels per sample
-    const bool pairing = herm && la && !ch.cw && !ch.copy_cw && pair_updates() && nb == (int)std::min<int64_t>(nb, n);
+    const bool pairing = la && !ch.cw && !ch.copy_cw && pair_updates() && nb == (int)std::min<int64_t>(nb, n);
     const int64_t strideW = 2 * strideU;
     char* WP = work + L.ut_off + (size_t)((step >> 1) & 1) * batch * strideW * es;
+    // pair roles: the first step of a pair defers its trailing update when the second step has a
+    // trailing region of its own (only while the trailing updates dominate: near the end the chain
+    // is the bound, and a pair's double-width lookahead update lengthens it); the second applies both
+    // panels.  Each step's operand panel (W21 or U12^T) goes to its half of the pair buffer, the
+    // second step's shifted down by nb rows so that row r of both halves is the same matrix row.
+    const int jn0 = (int)std::min<int64_t>(bs_of(j1), m2);
+    const bool pfirst =
+        pairing && !(step & 1) && jb == nb && jn0 == nb && m2 - jn0 > 0 && m2 > pair_min_rows(nb);
+    const bool psecond = pairing && (step & 1) && pair_open;
+    char* const PH = WP + (size_t)(psecond ? strideU + nb : ((step & 1) ? strideU : 0)) * es;  // my half
     // ---- stage 1
     DiagArgs d{};
     d.A = A; d.ld = ld; d.strideA = strideA; d.n = n; d.j0 = j0; d.tcol = j0; d.jb = jb; d.seed = seed; d.b0 = b0;
@@ -406,32 +430,28 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
         // U12 = L11^-1 A12 = A12 - Am A12 (Am = I - L11^-1), computed transposed so that every
         // operand is K-major:  U12^T = A12^T - A12^T Am^T  in the U12^T buffer, then copied back.
         char* A12 = Ab + (size_t)(j0 + j1 * ld) * es;
-        { ProfScope pa(4, 0.0, s1); CK(launch_transpose(es, A12, ld, strideA, UT, L.ldk, strideU, jb, (int)m2, batch, s1)); }
+        char* const UTs = pairing ? PH : UT;  // my U12^T panel (pairing: my half of the pair buffer)
+        const int64_t sU = pairing ? strideW : strideU;
+        { ProfScope pa(4, 0.0, s1); CK(launch_transpose(es, A12, ld, strideA, UTs, L.ldk, sU, jb, (int)m2, batch, s1)); }
         UpdateArgs q = base_update(kind, batch, vec);
-        q.Aop = UT; q.lda = L.ldk; q.strideA = strideU;                            // A12^T (j, k)
+        q.Aop = UTs; q.lda = L.ldk; q.strideA = sU;                                // A12^T (j, k)
         q.Bop = Am; q.ldb = nb; q.strideB = L.strideM;                             // Am (i, k)
-        q.C = UT; q.ldc = L.ldk; q.strideC = strideU;                              // U12^T in place
+        q.C = UTs; q.ldc = L.ldk; q.strideC = sU;                                  // U12^T in place
         q.a_rows = (int)m2; q.b_rows = jb; q.K = jb;
         q.row0 = 0; q.col0 = 0; q.rows = (int)m2; q.cols = jb;
         CK(launch_update(kind, q, s1));
         ProfScope pa(4, 0.0, s1);
-        CK(launch_transpose(es, UT, L.ldk, strideU, A12, ld, strideA, (int)m2, jb, batch, s1));  // U12 -> K
+        CK(launch_transpose(es, UTs, L.ldk, sU, A12, ld, strideA, (int)m2, jb, batch, s1));  // U12 -> K
       }
     }
     // ---- stage 3 operands
     UpdateArgs u = base_update(kind, batch, vec);
     u.Aop = Ab + (size_t)(j1 + j0 * ld) * es; u.lda = ld; u.strideA = strideA;  // L21
-    const int jn0 = (int)std::min<int64_t>(bs_of(j1), m2);
-    // pair roles: the first step of a pair defers its trailing update when the second step has a
-    // trailing region of its own; the second applies both panels
-    const bool pfirst = pairing && !(step & 1) && jb == nb && jn0 == nb && m2 - jn0 > 0;
-    const bool psecond = pairing && (step & 1) && pair_open;
     if (herm && pairing) {
-      // W21 of this step into its half of the pair buffer, rows aligned with the first step's
+      // W21 of this step into its half of the pair buffer (the K = 2 nb operand of the second step
+      // starts at row nb of half 0)
       ProfScope pa(4, 0.0, s1);
-      // (second of a pair: half 1, shifted down by the first step's nb rows so that row r of both
-      // halves is the same row of the matrix; the K = 2 nb operand then starts at row nb of half 0)
-      char* dst = WP + (size_t)(psecond ? strideU + nb : ((step & 1) ? strideU : 0)) * es;
+      char* dst = PH;
       CK(launch_scale_cols(kind, Ab + (size_t)(j1 + j0 * ld) * es, ld, strideA, dst, L.ldk, strideW, dvec,
                            nb, (int)m2, jb, batch, s1));
       u.Aop = psecond ? WP + (size_t)nb * es : dst; u.lda = L.ldk; u.strideA = strideW;  // W21 (both panels if 2nd)
@@ -445,6 +465,9 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       u.Aop = UT; u.lda = L.ldk; u.strideA = strideU;  // W21
       u.Bop = Ab + (size_t)(j1 + j0 * ld) * es; u.ldb = ld; u.strideB = strideA;  // L21 (conjugated on load)
       u.mask = 1; u.conj = (kind == HERM_Z);
+    } else if (pairing) {
+      u.Aop = Ab + (size_t)(j1 + (psecond ? j0 - nb : j0) * ld) * es;                 // L21 (both if 2nd)
+      u.Bop = psecond ? WP + (size_t)nb * es : PH; u.ldb = L.ldk; u.strideB = strideW;  // U12^T (both if 2nd)
     } else {
       u.Bop = UT; u.ldb = L.ldk; u.strideB = strideU;  // U12^T (j, k), K-major
     }

@@ -85,9 +85,11 @@ def test_lensemble_bench_size_residual():
     L = 0.5 * (L + L.T)
     Lc = L.clone()  # symmetric: column-major storage == L
     logdet = dpp.lensemble_to_marginal(Lc)
-    Kl = torch.tril(Lc)
-    K = Kl + torch.tril(Kl, -1).T
+    # column-major storage: K(i, l) = Lc[l, i], so the lower triangle of K is triu(Lc) transposed
+    Ku = torch.triu(Lc)
+    K = Ku.T + torch.triu(Lc, 1)
     x = torch.randn(n, 4, generator=g, device="cuda", dtype=torch.float64)
-    y = x - K @ (L @ x + x)  # (I - K)(L + I) x
+    z = L @ x + x
+    y = z - K @ z  # (I - K)(L + I) x
     assert float((y - x).abs().max()) <= 1e-9 * float(x.abs().max()) * (1.0 + float(lam.max()))
     assert abs(float(logdet) - float(torch.log1p(lam).sum())) <= 1e-9 * float(torch.log1p(lam).sum())

@@ -211,7 +211,8 @@ def test_large_parity_2048(oracle_mod):
 
 
 @pytest.mark.parametrize("env", [{"DPP_UPDATE_GENERIC": "1"}, {"DPP_WS_VARIANT": "0"}, {"DPP_DIAG_NT": "512"},
-                                 {"DPP_DIAG_BLOCKED": "1"}, {"DPP_PAIR": "0"}, {"DPP_TAIL_ROWS": "200"}])
+                                 {"DPP_DIAG_BLOCKED": "1"}, {"DPP_PAIR": "0"}, {"DPP_TAIL_ROWS": "200"},
+                                 {"DPP_PAIR_MIN_ROWS": "0"}])
 def test_alternate_update_kernels_subprocess(env):
     """The cp.async fallback update kernel (DPP_UPDATE_GENERIC=1), the 8-consumer-warp layout of
     the warp-specialized kernel (DPP_WS_VARIANT=0), the 512-thread register-tile diag kernel

@@ -4,13 +4,17 @@ sample, in order: per block step  panel GEMM, lookahead column (a), trailing upd
 
 Algorithmic bytes of (b) at step k (m2 = n - nb (k + 1), jn = min(nb, m2)): one read and one write
 of the lower triangle of the trailing region [jn, m2)^2 in fp64 -- the operand panels come from L2.
-Usage: python tools/traffic.py launches.csv n nb > profiles/..._update_traffic.json"""
+With paired updates (the default) an even step defers its trailing update to the next step, whose
+lookahead update covers two block columns; pass the driver's DPP_PAIR_MIN_ROWS (pairing only while
+the trailing size exceeds it; -1 = pairing off).
+Usage: python tools/traffic.py launches.csv n nb [pair_min_rows] > profiles/..._update_traffic.json"""
 import collections
 import csv
 import json
 import sys
 
 path, n, nb = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+pmin = int(sys.argv[4]) if len(sys.argv) > 4 else 6144
 rows = list(csv.reader(open(path)))
 hdr = None
 per = collections.OrderedDict()
@@ -29,15 +33,20 @@ for r in rows:
     per.setdefault(key, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", "")) * scale
 launches = list(per.values())
 steps = (n + nb - 1) // nb - 1
-# the last steps have no (b) launch once m2 <= nb; each step launches panel, (a), and (b) if m2 > jn
+# replicate the driver's launch order: panel, (a), and (b) unless deferred (first step of a pair)
 seq = []
-i = 0
+pair_open = False
 for k in range(steps):
-    m2 = n - nb * (k + 1)
-    jn = min(nb, m2)
-    kinds = ["panel", "a"] + (["b"] if m2 > jn else [])
+    j1 = nb * (k + 1)
+    m2 = n - j1
+    jn0 = min(nb, m2)
+    pfirst = pmin >= 0 and k % 2 == 0 and jn0 == nb and m2 - jn0 > 0 and m2 > pmin
+    psecond = pmin >= 0 and k % 2 == 1 and pair_open
+    jn = min(2 * nb if psecond else nb, m2)
+    kinds = ["panel", "a"] + (["b"] if (m2 > jn and not pfirst) else [])
     for kd in kinds:
         seq.append((kd, k, m2, jn))
+    pair_open = pfirst
 launches = launches[-len(seq):]  # the last sample of the capture
 meas = alg = 0.0
 nb_launch = 0
