@@ -488,7 +488,7 @@ def extra_workload(args):
         # sampler figure: ranks 10..500), a batch of independent samples per GPU per step
         n = args.n if args.n != N else 5000
         k = args.rank
-        B = args.batch if args.batch != 1024 else 64
+        B = args.batch if args.batch != 1024 else 592  # 4 samples per SM: one CTA per sample
         g = torch.Generator(device="cuda"); g.manual_seed(KSEED)
         G = torch.randn(n, k, generator=g, device="cuda", dtype=torch.float64)
         Q, _ = torch.linalg.qr(G)
@@ -515,7 +515,7 @@ def extra_workload(args):
                               "achieved": round(gbs, 1), "peak": peak_hbm, "unit": "GB/s",
                               "frac": round(gbs / peak_hbm, 4), "traffic": None,
                               "note": "the per-sample factor (n x k x 8 B) is L2-resident for small k"},
-                    gpu_launches=int(2 * k * args.steps),
+                    gpu_launches=int(args.steps),  # one fused launch per step (batch >= SMs)
                     clocks=clocks)
     elif args.workload == "lensemble":
         # L-ensemble -> marginal conversion, "3 samples worth of time"

@@ -16,10 +16,13 @@
 //   * elem_column_kernel: one thread per (row, sample): the new column as a dot product over j
 //     factor columns (coalesced column-major reads, 4 independent partial sums), divided by A_j,
 //     and the diagonal update.
-// Both are launched once per step on the caller's stream (2k launches per call).
+// Both are launched once per step on the caller's stream (2k launches per call) -- or, when the
+// batch has at least one sample per SM, elem_fused_kernel runs all k steps of a sample in one CTA
+// (one launch per call).
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <climits>
 #include <cstdint>
 
@@ -68,14 +71,24 @@ __global__ void elem_init_kernel(ElemArgs a) {
 
 constexpr int SEL_T = 1024;
 
-__global__ void __launch_bounds__(SEL_T) elem_select_kernel(ElemArgs a, int64_t j) {
-  const int64_t s = blockIdx.x;
+struct SelShared {
+  double wsum[SEL_T / 32];
+  double S, target;
+  long long t, last;
+};
+
+// Draw of pivot j for sample s by one CTA of SEL_T threads (block-wide scan of d over the items,
+// each thread a contiguous segment), the pivot bookkeeping, and the pivot's factor row L(t, 0:j)
+// copied next to the state.  Ends with the CTA synchronised.
+__device__ __forceinline__ void elem_select(const ElemArgs& a, int64_t s, int64_t j, SelShared& sh) {
   const double* d = a.d + s * a.n;
   uint8_t* ch = a.chosen + s * a.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ double wsum[SEL_T / 32];
-  __shared__ double sh_S, sh_target;
-  __shared__ long long sh_t, sh_last;
+  double* wsum = sh.wsum;
+  double& sh_S = sh.S;
+  double& sh_target = sh.target;
+  long long& sh_t = sh.t;
+  long long& sh_last = sh.last;
   // contiguous segment of this thread
   const int64_t per = (a.n + SEL_T - 1) / SEL_T;
   const int64_t i0 = min((int64_t)a.n, (int64_t)tid * per), i1 = min((int64_t)a.n, i0 + per);
@@ -156,6 +169,60 @@ __global__ void __launch_bounds__(SEL_T) elem_select_kernel(ElemArgs a, int64_t 
       a.loglik[s] = st.loglik;
       if (a.ties) { a.ties[2 * s] = st.n_ties; a.ties[2 * s + 1] = st.first_tie; }
     }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(SEL_T) elem_select_kernel(ElemArgs a, int64_t j) {
+  __shared__ SelShared sh;
+  elem_select(a, blockIdx.x, j, sh);
+}
+
+// The whole sampler for one sample per CTA (all k steps in one launch): the draw, then the new
+// factor column, rows strided over the CTA's threads (for batches large enough to fill the GPU with
+// one CTA per sample; removes the 2k launches per call).
+__global__ void __launch_bounds__(SEL_T) elem_fused_kernel(ElemArgs a) {
+  __shared__ SelShared sh;
+  extern __shared__ double lt_s[];
+  const int64_t s = blockIdx.x;
+  double* L = a.L + s * a.strideL;
+  const uint8_t* ch = a.chosen + s * a.n;
+  double* d = a.d + s * a.n;
+  for (int64_t i = threadIdx.x; i < a.n; i += SEL_T) {
+    d[i] = a.K[i + i * a.ld];
+    a.chosen[s * a.n + i] = 0;
+  }
+  if (threadIdx.x == 0) {
+    ElemState& st = a.st[s];
+    st.t = -1; st.Aj = 0.0; st.loglik = 0.0; st.n_ties = 0; st.first_tie = -1;
+  }
+  __syncthreads();
+  for (int64_t j = 0; j < a.k; ++j) {
+    elem_select(a, s, j, sh);
+    if (j + 1 == a.k) break;
+    for (int64_t m = threadIdx.x; m < j; m += SEL_T) lt_s[m] = a.lt[s * a.k + m];
+    __syncthreads();
+    const int64_t t = a.st[s].t;
+    const double Aj = a.st[s].Aj;
+    for (int64_t i = threadIdx.x; i < a.n; i += SEL_T) {
+      if (ch[i]) {
+        if (i != t) L[i + j * a.ldL] = 0.0;
+        continue;
+      }
+      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+      int64_t m = 0;
+      for (; m + 4 <= j; m += 4) {
+        c0 = fma(L[i + m * a.ldL], lt_s[m], c0);
+        c1 = fma(L[i + (m + 1) * a.ldL], lt_s[m + 1], c1);
+        c2 = fma(L[i + (m + 2) * a.ldL], lt_s[m + 2], c2);
+        c3 = fma(L[i + (m + 3) * a.ldL], lt_s[m + 3], c3);
+      }
+      for (; m < j; ++m) c0 = fma(L[i + m * a.ldL], lt_s[m], c0);
+      const double c = (a.K[i + t * a.ld] - ((c0 + c1) + (c2 + c3))) / Aj;
+      L[i + j * a.ldL] = c;
+      d[i] -= c * c;
+    }
+    __syncthreads();
   }
 }
 
@@ -241,10 +308,27 @@ int dpp_elementary_herm_d(int64_t batch, int64_t n, int64_t k, const double* K, 
   a.lt = reinterpret_cast<double*>(w + W.lt_off);
   a.st = reinterpret_cast<ElemState*>(w + W.st_off);
   a.order = order; a.loglik = loglik; a.ties = ties;
+  const size_t smem = (size_t)k * 8;
+  // one CTA per sample when the batch fills the GPU (DPP_ELEM_FUSED=0/1 forces a choice)
+  static int fused_env = -2;
+  if (fused_env == -2) {
+    const char* e = getenv("DPP_ELEM_FUSED");
+    fused_env = e ? atoi(e) : -1;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool fused = fused_env >= 0 ? fused_env == 1 : batch >= sms;
+  if (fused) {
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(elem_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return DPP_ECUDA;
+    elem_fused_kernel<<<(unsigned)batch, SEL_T, smem, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? DPP_OK : DPP_ECUDA;
+  }
   const dim3 rows((unsigned)((n + 255) / 256), (unsigned)batch);
   elem_init_kernel<<<rows, 256, 0, st>>>(a);
   if (cudaGetLastError() != cudaSuccess) return DPP_ECUDA;
-  const size_t smem = (size_t)k * 8;
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(elem_column_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return DPP_ECUDA;

@@ -79,3 +79,20 @@ def test_elementary_bench_configuration(oracle_mod):
         assert np.array_equal(order[s].cpu().numpy()[:m], o.order[:m])
         if o.n_ties == 0:
             assert abs(float(ll[s]) - o.loglik) <= 1e-9 * abs(o.loglik)
+
+
+@pytest.mark.parametrize("n,k", [(300, 40), (2000, 150)])
+def test_elementary_fused_batch(oracle_mod, n, k):
+    """Batches of at least one sample per SM run all k steps of a sample in one CTA (one launch):
+    the samples still equal the oracle's item for item."""
+    K = W.projection_kernel(n, k, seed=7 + n)
+    batch = 160
+    order, ll, _ = dpp.elementary(to_device(K, "herm_d"), k, batch=batch, seed=2, b0=0)
+    torch.cuda.synchronize()
+    order, ll = order.cpu().numpy(), ll.cpu().numpy()
+    for s in (0, 1, 77, batch - 1):
+        o = oracle_mod.elementary_herm_d(K, k, 2, s)
+        m = o.first_tie if o.n_ties else k
+        assert np.array_equal(order[s][:m], o.order[:m])
+        if o.n_ties == 0:
+            assert abs(ll[s] - o.loglik) <= 1e-10 * max(1.0, abs(o.loglik))
