@@ -284,13 +284,15 @@ int64_t tail_rows() {
 // for 128-wide Hermitian blocks, where the 86-us diag tile makes the chain the bound near the end --
 // measured C4 25.8 -> 26.1 TF/s -- 0 for 64-wide Hermitian blocks, whose chain is short (complex
 // Hermitian n = 8192: 27.0 vs 26.6 TF/s with 6144), 8192 for LU)
-int64_t pair_min_rows(int nb, bool herm) {
+int64_t pair_min_rows(int nb, bool herm, int batch) {
   static long long v = -2;
   if (v == -2) {
     const char* e = getenv("DPP_PAIR_MIN_ROWS");
     v = e ? atoll(e) : -1;
   }
   if (v >= 0) return (int64_t)v;
+  if (batch >= 8) return 0;  // batched: the chain is shared by the batch, the updates dominate throughout
+                             // (UST 40x40, 256 per launch: 2373 paired vs 2275 samples/s)
   if (!herm) return 8192;  // LU: two panel GEMMs and two lookahead updates per step (n = 8192: 27.6
                            // TF/s unpaired vs 26.1 paired; Aztec n = 25600: 33.3 paired vs 32.0)
   return nb >= 128 ? 6144 : 0;
@@ -399,7 +401,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     // second step's shifted down by nb rows so that row r of both halves is the same matrix row.
     const int jn0 = (int)std::min<int64_t>(bs_of(j1), m2);
     const bool pfirst =
-        pairing && !(step & 1) && jb == nb && jn0 == nb && m2 - jn0 > 0 && m2 > pair_min_rows(nb, herm);
+        pairing && !(step & 1) && jb == nb && jn0 == nb && m2 - jn0 > 0 && m2 > pair_min_rows(nb, herm, batch);
     const bool psecond = pairing && (step & 1) && pair_open;
     char* const PH = WP + (size_t)(psecond ? strideU + nb : ((step & 1) ? strideU : 0)) * es;  // my half
     // ---- stage 1
