@@ -260,6 +260,27 @@ def main():
                "d2h_bytes_per_step": int(mh.numel() + lh.numel() * 8 + ih.numel()),
                "samples_per_s": round(args.steps * world / (float(te.item()) / 1e3), 3)}
 
+    # context comparator (the paper's "DPP sampling ~ plain factorization"):
+    # cuSOLVER Cholesky (torch.linalg.cholesky -> potrf) of the same positive definite K, timed alone
+    comparator = None
+    if rank == 0 and not args.no_e2e:
+        try:
+            Kf = Kc.clone()
+            torch.linalg.cholesky(Kf)
+            torch.cuda.synchronize()
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record()
+            for _ in range(3):
+                torch.linalg.cholesky(Kf)
+            c1.record()
+            torch.cuda.synchronize()
+            cms = c0.elapsed_time(c1) / 3
+            comparator = {"what": "cuSOLVER potrf (torch.linalg.cholesky) of the same n x n K, plain factorization, "
+                                  "no sampling", "ms": round(cms, 3), "tflops": round(model_flops(n) / (cms / 1e3) / 1e12, 3)}
+            del Kf
+        except Exception as e:  # a comparator only: never fails the bench
+            comparator = {"error": str(e)[:200]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = min(16, len(os.sched_getaffinity(0)))
@@ -301,6 +322,7 @@ def main():
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "comparator_cusolver_potrf": comparator,
             "impl": "ours",
         }
         print(json.dumps(line), flush=True)
