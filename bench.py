@@ -152,6 +152,7 @@ def main():
     ap.add_argument("--aztec-d", type=int, default=80, help="aztec_c: diamond order")
     ap.add_argument("--rank", type=int, default=500, help="elementary: projection rank k")
     ap.add_argument("--lookahead", type=int, default=1, help="ust: 0 = single stream")
+    ap.add_argument("--nb", type=int, default=128, help="ust: block size")
     args = ap.parse_args()
     if args.workload != "c4" and args.impl == "ours":
         return extra_workload(args)
@@ -334,7 +335,7 @@ def main():
 def _traffic():
     """DRAM bytes per launch of the trailing-update kernel from the committed ncu capture
     (profiles/r01d_update_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum averaged over
-    the 126 (b) launches of one n=16384 sample); None if absent."""
+    the trailing-update launches of one n=16384 sample); None if absent."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "r01d_update_traffic.json")))
         return {"bytes_per_launch": int(d["measured_bytes_per_launch"]),
@@ -389,7 +390,7 @@ def extra_workload(args):
         K = W.ust_kernel(40, 40)
         Kc = torch.from_numpy(np.ascontiguousarray(K.T)).cuda()
         B = args.batch
-        opts = dpp.make_opts(nb=128, lookahead=args.lookahead, batch_chunk=min(B, args.batch_chunk))
+        opts = dpp.make_opts(nb=args.nb, lookahead=args.lookahead, batch_chunk=min(B, args.batch_chunk))
         op = dpp.DPP_OP_HERM_D | dpp.DPP_OP_BATCHED
         work = torch.empty(dpp.dpp_workspace_bytes(op, B, n, opts), dtype=torch.uint8, device="cuda")
         mask = torch.empty((B, n), dtype=torch.uint8, device="cuda")
@@ -405,7 +406,7 @@ def extra_workload(args):
                     dtype="f64", samples_per_s=round(B * args.steps * world / (ms / 1e3), 2),
                     config={"workload": f"BASELINE configs[1]: UST of the 40x40 grid (n=3120, rank 1599), {B} "
                                         f"independent samples per GPU per step", "n": n, "global_batch": B * world,
-                            "nb": 128, "batch_chunk": min(B, args.batch_chunk), "lookahead": args.lookahead, "seq_len": None,
+                            "nb": args.nb, "batch_chunk": min(B, args.batch_chunk), "lookahead": args.lookahead, "seq_len": None,
                             "parallelism": f"dp{world} (independent samples)"},
                     all_samples_are_spanning_trees_with_1599_edges=ok,
                     pct_fp64_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), 2), clocks=clocks)
