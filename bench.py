@@ -150,6 +150,7 @@ def main():
     ap.add_argument("--batch", type=int, default=1024, help="ust: samples per GPU per step")
     ap.add_argument("--batch-chunk", type=int, default=256, help="ust: samples factored concurrently")
     ap.add_argument("--aztec-d", type=int, default=80, help="aztec_c: diamond order")
+    ap.add_argument("--tally", type=int, default=0, help="aztec_c: untimed extra batches whose tilings are all checked")
     ap.add_argument("--rank", type=int, default=500, help="elementary: projection rank k")
     ap.add_argument("--lookahead", type=int, default=1, help="ust: 0 = single stream")
     ap.add_argument("--nb", type=int, default=128, help="ust: block size")
@@ -496,6 +497,16 @@ def extra_workload(args):
         masks = mask.cpu().numpy()
         good = sum(W.is_aztec_tiling(d, masks[b]) for b in range(B))
         want = -d * (d + 1) / 2 * float(np.log(2.0))
+        if args.tally > 0:  # untimed: tilings over args.tally further batches (fresh sample indices)
+            t_good, t_err = 0, []
+            for i in range(args.tally):
+                step(args.steps + args.warmup + i)
+                mk, lv = mask.cpu().numpy(), ll.cpu().numpy()
+                t_good += sum(W.is_aztec_tiling(d, mk[b]) for b in range(B))
+                t_err += [float(x) for x in np.abs(lv - want)]
+            line["tally"] = {"samples": args.tally * B, "perfect_tilings": t_good,
+                             "loglik_error_max": max(t_err), "loglik_error_median": float(np.median(t_err)),
+                             "b0": (rank * 1000 + args.steps + args.warmup) * B}
         flops = 8.0 * n ** 3 / 3.0 * B * args.steps * world
         line.update(value=round(flops / (ms / 1e3) / 1e9, 2), ms_per_step=round(ms / args.steps, 3), scaling="weak",
                     dtype="c64", samples_per_s=round(B * args.steps * world / (ms / 1e3), 4),

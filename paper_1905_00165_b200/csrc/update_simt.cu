@@ -138,21 +138,29 @@ __global__ void __launch_bounds__(SIMT_NT, 1) update_simt_kernel(const UpdateArg
       }
       __syncthreads();
     }
-    // epilogue: C -= acc (Hermitian: never above the diagonal); 16-byte accesses of HM rows when
-    // the group lies inside the tile and below the diagonal, element accesses otherwise
+    // epilogue: C -= acc (Hermitian: never above the diagonal).  Per group of HN columns x HM rows:
+    // 16-byte accesses when the whole group lies inside the tile and below the diagonal (vec: ldc
+    // keeps every column of the group 16-byte aligned like the first), element accesses otherwise.
+    // The group's loads are all issued before its stores (a load after a store to the same array
+    // waits for it: one serialized global round trip per group, not per column).
     T* Cg = reinterpret_cast<T*>(a.C) + (int64_t)ti.s * a.strideC;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int hg = 0; hg < 4; ++hg) {
+      const int h = hg >> 1, jg = (hg & 1) * HN;
       const int r0 = h * (BM / 2) + tx * HM;
+      const int cb = (hg & 1) * (BN / 2) + ty * HN;  // first column of the group
+      T* pb = Cg + ti.grow0 + r0 + (int64_t)(ti.gcol0 + cb - ti.cshift) * a.ldc;
+      const bool full = vec && cb + HN <= ti.ncols && r0 + HM <= ti.nrows &&
+                        (!MASK || ti.grow0 + r0 >= ti.gcol0 + cb + HN - 1) &&
+                        (reinterpret_cast<uintptr_t>(pb) & 15) == 0;
+      if (full) {
+        float4 cv[HN];
 #pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const int c = (j / HN) * (BN / 2) + ty * HN + (j % HN);
-        if (c >= ti.ncols) continue;
-        T* p = Cg + ti.grow0 + r0 + (int64_t)(ti.gcol0 + c - ti.cshift) * a.ldc;
-        const bool full = vec && r0 + HM <= ti.nrows && (!MASK || ti.grow0 + r0 >= ti.gcol0 + c) &&
-                          (reinterpret_cast<uintptr_t>(p) & 15) == 0;
-        if (full) {
-          float4 v = *reinterpret_cast<float4*>(p);
+        for (int jj = 0; jj < HN; ++jj) cv[jj] = *reinterpret_cast<const float4*>(pb + (int64_t)jj * a.ldc);
+#pragma unroll
+        for (int jj = 0; jj < HN; ++jj) {
+          const int j = jg + jj;
+          float4 v = cv[jj];
           if constexpr (!CPLX) {
             v.x -= acc[h * HM + 0][j][0]; v.y -= acc[h * HM + 1][j][0];
             v.z -= acc[h * HM + 2][j][0]; v.w -= acc[h * HM + 3][j][0];
@@ -160,8 +168,14 @@ __global__ void __launch_bounds__(SIMT_NT, 1) update_simt_kernel(const UpdateArg
             v.x -= acc[h * HM + 0][j][0]; v.y -= acc[h * HM + 0][j][1];
             v.z -= acc[h * HM + 1][j][0]; v.w -= acc[h * HM + 1][j][1];
           }
-          *reinterpret_cast<float4*>(p) = v;
-        } else {
+          *reinterpret_cast<float4*>(pb + (int64_t)jj * a.ldc) = v;
+        }
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < HN; ++jj) {
+          const int j = jg + jj, c = cb + jj;
+          if (c >= ti.ncols) continue;
+          T* p = pb + (int64_t)jj * a.ldc;
 #pragma unroll
           for (int r = 0; r < HM; ++r) {
             const int rr = r0 + r;
