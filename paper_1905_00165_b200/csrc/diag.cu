@@ -79,37 +79,47 @@ __global__ void __launch_bounds__(NT, 1) diag_kernel(const DiagArgs a) {
   }
   // publish pivot columns kn, kn+1 (strictly below their diagonal, zero elsewhere), their
   // diagonal entries and, LU, rows kn, kn+1 (strictly right of the diagonal).  Zero padding lets
-  // the step below run without per-row predicates.  The owning register is selected with
-  // compile-time indices only (a runtime index into R would demote the tile to local memory).
-  auto publish = [&](int kn, int buf) {
-#pragma unroll
-    for (int ib = 0; ib < CB; ++ib) {
-      const int l = tc + TC * ib;
-      if (l == kn || l == kn + 1) {
-#pragma unroll
-        for (int ia = 0; ia < RA; ++ia) {
-          const int i = tr + TR * ia;
-          const T v = R[ia][ib];
-          if (i == l) pivbuf[buf][l - kn] = v;
-          colbuf[buf][l - kn][i] = (i > l) ? v : zero<T>();
-        }
-      }
-    }
-    if (!HERM) {
+  // the step below run without per-row predicates.  The owning register block is a compile-time
+  // index (a runtime index into R would demote the tile to local memory): columns kn, kn+1 (kn even)
+  // both lie in register column block IB = kn / TC, rows kn, kn+1 in row block IA = kn / TR, and
+  // the caller passes the block it knows kn is in.
+  auto publish_col = [&](auto IBC, int kn, int buf) {
+    constexpr int IB = decltype(IBC)::value;
+    const int l = tc + TC * IB;
+    if (l == kn || l == kn + 1) {
 #pragma unroll
       for (int ia = 0; ia < RA; ++ia) {
         const int i = tr + TR * ia;
-        if (i == kn || i == kn + 1) {
-#pragma unroll
-          for (int ib = 0; ib < CB; ++ib) {
-            const int l = tc + TC * ib;
-            rowbuf[HERM ? 0 : buf][i - kn][l] = (l > i) ? R[ia][ib] : zero<T>();
-          }
-        }
+        const T v = R[ia][IB];
+        if (i == l) pivbuf[buf][l - kn] = v;
+        colbuf[buf][l - kn][i] = (i > l) ? v : zero<T>();
       }
     }
   };
-  publish(0, 0);
+  auto publish_row = [&](auto IAC, int kn, int buf) {
+    constexpr int IA = decltype(IAC)::value;
+    const int i = tr + TR * IA;
+    if (i == kn || i == kn + 1) {
+#pragma unroll
+      for (int ib = 0; ib < CB; ++ib) {
+        const int l = tc + TC * ib;
+        rowbuf[HERM ? 0 : buf][i - kn][l] = (l > i) ? R[IA][ib] : zero<T>();
+      }
+    }
+  };
+  // kn in [16P + 2, 16P + 16] (the pivot pair after one of phase P), or 0
+  auto publish = [&](auto PC, int kn, int buf) {
+    constexpr int P = decltype(PC)::value;
+    constexpr int IBa = (16 * P) / TC, IBb = (16 * P + 16) / TC;
+    if (kn / TC == IBa) publish_col(std::integral_constant<int, IBa>{}, kn, buf);
+    else if constexpr (IBb < CB) publish_col(std::integral_constant<int, IBb>{}, kn, buf);
+    if (!HERM) {
+      constexpr int IAa = (16 * P) / TR, IAb = (16 * P + 16) / TR;
+      if (kn / TR == IAa) publish_row(std::integral_constant<int, IAa>{}, kn, buf);
+      else if constexpr (IAb < RA) publish_row(std::integral_constant<int, IAb>{}, kn, buf);
+    }
+  };
+  publish(std::integral_constant<int, 0>{}, 0, 0);
   __syncthreads();
 
   // Two pivots per barrier: every thread redoes the 2x2 micro-step of pivots (k, k+1) from the two
@@ -186,7 +196,7 @@ __global__ void __launch_bounds__(NT, 1) diag_kernel(const DiagArgs a) {
           R[ia][ib] = fms(R[ia][ib], L0[ia], W0[ib]);
           R[ia][ib] = fms(R[ia][ib], L1[ia], W1[ib]);
         }
-    if (k + 2 < jb) publish(k + 2, nxt);
+    if (k + 2 < jb) publish(PC, k + 2, nxt);
     __syncthreads();
   };
   using std::integral_constant;
@@ -204,24 +214,39 @@ __global__ void __launch_bounds__(NT, 1) diag_kernel(const DiagArgs a) {
   }
 
   // ---- finalize the factor: L = (unscaled column) * (1/p), diagonal = final pivot; also stage
-  //      the triangular factors block-packed for the inversion (identity beyond jb)
+  //      the triangular factors block-packed for the inversion (identity beyond jb).  The raw tile
+  //      goes to shared memory first (one store per register) and a rolled loop does the rest:
+  //      the unrolled per-register form was ~10 KB of straight-line code run once (instruction
+  //      fetch stalls dominated it).
   const bool ops = a.need_ops != 0;
 #pragma unroll
   for (int ia = 0; ia < RA; ++ia)
 #pragma unroll
     for (int ib = 0; ib < CB; ++ib) {
       const int i = tr + TR * ia, l = tc + TC * ib;
-      T v = R[ia][ib];
-      if (i > l) v = mul(v, rv[l < jb ? l : 0]);
-      else if (i == l) v = pv[i < jb ? i : 0];
-      const bool in = i < jb && l < jb;
-      if (in && (!HERM || i >= l)) A[(int64_t)l * a.ld + i] = v;
-      if (ops) {
-        const T one = make_real(1.0, zero<T>());
-        if (i >= l) Lb[bp(i, l)] = (i == l) ? one : (in ? v : zero<T>());
-        if (!HERM && i <= l) Ub[bp(l, i)] = in ? v : (i == l ? one : zero<T>());  // U^T(l, i) = U(i, l)
-      }
+      if (i >= l) Lb[bp(i, l)] = R[ia][ib];
+      if (!HERM && i <= l) Ub[bp(l, i)] = R[ia][ib];  // U^T(l, i) = U(i, l)
     }
+  __syncthreads();
+  for (int e = tid; e < NB * NB; e += NT) {
+    const int i = e % NB, l = e / NB;  // column-major: consecutive threads, consecutive rows
+    const bool in = i < jb && l < jb;
+    const T one = make_real(1.0, zero<T>());
+    if (i > l) {
+      const T v = mul(Lb[bp(i, l)], rv[l < jb ? l : 0]);
+      if (in) A[(int64_t)l * a.ld + i] = v;
+      Lb[bp(i, l)] = in ? v : zero<T>();
+    } else if (i == l) {
+      const T v = pv[i < jb ? i : 0];
+      if (in) A[(int64_t)l * a.ld + i] = v;
+      Lb[bp(i, l)] = one;
+      if (!HERM) Ub[bp(l, i)] = in ? v : one;
+    } else if (!HERM) {
+      const T v = Ub[bp(l, i)];
+      if (in) A[(int64_t)l * a.ld + i] = v;
+      Ub[bp(l, i)] = in ? v : zero<T>();
+    }
+  }
   // ---- decisions, likelihood terms and diagnostics: warp 0 reduces the flags with ballots and
   //      shuffles; the log-likelihood terms are summed by one lane IN PIVOT ORDER
   for (int k = tid; k < jb; k += NT) {
@@ -319,12 +344,11 @@ __global__ void __launch_bounds__(NT, 1) diag_kernel(const DiagArgs a) {
 template <typename T, bool HERM, int NB, int NT>
 static cudaError_t launch_diag_nt(const DiagArgs& a, cudaStream_t s) {
   constexpr int NBLK = NB / 16, NPB = NBLK * (NBLK + 1) / 2;
-  const size_t smem = a.need_ops ? (size_t)((HERM ? 2 : 3) * NPB * 256 + (NBLK - 1) * 256) * sizeof(T) : 0;
+  // the packed factors are also the staging area of the finalize pass: always allocated
+  const size_t smem = (size_t)((HERM ? 2 : 3) * NPB * 256 + (NBLK - 1) * 256) * sizeof(T);
   auto* fn = diag_kernel<T, HERM, NB, NT>;
-  if (smem > 0) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   dim3 grid(1, a.batch);
   fn<<<grid, NT, smem, s>>>(a);
   return cudaGetLastError();
