@@ -51,9 +51,9 @@ __global__ void __launch_bounds__(NT, 1) diag_kernel(const DiagArgs a) {
   __shared__ uint8_t keepv[NB];
   extern __shared__ __align__(16) unsigned char dsm[];
   T* Lb = reinterpret_cast<T*>(dsm);          // block-packed L11 (unit lower)
-  T* Ub = Lb + NPB * 256;                      // LU: block-packed U11^T (lower, non-unit)
-  T* Xb = Ub + (HERM ? 0 : NPB * 256);         // inverse
-  T* Tb = Xb + NPB * 256;                      // scratch (NBLK - 1 blocks)
+  T* Ub = Lb + NPB * BLK_SZ;                   // LU: block-packed U11^T (lower, non-unit)
+  T* Xb = Ub + (HERM ? 0 : NPB * BLK_SZ);      // inverse
+  T* Tb = Xb + NPB * BLK_SZ;                   // scratch (NBLK - 1 blocks)
 
   const int s = blockIdx.y;
   const int jb = a.jb;
@@ -345,7 +345,7 @@ template <typename T, bool HERM, int NB, int NT>
 static cudaError_t launch_diag_nt(const DiagArgs& a, cudaStream_t s) {
   constexpr int NBLK = NB / 16, NPB = NBLK * (NBLK + 1) / 2;
   // the packed factors are also the staging area of the finalize pass: always allocated
-  const size_t smem = (size_t)((HERM ? 2 : 3) * NPB * 256 + (NBLK - 1) * 256) * sizeof(T);
+  const size_t smem = (size_t)((HERM ? 2 : 3) * NPB + NBLK - 1) * BLK_SZ * sizeof(T);
   auto* fn = diag_kernel<T, HERM, NB, NT>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -23,6 +23,13 @@
 
 namespace dpp {
 
+// block-packed 16x16 blocks with a column pitch of 16 (see tri_inverse.cuh's bp)
+__device__ __forceinline__ int bp16(int i, int k) {
+  const int I = i >> 4, J = k >> 4;
+  return ((I * (I + 1) / 2 + J) << 8) + (i & 15) + ((k & 15) << 4);
+}
+
+
 __device__ __forceinline__ double shfl_idx(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 __device__ __forceinline__ double2 shfl_idx(double2 v, int src) {
   return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
@@ -198,7 +205,8 @@ __global__ void __launch_bounds__(256, 1) diag_herm_blocked_kernel(const DiagArg
   if (!a.need_ops) return;
   // ---- stage-2 operator: Bm(j,k) = delta_jk - conj(Linv(j,k)) / D(j), from the factored tile
   const int nblk = (jb + 15) >> 4;
-  tri_inverse_lower_g<T, true, NT>([=](int I, int K) { return S + 16 * I + 16 * K * LDS; }, LDS, Xb, Tb, nblk);
+  // X blocks with a pitch of 16 here (this kernel's shared memory is full: no room for bp's padding)
+  tri_inverse_lower_g<T, true, NT>([=](int I, int K) { return S + 16 * I + 16 * K * LDS; }, LDS, Xb, Tb, nblk, 16);
   double* dvec = a.dvec + (int64_t)s * a.ldm;
   for (int k = tid; k < jb; k += NT) dvec[k] = pf[k];
   T* Bm = reinterpret_cast<T*>(a.Bm) + (int64_t)s * a.strideM;
@@ -206,7 +214,7 @@ __global__ void __launch_bounds__(256, 1) diag_herm_blocked_kernel(const DiagArg
     for (int j = lane; j < jb; j += 32) {
       T v = zero<T>();
       if (j >= k) {
-        v = neg(scal(cj(Xb[bp(j, k)]), pr[j]));
+        v = neg(scal(cj(Xb[bp16(j, k)]), pr[j]));
         if (j == k) v = make_real(re(v) + 1.0, v);
       }
       Bm[j + (int64_t)k * a.ldm] = v;

@@ -58,8 +58,8 @@ __global__ void __launch_bounds__(256) lens_tile_inverse_kernel(const T* A, int6
   constexpr int NBLK = NB / 16, NPB = NBLK * (NBLK + 1) / 2;
   extern __shared__ __align__(16) unsigned char dsm[];
   T* Lb = reinterpret_cast<T*>(dsm);
-  T* Xb = Lb + NPB * 256;
-  T* Tb = Xb + NPB * 256;
+  T* Xb = Lb + NPB * BLK_SZ;
+  T* Tb = Xb + NPB * BLK_SZ;
   const int64_t k = blockIdx.x, j0 = k * NB;
   const int jb = (int)min((int64_t)NB, n - j0);
   const T* Tl = A + j0 + j0 * ld;
@@ -148,7 +148,7 @@ int lens_run(dpp::Kind kind, int64_t n, T* A, int64_t ld, double* logdet, void* 
   T* Y = reinterpret_cast<T*>(w + W.y_off);
   {
     constexpr int NBLK = NB / 16, NPB = NBLK * (NBLK + 1) / 2;
-    const size_t smem = (size_t)(2 * NPB * 256 + (NBLK - 1) * 256) * sizeof(T);
+    const size_t smem = (size_t)(2 * NPB + NBLK - 1) * BLK_SZ * sizeof(T);
     if (cudaFuncSetAttribute(lens_tile_inverse_kernel<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return DPP_ECUDA;

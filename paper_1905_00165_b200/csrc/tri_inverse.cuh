@@ -31,10 +31,15 @@ __device__ __forceinline__ float2 madd(float2 c, float2 a, float2 b) {
 __device__ __forceinline__ float neg(float a) { return -a; }
 __device__ __forceinline__ float2 neg(float2 a) { return make_float2(-a.x, -a.y); }
 
-// block-packed lower-triangular storage: 16x16 blocks (I >= J), column-major inside a block
+// block-packed lower-triangular storage: 16x16 blocks (I >= J), column-major inside a block with a
+// column pitch of BLK_LD = 20 elements.  With a pitch of 16 every column of a block starts on the
+// same bank, and the DMMA fragment loads below (lane -> (row lane/4, k lane%4) for A, (k lane%4,
+// column lane/4) for B) hit each bank 4 (A) or 8 (B) times per request; with 20 they are
+// conflict-free (each 8-byte bank pair serves two lanes: the minimum of two wavefronts).
+constexpr int BLK_LD = 20, BLK_SZ = 16 * BLK_LD;
 __device__ __forceinline__ int bp(int i, int k) {
   const int I = i >> 4, J = k >> 4;
-  return ((I * (I + 1) / 2 + J) << 8) + (i & 15) + ((k & 15) << 4);
+  return (I * (I + 1) / 2 + J) * BLK_SZ + (i & 15) + (k & 15) * BLK_LD;
 }
 
 // C (16x16) += A (16x16) B (16x16) on 16x16 column-major blocks in shared memory, one warp, with
@@ -50,7 +55,7 @@ template <> struct BlockAcc16<double> {
 #pragma unroll
       for (int j = 0; j < 2; ++j) c[i][j][0] = c[i][j][1] = 0.0;
   }
-  __device__ __forceinline__ void mma(const double* A, const double* B, int lane, int lda = 16) {
+  __device__ __forceinline__ void mma(const double* A, const double* B, int lane, int lda = BLK_LD, int ldb = BLK_LD) {
 #pragma unroll
     for (int k4 = 0; k4 < 4; ++k4) {
       const int kk = k4 * 4 + (lane & 3);
@@ -58,7 +63,7 @@ template <> struct BlockAcc16<double> {
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         a[t] = A[t * 8 + (lane >> 2) + kk * lda];
-        b[t] = B[kk + ((t * 8 + (lane >> 2)) << 4)];
+        b[t] = B[kk + (t * 8 + (lane >> 2)) * ldb];
       }
 #pragma unroll
       for (int i = 0; i < 2; ++i)
@@ -67,14 +72,14 @@ template <> struct BlockAcc16<double> {
     }
   }
   // C -> block (neg: store -C)
-  __device__ __forceinline__ void store(double* C, int lane, bool neg) const {
+  __device__ __forceinline__ void store(double* C, int lane, bool neg, int ldc = BLK_LD) const {
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-          C[i * 8 + (lane >> 2) + ((j * 8 + 2 * (lane & 3) + e) << 4)] = neg ? -c[i][j][e] : c[i][j][e];
+          C[i * 8 + (lane >> 2) + (j * 8 + 2 * (lane & 3) + e) * ldc] = neg ? -c[i][j][e] : c[i][j][e];
   }
 };
 template <> struct BlockAcc16<double2> {
@@ -85,7 +90,7 @@ template <> struct BlockAcc16<double2> {
 #pragma unroll
       for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
   }
-  __device__ __forceinline__ void mma(const double2* A, const double2* B, int lane, int lda = 16) {
+  __device__ __forceinline__ void mma(const double2* A, const double2* B, int lane, int lda = BLK_LD, int ldb = BLK_LD) {
 #pragma unroll
     for (int k4 = 0; k4 < 4; ++k4) {
       const int kk = k4 * 4 + (lane & 3);
@@ -93,7 +98,7 @@ template <> struct BlockAcc16<double2> {
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         a[t] = A[t * 8 + (lane >> 2) + kk * lda];
-        b[t] = B[kk + ((t * 8 + (lane >> 2)) << 4)];
+        b[t] = B[kk + (t * 8 + (lane >> 2)) * ldb];
       }
 #pragma unroll
       for (int i = 0; i < 2; ++i)
@@ -106,7 +111,7 @@ template <> struct BlockAcc16<double2> {
         }
     }
   }
-  __device__ __forceinline__ void store(double2* C, int lane, bool neg) const {
+  __device__ __forceinline__ void store(double2* C, int lane, bool neg, int ldc = BLK_LD) const {
     const double sg = neg ? -1.0 : 1.0;
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -114,7 +119,7 @@ template <> struct BlockAcc16<double2> {
       for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-          C[i * 8 + (lane >> 2) + ((j * 8 + 2 * (lane & 3) + e) << 4)] = make_double2(sg * cr[i][j][e], sg * ci[i][j][e]);
+          C[i * 8 + (lane >> 2) + (j * 8 + 2 * (lane & 3) + e) * ldc] = make_double2(sg * cr[i][j][e], sg * ci[i][j][e]);
   }
 };
 
@@ -128,7 +133,7 @@ template <typename T> struct BlockAccSimt {
 #pragma unroll
       for (int j = 0; j < 2; ++j) c[i][j][0] = c[i][j][1] = dpp::zero<T>();
   }
-  __device__ __forceinline__ void mma(const T* A, const T* B, int lane, int lda = 16) {
+  __device__ __forceinline__ void mma(const T* A, const T* B, int lane, int lda = BLK_LD, int ldb = BLK_LD) {
 #pragma unroll 4
     for (int k = 0; k < 16; ++k)
 #pragma unroll
@@ -137,17 +142,17 @@ template <typename T> struct BlockAccSimt {
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) c[i][j][e] = madd(c[i][j][e], a, B[k + ((j * 8 + 2 * (lane & 3) + e) << 4)]);
+          for (int e = 0; e < 2; ++e) c[i][j][e] = madd(c[i][j][e], a, B[k + (j * 8 + 2 * (lane & 3) + e) * ldb]);
       }
   }
-  __device__ __forceinline__ void store(T* C, int lane, bool ng) const {
+  __device__ __forceinline__ void store(T* C, int lane, bool ng, int ldc = BLK_LD) const {
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-          C[i * 8 + (lane >> 2) + ((j * 8 + 2 * (lane & 3) + e) << 4)] = ng ? neg(c[i][j][e]) : c[i][j][e];
+          C[i * 8 + (lane >> 2) + (j * 8 + 2 * (lane & 3) + e) * ldc] = ng ? neg(c[i][j][e]) : c[i][j][e];
   }
 };
 template <> struct BlockAcc16<float> : BlockAccSimt<float> {};
@@ -155,9 +160,11 @@ template <> struct BlockAcc16<float2> : BlockAccSimt<float2> {};
 
 // X = L^{-1} for a lower-triangular L (unit or not) of order 16*nblk; X block-packed in smem, L
 // given by a block accessor Lblk(I, K) -> pointer to its 16x16 block (I >= K), element (i, k) at
-// [i + k * ldl].  Tb: scratch for (nblk - 1) 16x16 blocks.  All NT threads participate.
+// [i + k * ldl].  Tb: scratch for (nblk - 1) 16x16 blocks.  All NT threads participate.  X (and
+// Tb) blocks: column pitch xld, xld * 16 elements per block (bp's layout by default).
 template <typename T, bool UNIT, int NT, class LBlk>
-__device__ void tri_inverse_lower_g(LBlk Lblk_of, int ldl, T* Xb, T* Tb, int nblk) {
+__device__ void tri_inverse_lower_g(LBlk Lblk_of, int ldl, T* Xb, T* Tb, int nblk, int xld = BLK_LD) {
+  const int xsz = 16 * xld;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NWARPS = NT / 32;
   // diagonal blocks: warp w inverts block w; lane c < 16 forms column c of the inverse by forward
@@ -176,9 +183,9 @@ __device__ void tri_inverse_lower_g(LBlk Lblk_of, int ldl, T* Xb, T* Tb, int nbl
 #pragma unroll
         for (int i = l + 1; i < 16; ++i) x[i] = fms(x[i], Lblk[i + l * ldl], x[l]);
       }
-      T* Xblk = Xb + ((I * (I + 1) / 2 + I) << 8);
+      T* Xblk = Xb + (I * (I + 1) / 2 + I) * xsz;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) Xblk[i + (c << 4)] = x[i];
+      for (int i = 0; i < 16; ++i) Xblk[i + c * xld] = x[i];
     }
   }
   __syncthreads();
@@ -190,14 +197,14 @@ __device__ void tri_inverse_lower_g(LBlk Lblk_of, int ldl, T* Xb, T* Tb, int nbl
       const int I = d + q, J = q;
       BlockAcc16<T> acc;
       acc.zero();
-      for (int K = J; K < I; ++K) acc.mma(Lblk_of(I, K), Xb + ((K * (K + 1) / 2 + J) << 8), lane, ldl);
-      T* Tq = Tb + (q << 8);
-      acc.store(Tq, lane, false);
+      for (int K = J; K < I; ++K) acc.mma(Lblk_of(I, K), Xb + (K * (K + 1) / 2 + J) * xsz, lane, ldl, xld);
+      T* Tq = Tb + q * xsz;
+      acc.store(Tq, lane, false, xld);
       __syncwarp();
       BlockAcc16<T> acc2;
       acc2.zero();
-      acc2.mma(Xb + ((I * (I + 1) / 2 + I) << 8), Tq, lane);
-      acc2.store(Xb + ((I * (I + 1) / 2 + J) << 8), lane, true);
+      acc2.mma(Xb + (I * (I + 1) / 2 + I) * xsz, Tq, lane, xld, xld);
+      acc2.store(Xb + (I * (I + 1) / 2 + J) * xsz, lane, true, xld);
       __syncwarp();
     }
     __syncthreads();
@@ -207,8 +214,8 @@ __device__ void tri_inverse_lower_g(LBlk Lblk_of, int ldl, T* Xb, T* Tb, int nbl
 // the same with L block-packed in smem
 template <typename T, bool UNIT, int NT>
 __device__ void tri_inverse_lower(const T* Lb, T* Xb, T* Tb, int nblk) {
-  tri_inverse_lower_g<T, UNIT, NT>([=](int I, int K) { return Lb + ((I * (I + 1) / 2 + K) << 8); }, 16, Xb, Tb,
-                                   nblk);
+  tri_inverse_lower_g<T, UNIT, NT>([=](int I, int K) { return Lb + (I * (I + 1) / 2 + K) * BLK_SZ; }, BLK_LD, Xb,
+                                   Tb, nblk);
 }
 
 }  // namespace dpp
