@@ -195,7 +195,13 @@ int device_sms() {
 // g = 2 for the second step of a pair: its trailing update has K = 2nb (twice the tile time) and
 // the chain beside it holds the next pair's two diag tiles and two panels.
 int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile, bool herm, int g = 1) {
-  const double diag_tiles = 5.0;  // the diag tile ~ 5 update-tile times (measured ~100 us vs ~20 us)
+  // the diag tile in update-tile times (DPP_DIAG_TILES; 5 measured ~100 us vs ~20 us; after the
+  // diag kernel went to 63 us, 2.5 .. 5 give the same C4 / UST rates within noise)
+  static double diag_tiles = -1.0;
+  if (diag_tiles < 0) {
+    const char* e = getenv("DPP_DIAG_TILES");
+    diag_tiles = e ? atof(e) : 5.0;
+  }
   const double side = (double)((m2 + tile - 1) / tile), side_b = (double)((m2 - jn + tile - 1) / tile);
   const double ta = (herm ? 1.0 : 2.0) * side * batch;     // (a): next block column (LU: + row)
   const double tp = (herm ? 1.0 : 2.0) * side_b * batch;   // next panel GEMM(s)
