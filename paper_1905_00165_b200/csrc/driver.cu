@@ -56,6 +56,8 @@ int resolve_opts(Kind kind, const dpp_opts_t* o, Opts* r) {
 
 size_t esize(Kind k) { return kind_esize(k); }
 
+int group_size();
+
 // Workspace layout (all regions 256-byte aligned):
 //   [SampleState x chunk]
 //   [panel operators: Bm (and Am for LU), nb x nb per sample]
@@ -82,8 +84,8 @@ WsLayout layout(Kind kind, int64_t chunk, int64_t n, int nb, bool copies, bool h
   if (!kind_herm(kind)) off = align_up(off + (size_t)chunk * L.strideM * es);
   L.d_off = off;
   if (kind_herm(kind)) off = align_up(off + 2 * (size_t)chunk * nb * 8);
-  L.ut_off = off;  // W21 (Hermitian) or U12^T (LU): two pair buffers of two panels each
-  off = align_up(off + 4 * (size_t)chunk * (size_t)L.strideU * es);
+  L.ut_off = off;  // W21 (Hermitian) or U12^T (LU): two group buffers of max(G, 2) panels each
+  off = align_up(off + 2 * (size_t)std::max(group_size(), 2) * chunk * (size_t)L.strideU * es);
   L.dh_off = off;  // Hermitian: D of every pivot so far (chunk x n), the column-chunked schedule
   if (kind_herm(kind)) off = align_up(off + (size_t)chunk * (size_t)std::max<int64_t>(n, 1) * 8);
   L.k_off = off;
@@ -192,8 +194,8 @@ int device_sms() {
 // SMs to leave to the lookahead stream while the trailing update (b) of this step runs
 // persistently on the rest: minimise max(T1, T2) with T1 = diag latency + (tiles of the next
 // block column's update + next panel) / R, T2 = tiles of (b) / (SMs - R), in units of one tile.
-// g = 2 for the second step of a pair: its trailing update has K = 2nb (twice the tile time) and
-// the chain beside it holds the next pair's two diag tiles and two panels.
+// g = G for the last step of a group: its trailing update has K = G nb (G times the tile time) and
+// the chain beside it holds the next group's G diag tiles and G panels.
 int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile, bool herm, int g = 1) {
   // the diag tile in update-tile times (DPP_DIAG_TILES; 5 measured ~100 us vs ~20 us; after the
   // diag kernel went to 63 us, 2.5 .. 5 give the same C4 / UST rates within noise)
@@ -262,18 +264,19 @@ int chunk_cols(bool host, int64_t n) {
 // vs 19.3 TF/s at n = 16384) -- the right-looking order needs every column before the first
 // trailing update completes, and the work a left-looking order could do on the first columns is
 // small, so little of the copy can hide behind compute.
-// Paired trailing updates (Hermitian, lookahead on): the trailing update of an even step is
-// deferred and applied together with the next step's, one DMMA pass with K = 2 nb (the two panels
-// are adjacent columns of the factor; their pre-scaled copies W21 are stacked in one buffer), so
-// the update kernel's per-tile epilogue and the C read/write are amortized over twice the work.
-// DPP_PAIR=0 turns it off.
-bool pair_updates() {
+// Grouped trailing updates (lookahead on): the trailing updates of G consecutive steps are applied
+// by the group's last step as ONE DMMA pass with K = G nb (the G panels are adjacent columns of the
+// factor; their operand copies -- W21 = L21 D1, or U12^T -- are stacked in one buffer), so the
+// update kernel's per-tile epilogue and the C read/write are amortized over G times the work.
+// G = 2 ("paired updates") by default; DPP_GROUP=g sets G, DPP_PAIR=0 turns grouping off.
+int group_size() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("DPP_PAIR");
-    v = (e && e[0] == '0') ? 0 : 1;
+    const char* g = getenv("DPP_GROUP");
+    v = (e && e[0] == '0') ? 1 : (g ? std::max(1, std::min(8, atoi(g))) : 2);
   }
-  return v == 1;
+  return v;
 }
 
 // rows below which the real Hermitian sampler switches to half-width blocks (DPP_TAIL_ROWS, 0 = off)
@@ -341,8 +344,8 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
   void* Am = work + L.am_off;
   int step = 0;
   bool have_rest = false;
-  bool pair_open = false;  // the previous step deferred its trailing update to this one
-  bool prev_psecond = false;  // the previous step was the second of a pair
+  int gpos = -1;            // position of the previous step in its group (-1: none)
+  bool prev_glast = false;  // the previous step was the last of a group
   const int sms = device_sms();
   if (!herm || !la || ch.cw < nb || ch.cw % nb) ch.cw = 0;
   if (ch.cw && (n + ch.cw - 1) / ch.cw > MAX_CHUNKS) ch.cw = (n + MAX_CHUNKS - 1) / MAX_CHUNKS / nb * nb + nb;
@@ -396,20 +399,31 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     // double-buffered like D1
     const int64_t strideU = L.strideU;
     char* UT = work + L.ut_off + (size_t)(step & 1) * batch * strideU * es;
-    // pairing: steps (2p, 2p+1) share the pair buffer (p & 1) of 2 panels per sample
-    const bool pairing = la && !ch.cw && !ch.copy_cw && pair_updates() && nb == (int)std::min<int64_t>(nb, n);
-    const int64_t strideW = 2 * strideU;
-    char* WP = work + L.ut_off + (size_t)((step >> 1) & 1) * batch * strideW * es;
-    // pair roles: the first step of a pair defers its trailing update when the second step has a
-    // trailing region of its own (only while the trailing updates dominate: near the end the chain
-    // is the bound, and a pair's double-width lookahead update lengthens it); the second applies both
-    // panels.  Each step's operand panel (W21 or U12^T) goes to its half of the pair buffer, the
-    // second step's shifted down by nb rows so that row r of both halves is the same matrix row.
-    const int jn0 = (int)std::min<int64_t>(bs_of(j1), m2);
-    const bool pfirst =
-        pairing && !(step & 1) && jb == nb && jn0 == nb && m2 - jn0 > 0 && m2 > pair_min_rows(nb, herm, batch);
-    const bool psecond = pairing && (step & 1) && pair_open;
-    char* const PH = WP + (size_t)(psecond ? strideU + nb : ((step & 1) ? strideU : 0)) * es;  // my half
+    // grouping: steps (G g .. G g + G-1) share the group buffer (g & 1) of G panels per sample
+    const int G = group_size();
+    const bool grouping = la && !ch.cw && !ch.copy_cw && G > 1 && nb == (int)std::min<int64_t>(nb, n);
+    const int64_t strideW = (int64_t)std::max(G, 2) * strideU;
+    char* WP = work + L.ut_off + (size_t)((step / G) & 1) * batch * strideW * es;
+    // group roles: a group starts at a step that is a multiple of G when all its G blocks are full
+    // width, its last step has a trailing region of its own, and the trailing updates still dominate
+    // (near the end the chain is the bound, and a group's G-wide lookahead update lengthens it).
+    // Every step but the last defers its trailing update; the last applies all G panels.  Each
+    // step's operand panel (W21 or U12^T) goes to its slot of the group buffer, slot i shifted down
+    // by i nb rows so that row r of every slot is the same matrix row.
+    int gp = -1;  // this step's position in its group
+    if (grouping) {
+      if (gpos >= 0 && gpos < G - 1) {
+        gp = gpos + 1;
+      } else if (step % G == 0 && m2 - (int64_t)(G - 1) * nb > 0 && m2 > pair_min_rows(nb, herm, batch)) {
+        bool full = true;
+        for (int g = 0; g < G; ++g) full = full && bs_of(j0 + (int64_t)g * nb) == nb;
+        if (full) gp = 0;
+      }
+    }
+    const bool glast = gp == G - 1, gnonlast = gp >= 0 && !glast;
+    char* const PH = WP + (size_t)(gp >= 0 ? gp * (strideU + nb) : (step % G) * strideU) * es;  // my slot
+    char* const WG = WP + (size_t)(gp > 0 ? gp * nb : 0) * es;  // the stacked operand of panels 0..gp
+    const int64_t jg0 = gp > 0 ? j0 - (int64_t)gp * nb : j0;  // the group's first column
     // ---- stage 1
     DiagArgs d{};
     d.A = A; d.ld = ld; d.strideA = strideA; d.n = n; d.j0 = j0; d.tcol = j0; d.jb = jb; d.seed = seed; d.b0 = b0;
@@ -440,8 +454,8 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
         // U12 = L11^-1 A12 = A12 - Am A12 (Am = I - L11^-1), computed transposed so that every
         // operand is K-major:  U12^T = A12^T - A12^T Am^T  in the U12^T buffer, then copied back.
         char* A12 = Ab + (size_t)(j0 + j1 * ld) * es;
-        char* const UTs = pairing ? PH : UT;  // my U12^T panel (pairing: my half of the pair buffer)
-        const int64_t sU = pairing ? strideW : strideU;
+        char* const UTs = grouping ? PH : UT;  // my U12^T panel (grouping: my slot of the group buffer)
+        const int64_t sU = grouping ? strideW : strideU;
         { ProfScope pa(4, 0.0, s1); CK(launch_transpose(es, A12, ld, strideA, UTs, L.ldk, sU, jb, (int)m2, batch, s1)); }
         UpdateArgs q = base_update(kind, batch, vec);
         q.Aop = UTs; q.lda = L.ldk; q.strideA = sU;                                // A12^T (j, k)
@@ -457,15 +471,14 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     // ---- stage 3 operands
     UpdateArgs u = base_update(kind, batch, vec);
     u.Aop = Ab + (size_t)(j1 + j0 * ld) * es; u.lda = ld; u.strideA = strideA;  // L21
-    if (herm && pairing) {
-      // W21 of this step into its half of the pair buffer (the K = 2 nb operand of the second step
-      // starts at row nb of half 0)
+    if (herm && grouping) {
+      // W21 of this step into its slot of the group buffer (the K = (gp+1) nb operand of group
+      // position gp starts at row gp nb of slot 0)
       ProfScope pa(4, 0.0, s1);
-      char* dst = PH;
-      CK(launch_scale_cols(kind, Ab + (size_t)(j1 + j0 * ld) * es, ld, strideA, dst, L.ldk, strideW, dvec,
+      CK(launch_scale_cols(kind, Ab + (size_t)(j1 + j0 * ld) * es, ld, strideA, PH, L.ldk, strideW, dvec,
                            nb, (int)m2, jb, batch, s1));
-      u.Aop = psecond ? WP + (size_t)nb * es : dst; u.lda = L.ldk; u.strideA = strideW;  // W21 (both panels if 2nd)
-      u.Bop = Ab + (size_t)(j1 + (psecond ? j0 - nb : j0) * ld) * es; u.ldb = ld; u.strideB = strideA;
+      u.Aop = gp >= 0 ? WG : PH; u.lda = L.ldk; u.strideA = strideW;  // W21 of panels 0..gp
+      u.Bop = Ab + (size_t)(j1 + jg0 * ld) * es; u.ldb = ld; u.strideB = strideA;
       u.mask = 1; u.conj = (kind == HERM_Z);
     } else if (herm) {
       // A22 -= W21 L21^H with W21 = L21 D1 (pre-scaled copy; the DMMA loop does no scaling)
@@ -475,17 +488,17 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       u.Aop = UT; u.lda = L.ldk; u.strideA = strideU;  // W21
       u.Bop = Ab + (size_t)(j1 + j0 * ld) * es; u.ldb = ld; u.strideB = strideA;  // L21 (conjugated on load)
       u.mask = 1; u.conj = (kind == HERM_Z);
-    } else if (pairing) {
-      u.Aop = Ab + (size_t)(j1 + (psecond ? j0 - nb : j0) * ld) * es;                 // L21 (both if 2nd)
-      u.Bop = psecond ? WP + (size_t)nb * es : PH; u.ldb = L.ldk; u.strideB = strideW;  // U12^T (both if 2nd)
+    } else if (grouping) {
+      u.Aop = Ab + (size_t)(j1 + jg0 * ld) * es;                                    // L21 of panels 0..gp
+      u.Bop = gp >= 0 ? WG : PH; u.ldb = L.ldk; u.strideB = strideW;                // U12^T of panels 0..gp
     } else {
       u.Bop = UT; u.ldb = L.ldk; u.strideB = strideU;  // U12^T (j, k), K-major
     }
     u.C = Ab + (size_t)(j1 + j1 * ld) * es; u.ldc = ld; u.strideC = strideA;
-    u.a_rows = (int)m2; u.b_rows = (int)m2; u.K = psecond ? nb + jb : jb;
-    // width of the lookahead region: the next block -- or, at the second step of a pair, the next
-    // pair's two blocks, so the next pair's whole diag/panel chain runs under this pair's update
-    const int jn = (int)std::min<int64_t>(psecond ? 2 * nb : bs_of(j1), m2);
+    u.a_rows = (int)m2; u.b_rows = (int)m2; u.K = (gp > 0 ? gp * nb : 0) + jb;
+    // width of the lookahead region: the next block -- or, at the last step of a group, the next
+    // group's G blocks, so the next group's whole diag/panel chain runs under this group's update
+    const int jn = (int)std::min<int64_t>(glast ? (int64_t)G * nb : bs_of(j1), m2);
     if (!la) {
       u.row0 = 0; u.col0 = 0; u.rows = (int)m2; u.cols = (int)m2; u.tri = herm;
       ProfScope ps(3, region_flops(kind, 0, 0, m2, m2, jb) * batch, s1);
@@ -495,10 +508,10 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     CK(cudaEventRecord(ds->ev_panel, s1));
     // (a) next block column [0, jn) x rows [0, m2)  (+ LU: next block row [0, jn) x cols [jn, m2));
     // chunked: only while the next block is in this chunk (else the catch-up update covers it)
-    // (the first step of a pair needs no wait: its lookahead block was covered by the previous
-    // pair's lookahead update and is not part of the previous trailing update)
-    if (have_rest && !(pfirst && prev_psecond)) CK(cudaStreamWaitEvent(s1, ds->ev_rest, 0));
-    prev_psecond = psecond;
+    // (a non-last step of a group needs no wait: its lookahead block was covered by the previous
+    // group's lookahead update and is not part of the previous trailing update)
+    if (have_rest && !(gnonlast && (gp > 0 || prev_glast))) CK(cudaStreamWaitEvent(s1, ds->ev_rest, 0));
+    prev_glast = glast;
     if (j1 < ce) {
       UpdateArgs ua = u;
       ua.row0 = 0; ua.col0 = 0; ua.rows = (int)m2; ua.cols = jn; ua.tri = 0;
@@ -514,14 +527,14 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     }
     // (b) the rest [jn, m2)^2 on S2 (chunked: its columns restricted to the chunk)
     const int64_t colsb = std::min<int64_t>(m2, ce - j1) - jn;
-    pair_open = pfirst;  // the next step applies this step's trailing update with its own
-    if (m2 > jn && colsb > 0 && !pfirst) {
+    gpos = gp;  // a non-last position: the group's last step applies this step's trailing update
+    if (m2 > jn && colsb > 0 && !gnonlast) {
       CK(cudaStreamWaitEvent(s2, ds->ev_panel, 0));
       UpdateArgs ub = u;
       ub.row0 = jn; ub.col0 = jn; ub.rows = (int)(m2 - jn); ub.cols = (int)colsb;
       ub.tri = herm && colsb == m2 - jn;
       if (vec)
-        ub.grid_limit = sms - reserve_sms(m2, jn, sms, batch, kind_cplx(kind) ? 64 : 128, herm, psecond ? 2 : 1);
+        ub.grid_limit = sms - reserve_sms(m2, jn, sms, batch, kind_cplx(kind) ? 64 : 128, herm, glast ? G : 1);
       if (ch.copy_cw && ch.ev && step < ch.split_steps) {
         // one launch per copy chunk of the trailing columns, each gated by its own chunk
         for (int64_t g0 = j1 + jn; g0 < j1 + jn + colsb;) {

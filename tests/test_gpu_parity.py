@@ -245,6 +245,48 @@ print("GENERIC_OK")
     assert "GENERIC_OK" in r.stdout, r.stdout + r.stderr
 
 
+@pytest.mark.parametrize("group", ["3", "4"])
+def test_grouped_trailing_updates_subprocess(group):
+    """Trailing updates grouped by G = 3 and 4 steps (DPP_GROUP; one K = G nb pass applied by the
+    group's last step, the lookahead update of the middle steps with K = (i+1) nb) give the
+    oracle's samples and factors for all three kinds, single and batched, at sizes where several
+    groups form and a ragged tail stays ungrouped (each run in a fresh process)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, oracle, workloads as W, paper_1905_00165_b200 as dpp
+from tests.gpu_util import to_device, from_device, compare_masks, assert_factor_close, assert_loglik_close
+for kind, n in (("herm_d", 1111), ("herm_z", 555), ("lu_z", 480)):
+    K = W.haar_kernel(n, seed=n, complex_=(kind != "herm_d"))
+    if kind == "lu_z":
+        K = W.similarity(K, seed=n)
+    fn = {"herm_d": oracle.sample_herm_d, "herm_z": oracle.sample_herm_z, "lu_z": oracle.sample_lu_z}[kind]
+    o = fn(K, 5, 0)
+    Kc = to_device(K, kind)
+    s = dpp.sample(kind, Kc, 5)
+    torch.cuda.synchronize()
+    compare_masks(s.mask.cpu().numpy(), o)
+    if o.n_ties == 0:
+        assert_factor_close(from_device(Kc, n), o.factor, K, kind)
+        assert_loglik_close(float(s.loglik), o.loglik)
+    # batched: samples b0 .. b0 + 2 of the same kernel
+    Kb = to_device(K, kind)
+    sb = dpp.sample_batched(kind, Kb, 3, seed=5, b0=1)
+    torch.cuda.synchronize()
+    for b in range(3):
+        ob = fn(K, 5, 1 + b)
+        compare_masks(sb.mask[b].cpu().numpy(), ob)
+        if ob.n_ties == 0:
+            assert_loglik_close(float(sb.loglik[b]), ob.loglik)
+print("GROUP_OK")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PYTHONPATH=root, DPP_GROUP=group, DPP_PAIR_MIN_ROWS="0")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert "GROUP_OK" in r.stdout, r.stdout + r.stderr
+
+
 def test_column_chunked_schedule_subprocess():
     """The column-chunked schedule (DPP_CHUNK_COLS=256: right-looking inside 256-column chunks, a
     K = c0 catch-up GEMM per chunk, and for the _host entry point the copy pipelined chunk by chunk
