@@ -297,9 +297,26 @@ static int ws_variant() {
   return v;
 }
 
+// DPP_WS_SMALL=1: small non-persistent launches (the chain's panel GEMM and lookahead column: at
+// most one 128 x 128 tile per free SM) take the 64 x 128 tiles of variant 2 -- such a launch runs
+// in one wave, so its duration is one tile's latency.  Off by default: measured neutral at C4
+// (26.62 / 26.76 vs 26.61 / 26.61 TF/s, panel stage 78.4 vs 78.6 ms per 5 samples) -- the
+// per-launch fixed costs (launch, C-tile load, ring fill, store) dominate a one-tile launch.
+static bool ws_small_tiles(const UpdateArgs& a) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPP_WS_SMALL");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (!v || a.grid_limit > 0 || a.bcc_P != 0) return false;
+  const long long tm = (a.rows + 127) / 128, tn = (a.cols + 127) / 128;
+  return tm * tn * a.batch <= num_sms() / 2;
+}
+
 template <bool CPLX, bool BNMAJ, bool MASK, bool SCALE, bool CONJ>
 cudaError_t launch_update_ws_t(UpdateArgs a, cudaStream_t s) {
   if constexpr (!CPLX) {
+    if (ws_variant() == 1 && ws_small_tiles(a)) return launch_update_ws_v<CPLX, BNMAJ, MASK, SCALE, CONJ, 2>(a, s);
     if (ws_variant() == 1) return launch_update_ws_v<CPLX, BNMAJ, MASK, SCALE, CONJ, 1>(a, s);
     if (ws_variant() == 2) return launch_update_ws_v<CPLX, BNMAJ, MASK, SCALE, CONJ, 2>(a, s);
   }
