@@ -356,7 +356,7 @@ static cudaError_t launch_diag_nt(const DiagArgs& a, cudaStream_t s) {
 
 // Threads per tile CTA: 256 (8 x 8 register blocks per thread at nb = 128).  DPP_DIAG_NT=512
 // selects a 32 x 16 thread grid for tiles of 64 and more (measured slower at nb = 128: 107 vs
-// 101 us per tile -- the per-pivot chain, not the update FLOPs, bounds this kernel).
+// 101 us per tile at the time -- the per-pivot chain, not the update FLOPs, bounds this kernel).
 static int diag_nt_override() {
   static int v = -1;
   if (v < 0) {

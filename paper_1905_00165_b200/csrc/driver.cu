@@ -290,7 +290,7 @@ int64_t tail_rows() {
 }
 
 // trailing size below which updates are no longer paired (DPP_PAIR_MIN_ROWS; defaults: 6144 rows
-// for 128-wide Hermitian blocks, where the 86-us diag tile makes the chain the bound near the end --
+// for 128-wide Hermitian blocks, where the 63..86-us diag tile makes the chain the bound near the end --
 // measured C4 25.8 -> 26.1 TF/s -- 0 for 64-wide Hermitian blocks, whose chain is short (complex
 // Hermitian n = 8192: 27.0 vs 26.6 TF/s with 6144), 8192 for LU)
 int64_t pair_min_rows(int nb, bool herm, int batch) {

@@ -8,8 +8,9 @@
 //  * one PRODUCER warp streams operand K-chunks with TMA bulk copies (cp.async.bulk, one 1-D copy
 //    per column segment into padded shared rows) into a STAGES-deep ring guarded by full/empty
 //    mbarriers; a second warp owns the C tile (bulk load -> consumers subtract -> bulk store);
-//  * eight CONSUMER warps run DMMA.8x8x4 (mma.sync m8n8k4 f64) out of the ring with no CTA-wide
-//    barrier in the main loop and subtract their accumulators from the C tile in shared memory.
+//  * CONSUMER warps (real: 16 of 32x32 in the default layout V1; complex: 8 of 32x16) run
+//    DMMA.8x8x4 (mma.sync m8n8k4 f64) out of the ring with no CTA-wide barrier in the main loop and
+//    subtract their accumulators from the C tile in shared memory.
 // Ragged edges: rows/columns beyond the tile are left stale in shared memory (they only feed
 // masked outputs); K-columns beyond jb are zero-filled; an odd trailing row (real) is moved with
 // ordinary loads/stores.
