@@ -449,6 +449,12 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       p.C = Ab + (size_t)(j1 + j0 * ld) * es; p.ldc = ld; p.strideC = strideA;    // L21 in place
       p.a_rows = (int)m2; p.b_rows = jb; p.K = jb;
       p.row0 = 0; p.col0 = 0; p.rows = (int)m2; p.cols = jb;
+      if (herm) {
+        // and the pre-scaled copy W21 = L21 D1 (the trailing-update operand) into its panel slot
+        // (written by the panel kernel's epilogue when it is the warp-specialized one)
+        p.wout = grouping ? PH : UT; p.ldw = L.ldk; p.strideWo = grouping ? strideW : strideU;
+        p.wscale = dvec; p.wsstride = nb;
+      }
       CK(launch_update(kind, p, s1));
       if (!herm) {
         // U12 = L11^-1 A12 = A12 - Am A12 (Am = I - L11^-1), computed transposed so that every
@@ -472,19 +478,14 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     UpdateArgs u = base_update(kind, batch, vec);
     u.Aop = Ab + (size_t)(j1 + j0 * ld) * es; u.lda = ld; u.strideA = strideA;  // L21
     if (herm && grouping) {
-      // W21 of this step into its slot of the group buffer (the K = (gp+1) nb operand of group
-      // position gp starts at row gp nb of slot 0)
-      ProfScope pa(4, 0.0, s1);
-      CK(launch_scale_cols(kind, Ab + (size_t)(j1 + j0 * ld) * es, ld, strideA, PH, L.ldk, strideW, dvec,
-                           nb, (int)m2, jb, batch, s1));
+      // W21 of this step is in its slot of the group buffer (written with the panel; the
+      // K = (gp+1) nb operand of group position gp starts at row gp nb of slot 0)
       u.Aop = gp >= 0 ? WG : PH; u.lda = L.ldk; u.strideA = strideW;  // W21 of panels 0..gp
       u.Bop = Ab + (size_t)(j1 + jg0 * ld) * es; u.ldb = ld; u.strideB = strideA;
       u.mask = 1; u.conj = (kind == HERM_Z);
     } else if (herm) {
-      // A22 -= W21 L21^H with W21 = L21 D1 (pre-scaled copy; the DMMA loop does no scaling)
-      ProfScope pa(4, 0.0, s1);
-      CK(launch_scale_cols(kind, Ab + (size_t)(j1 + j0 * ld) * es, ld, strideA, UT, L.ldk, strideU, dvec,
-                           nb, (int)m2, jb, batch, s1));
+      // A22 -= W21 L21^H with W21 = L21 D1 (pre-scaled copy written with the panel; the DMMA loop
+      // does no scaling)
       u.Aop = UT; u.lda = L.ldk; u.strideA = strideU;  // W21
       u.Bop = Ab + (size_t)(j1 + j0 * ld) * es; u.ldb = ld; u.strideB = strideA;  // L21 (conjugated on load)
       u.mask = 1; u.conj = (kind == HERM_Z);

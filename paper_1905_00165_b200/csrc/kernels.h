@@ -74,6 +74,14 @@ struct UpdateArgs {
   // column 0, row j1 (A22 row 0); bcc_j1 = global index of A22 row 0.
   int bcc_P, bcc_r, bcc_nb, bcc_q0;
   int64_t bcc_j1;
+  // optional second output W = C_new diag(wscale) over the region (the Hermitian panel's
+  // pre-scaled copy W21 = L21 D1): element (i, j) at i + j*ldw, wscale[j] per column, strides per
+  // sample strideWo / wsstride.  Written by the consumer warps of the warp-specialized panel
+  // kernel (fused) or, for the other kernels, by a column-scaling pass after the update.
+  void* wout;
+  int64_t ldw, strideWo;
+  const double* wscale;
+  int64_t wsstride;
 };
 
 cudaError_t launch_diag(Kind kind, int nb, const DiagArgs& a, cudaStream_t s);

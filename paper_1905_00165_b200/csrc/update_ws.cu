@@ -230,6 +230,20 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, (V == 2) ? 2 : 
     mbar_wait(cfull, cphase);
     cphase ^= 1;
     acc.template subtract_into<MASK, TM, TN, LY::LDC>(Cs, wm, wn, lane, ti);
+    if constexpr (!MASK) {
+      if (a.wout) {
+        // second output W = C_new diag(wscale) (the Hermitian panel's W21 = L21 D1): each warp
+        // re-reads its own TM x TN part of the updated tile, one row per lane, coalesced stores
+        __syncwarp();
+        T* Wg = reinterpret_cast<T*>(a.wout) + (int64_t)ti.s * a.strideWo + ti.grow0 + (int64_t)ti.gcol0 * a.ldw;
+        const double* d = a.wscale + (int64_t)ti.s * a.wsstride + ti.gcol0;
+        for (int c = wn * TN; c < wn * TN + TN && c < ti.ncols; ++c) {
+          const double dc = __ldg(d + c);
+          for (int r = wm * TM + lane; r < wm * TM + TM && r < ti.nrows; r += 32)
+            Wg[r + (int64_t)c * a.ldw] = scal(Cs[c * LY::LDC + r], dc);
+        }
+      }
+    }
     if (ti.diag) {
       // Hermitian diagonal tile: element stores that never touch the strict upper triangle
       T* Cg = reinterpret_cast<T*>(a.C) + (int64_t)ti.s * a.strideC;

@@ -211,13 +211,14 @@ def test_large_parity_2048(oracle_mod):
 
 
 @pytest.mark.parametrize("env", [{"DPP_UPDATE_GENERIC": "1"}, {"DPP_WS_VARIANT": "0"}, {"DPP_WS_VARIANT": "2"},
-                                 {"DPP_WS_SMALL": "1"}, {"DPP_DIAG_NT": "512"},
+                                 {"DPP_WS_SMALL": "1"}, {"DPP_FUSE_W": "0"}, {"DPP_DIAG_NT": "512"},
                                  {"DPP_DIAG_BLOCKED": "1"}, {"DPP_PAIR": "0"}, {"DPP_TAIL_ROWS": "200"},
                                  {"DPP_PAIR_MIN_ROWS": "0"}])
 def test_alternate_update_kernels_subprocess(env):
     """The cp.async fallback update kernel (DPP_UPDATE_GENERIC=1), the 8-consumer-warp layout of
     the warp-specialized kernel (DPP_WS_VARIANT=0), its 64 x 128-tile layout for every launch
-    (DPP_WS_VARIANT=2) or for the small chain launches only (DPP_WS_SMALL=1), the 512-thread
+    (DPP_WS_VARIANT=2) or for the small chain launches only (DPP_WS_SMALL=1), the pre-scaled panel
+    copy W21 by a separate column-scaling pass instead of the panel kernel (DPP_FUSE_W=0), the 512-thread
     register-tile diag kernel
     (DPP_DIAG_NT=512), the 32-column-blocked Hermitian diag kernel (DPP_DIAG_BLOCKED=1) and the
     unpaired trailing updates (DPP_PAIR=0: one K = nb update per step) give the same
