@@ -148,7 +148,7 @@ def main():
                          "elementary: Listing 2 on a rank-k projection, n=5000 (the paper's Fig. setting); lensemble: "
                          "K = I - (L+I)^{-1} at n=16384")
     ap.add_argument("--batch", type=int, default=1024, help="ust: samples per GPU per step")
-    ap.add_argument("--batch-chunk", type=int, default=256, help="ust: samples factored concurrently")
+    ap.add_argument("--batch-chunk", type=int, default=1024, help="ust: samples factored concurrently")
     ap.add_argument("--aztec-d", type=int, default=80, help="aztec_c: diamond order")
     ap.add_argument("--tally", type=int, default=0, help="aztec_c: untimed extra batches whose tilings are all checked")
     ap.add_argument("--rank", type=int, default=500, help="elementary: projection rank k")

@@ -424,6 +424,10 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     char* const PH = WP + (size_t)(gp >= 0 ? gp * (strideU + nb) : (step % G) * strideU) * es;  // my slot
     char* const WG = WP + (size_t)(gp > 0 ? gp * nb : 0) * es;  // the stacked operand of panels 0..gp
     const int64_t jg0 = gp > 0 ? j0 - (int64_t)gp * nb : j0;  // the group's first column
+    bool copyback = false;  // LU: the U12^T -> A12 copy deferred to the trailing stream
+    const char* cb_src = nullptr;
+    char* cb_dst = nullptr;
+    int64_t cb_stride = 0;
     // ---- stage 1
     DiagArgs d{};
     d.A = A; d.ld = ld; d.strideA = strideA; d.n = n; d.j0 = j0; d.tcol = j0; d.jb = jb; d.seed = seed; d.b0 = b0;
@@ -470,8 +474,14 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
         q.a_rows = (int)m2; q.b_rows = jb; q.K = jb;
         q.row0 = 0; q.col0 = 0; q.rows = (int)m2; q.cols = jb;
         CK(launch_update(kind, q, s1));
-        ProfScope pa(4, 0.0, s1);
-        CK(launch_transpose(es, UTs, L.ldk, sU, A12, ld, strideA, (int)m2, jb, batch, s1));  // U12 -> K
+        if (!la) {
+          ProfScope pa(4, 0.0, s1);
+          CK(launch_transpose(es, UTs, L.ldk, sU, A12, ld, strideA, (int)m2, jb, batch, s1));  // U12 -> K
+        } else {
+          // U12 -> K is only output (no later step reads A12): off the chain, on the trailing
+          // stream once the panel is done (below)
+          copyback = true; cb_src = UTs; cb_stride = sU; cb_dst = A12;
+        }
       }
     }
     // ---- stage 3 operands
@@ -507,6 +517,12 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       continue;
     }
     CK(cudaEventRecord(ds->ev_panel, s1));
+    if (copyback) {
+      CK(cudaStreamWaitEvent(s2, ds->ev_panel, 0));
+      ProfScope pa(4, 0.0, s2);
+      CK(launch_transpose(es, cb_src, L.ldk, cb_stride, cb_dst, ld, strideA, (int)m2, jb, batch, s2));  // U12 -> K
+      copyback = false;
+    }
     // (a) next block column [0, jn) x rows [0, m2)  (+ LU: next block row [0, jn) x cols [jn, m2));
     // chunked: only while the next block is in this chunk (else the catch-up update covers it)
     // (a non-last step of a group needs no wait: its lookahead block was covered by the previous
