@@ -307,6 +307,15 @@ int64_t pair_min_rows(int nb, bool herm, int batch) {
   return nb >= 128 ? 6144 : 0;
 }
 
+bool head_block() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPP_HEAD_BLOCK");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 bool copy_gated() {
   static int v = -1;
   if (v < 0) {
@@ -356,7 +365,16 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
   // does not change the sample.
   const int64_t thr = (nb == 128 && herm && la && !ch.cw && !ch.copy_cw) ? tail_rows() : 0;
   auto bs_of = [&](int64_t j) -> int { return (thr > 0 && n - j <= thr) ? nb / 2 : nb; };
-  auto blk = [&](int64_t j) -> int64_t { return std::min<int64_t>(bs_of(j), n - j); };
+  // Head block: when nb does not divide n, the FIRST block takes the remainder (n mod nb) so that
+  // every trailing region is a whole number of 128-row tiles (a ragged last block would leave a
+  // partly empty tile row and column in every trailing update).  Only when the remainder keeps every
+  // block origin 16-byte aligned (the TMA operand copies): a multiple of 16 / element-size rows.
+  // DPP_HEAD_BLOCK=0: ragged last block.
+  const int64_t rem = n % nb;
+  const int64_t head = (head_block() && !ch.cw && !ch.copy_cw && thr == 0 && n > nb && rem &&
+                        rem % (int64_t)(16 / es) == 0) ? rem : 0;
+  const int gbase = head ? 1 : 0;  // groups are aligned after the head block
+  auto blk = [&](int64_t j) -> int64_t { return (head && j == 0) ? head : std::min<int64_t>(bs_of(j), n - j); };
   for (int64_t j0 = 0; j0 < n; j0 += blk(j0), ++step) {
     const int jb = (int)blk(j0);
     const int64_t j1 = j0 + jb, m2 = n - j1;
@@ -403,7 +421,8 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     const int G = group_size();
     const bool grouping = la && !ch.cw && !ch.copy_cw && G > 1 && nb == (int)std::min<int64_t>(nb, n);
     const int64_t strideW = (int64_t)std::max(G, 2) * strideU;
-    char* WP = work + L.ut_off + (size_t)((step / G) & 1) * batch * strideW * es;
+    const int gstep = step - gbase;  // (-1 for the head block: group buffer 1, unused by group 0)
+    char* WP = work + L.ut_off + (size_t)((gstep < 0 ? 1 : gstep / G) & 1) * batch * strideW * es;
     // group roles: a group starts at a step that is a multiple of G when all its G blocks are full
     // width, its last step has a trailing region of its own, and the trailing updates still dominate
     // (near the end the chain is the bound, and a group's G-wide lookahead update lengthens it).
@@ -414,7 +433,8 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     if (grouping) {
       if (gpos >= 0 && gpos < G - 1) {
         gp = gpos + 1;
-      } else if (step % G == 0 && m2 - (int64_t)(G - 1) * nb > 0 && m2 > pair_min_rows(nb, herm, batch)) {
+      } else if (gstep >= 0 && gstep % G == 0 && m2 - (int64_t)(G - 1) * nb > 0 &&
+                 m2 > pair_min_rows(nb, herm, batch)) {
         bool full = true;
         for (int g = 0; g < G; ++g) full = full && bs_of(j0 + (int64_t)g * nb) == nb;
         if (full) gp = 0;

@@ -211,14 +211,16 @@ def test_large_parity_2048(oracle_mod):
 
 
 @pytest.mark.parametrize("env", [{"DPP_UPDATE_GENERIC": "1"}, {"DPP_WS_VARIANT": "0"}, {"DPP_WS_VARIANT": "2"},
-                                 {"DPP_WS_SMALL": "1"}, {"DPP_FUSE_W": "0"}, {"DPP_DIAG_NT": "512"},
+                                 {"DPP_WS_SMALL": "1"}, {"DPP_FUSE_W": "0"}, {"DPP_HEAD_BLOCK": "0"},
+                                 {"DPP_DIAG_NT": "512"},
                                  {"DPP_DIAG_BLOCKED": "1"}, {"DPP_PAIR": "0"}, {"DPP_TAIL_ROWS": "200"},
                                  {"DPP_PAIR_MIN_ROWS": "0"}])
 def test_alternate_update_kernels_subprocess(env):
     """The cp.async fallback update kernel (DPP_UPDATE_GENERIC=1), the 8-consumer-warp layout of
     the warp-specialized kernel (DPP_WS_VARIANT=0), its 64 x 128-tile layout for every launch
     (DPP_WS_VARIANT=2) or for the small chain launches only (DPP_WS_SMALL=1), the pre-scaled panel
-    copy W21 by a separate column-scaling pass instead of the panel kernel (DPP_FUSE_W=0), the 512-thread
+    copy W21 by a separate column-scaling pass instead of the panel kernel (DPP_FUSE_W=0), the
+    ragged block last instead of first (DPP_HEAD_BLOCK=0), the 512-thread
     register-tile diag kernel
     (DPP_DIAG_NT=512), the 32-column-blocked Hermitian diag kernel (DPP_DIAG_BLOCKED=1) and the
     unpaired trailing updates (DPP_PAIR=0: one K = nb update per step) give the same
@@ -261,7 +263,8 @@ def test_grouped_trailing_updates_subprocess(group):
     code = r'''
 import numpy as np, torch, oracle, workloads as W, paper_1905_00165_b200 as dpp
 from tests.gpu_util import to_device, from_device, compare_masks, assert_factor_close, assert_loglik_close
-for kind, n in (("herm_d", 1111), ("herm_z", 555), ("lu_z", 480)):
+for kind, n in (("herm_d", 1111), ("herm_d", 1130), ("herm_z", 555), ("lu_z", 480)):
+    # (1130: an even remainder, so the head block is taken -- on the aligned batched copies too)
     K = W.haar_kernel(n, seed=n, complex_=(kind != "herm_d"))
     if kind == "lu_z":
         K = W.similarity(K, seed=n)
@@ -360,7 +363,8 @@ def test_host_copy_gated_subprocess():
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PYTHONPATH=root, DPP_COPY_GATED="1", DPP_PAIR="0")  # same update grouping on both paths
+    env = dict(os.environ, PYTHONPATH=root, DPP_COPY_GATED="1", DPP_PAIR="0",
+               DPP_HEAD_BLOCK="0")  # same blocking and update grouping on both paths
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-k", "test_host_equals_device_path",
                         os.path.join(root, "tests", "test_gpu_parity.py")], cwd=root, env=env, capture_output=True,
                        text=True, timeout=900)
