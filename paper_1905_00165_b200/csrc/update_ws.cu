@@ -216,15 +216,28 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, (V == 2) ? 2 : 
     if (!ti.valid) continue;
     MmaAcc<CPLX, MI, NI> acc;
     acc.zero();
-    for (int kc = a.ktri ? ti.grow0 / C::KC : 0; kc < nchunks; ++kc) {
-      mbar_wait(&full[stage], phase);
-      const T* As = ring + stage * LY::STAGE_ELEMS;
-      mma_chunk<CPLX, BNMAJ, SCALE, CONJ, C::KC, MI, NI, LY::LDA, LY::LDBK, LY::LDBN>(
-          acc, As, As + LY::A_ELEMS, reinterpret_cast<const double*>(As + LY::A_ELEMS + LY::B_ELEMS), wm * TM,
-          wn * TN, lane);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+    // a warp tile strictly above the diagonal of a masked diagonal tile writes nothing: it only
+    // keeps pace with the ring (waits and releases every stage) and leaves the DMMA pipe to the others
+    const bool idle = MASK && ti.diag && ti.gcol0 + wn * TN > ti.grow0 + wm * TM + TM - 1;
+    const int kc0 = a.ktri ? ti.grow0 / C::KC : 0;
+    if (idle) {
+      for (int kc = kc0; kc < nchunks; ++kc) {
+        mbar_wait(&full[stage], phase);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    } else {
+      for (int kc = kc0; kc < nchunks; ++kc) {
+        mbar_wait(&full[stage], phase);
+        const T* As = ring + stage * LY::STAGE_ELEMS;
+        mma_chunk<CPLX, BNMAJ, SCALE, CONJ, C::KC, MI, NI, LY::LDA, LY::LDBK, LY::LDBN>(
+            acc, As, As + LY::A_ELEMS, reinterpret_cast<const double*>(As + LY::A_ELEMS + LY::B_ELEMS), wm * TM,
+            wn * TN, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
     }
     // ---- epilogue: C -= acc in shared memory; the C warp writes the tile back
     mbar_wait(cfull, cphase);
