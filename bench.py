@@ -138,6 +138,8 @@ def main():
     ap.add_argument("--n", type=int, default=N)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--prof", choices=["trailing", "all"], default="trailing",
+                    help="c4: stages bracketed by events inside the timed region")
     ap.add_argument("--workload", default="c4", choices=["c4", "ust", "dist", "dist_z", "herm_z", "lu_z", "aztec", "herm_s", "aztec_c", "elementary", "lensemble"],
                     help="c4 (default, BASELINE configs[3]); ust: configs[1] batch of UST samples per GPU; "
                          "dist / dist_z: configs[4] 1D block-column-cyclic single sample over all ranks (real n=65536 / "
@@ -203,13 +205,15 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    dpp.dpp_profile_begin()
+    # the trailing update's launches are bracketed by events inside the timed region (the roofline's
+    # live measurement); --prof all also brackets every chain launch there
+    dpp.dpp_profile_begin_stages(0x1F if args.prof == "all" else 1 << dpp.STAGES.index("update_trailing"))
     e0.record(stream)
     for i in range(args.steps):
         step(args.warmup + i)
     e1.record(stream)
     torch.cuda.synchronize()
-    prof = dpp.dpp_profile_end()
+    prof = _fill_stages(dpp.dpp_profile_end(), step, args)
     if world > 1:
         dist.barrier()
     clocks = clk.stop()
@@ -346,8 +350,11 @@ def _traffic():
         return None
 
 
-def _timed(fn, steps, warmup, world, dist):
+def _timed(fn, steps, warmup, world, dist, prof_mask=0):
+    """Warm-up, then `steps` timed calls between CUDA events; with prof_mask the stages it names
+    are bracketed by events inside the timed region (read with dpp.dpp_profile_end())."""
     import torch
+    import paper_1905_00165_b200 as dpp
     for i in range(warmup):
         fn(i)
     torch.cuda.synchronize()
@@ -357,6 +364,8 @@ def _timed(fn, steps, warmup, world, dist):
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if prof_mask:
+        dpp.dpp_profile_begin_stages(prof_mask)
     e0.record()
     for i in range(steps):
         fn(warmup + i)
@@ -369,6 +378,22 @@ def _timed(fn, steps, warmup, world, dist):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item()), clocks
+
+
+def _fill_stages(prof, step, args):
+    """With --prof trailing only the trailing update was bracketed inside the timed region: the
+    other stages' launches and times come from one more (untimed) step with every stage bracketed,
+    scaled to the K timed steps."""
+    import torch
+    import paper_1905_00165_b200 as dpp
+    if args.prof == "all":
+        return prof
+    dpp.dpp_profile_begin()
+    step(args.warmup + args.steps)
+    torch.cuda.synchronize()
+    one = dpp.dpp_profile_end()
+    return {k: (v if k == "update_trailing" else {kk: vv * args.steps for kk, vv in one[k].items()})
+            for k, v in prof.items()}
 
 
 def extra_workload(args):
@@ -424,9 +449,9 @@ def extra_workload(args):
 
         def step(i):
             dpp.dpp_sample_lu_z_batched(1, n, Kc, n, 0, SEED, rank * 1000 + i, mask, ll, None, opts, work)
-        dpp.dpp_profile_begin()
-        ms, clocks = _timed(step, args.steps, args.warmup, world, dist)
-        prof = dpp.dpp_profile_end()
+        ms, clocks = _timed(step, args.steps, args.warmup, world, dist,
+                            0x1F if args.prof == "all" else 1 << dpp.STAGES.index("update_trailing"))
+        prof = _fill_stages(dpp.dpp_profile_end(), step, args)
         ok = W.is_aztec_tiling(d, mask[0].cpu().numpy())
         flops = 8.0 * n ** 3 / 3.0 * args.steps * world  # complex LU, paper convention (R11)
         up = prof["update_trailing"]
@@ -456,9 +481,9 @@ def extra_workload(args):
 
         def step(i):
             dpp.dpp_sample_herm_s_batched(1, n, Kc, n, 0, SEED, rank * 1000 + i, mask, ll, None, opts, work)
-        dpp.dpp_profile_begin()
-        ms, clocks = _timed(step, args.steps, args.warmup, world, dist)
-        prof = dpp.dpp_profile_end()
+        ms, clocks = _timed(step, args.steps, args.warmup, world, dist,
+                            0x1F if args.prof == "all" else 1 << dpp.STAGES.index("update_trailing"))
+        prof = _fill_stages(dpp.dpp_profile_end(), step, args)
         flops = model_flops(n) * args.steps * world
         up = prof["update_trailing"]
         ach = up["flops"] / max(up["ms"], 1e-9) / 1e9

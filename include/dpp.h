@@ -290,6 +290,9 @@ typedef struct {
   double flops[5];
 } dpp_profile_t;
 int dpp_profile_begin(void);
+/* The same, recording only the stages whose bit (1 << stage) is set in stage_mask
+ * (the others launch without events).  DPP_EINVAL if stage_mask has no bit 0..4. */
+int dpp_profile_begin_stages(unsigned stage_mask);
 int dpp_profile_end(dpp_profile_t* out);
 
 const char* dpp_strerror(int code);

@@ -80,6 +80,7 @@ class dpp_profile_t(ctypes.Structure):
 
 
 _sig("dpp_profile_begin", ctypes.c_int, [])
+_sig("dpp_profile_begin_stages", ctypes.c_int, [ctypes.c_uint])
 _sig("dpp_profile_end", ctypes.c_int, [ctypes.POINTER(dpp_profile_t)])
 _sig("dpp_strerror", ctypes.c_char_p, [ctypes.c_int])
 _sig("dpp_version", ctypes.c_char_p, [])
@@ -92,7 +93,7 @@ EXPORTS = ["dpp_workspace_bytes", "dpp_sample_herm_d", "dpp_sample_herm_z", "dpp
            "dpp_sample_herm_d_batched", "dpp_sample_herm_z_batched", "dpp_sample_lu_z_batched",
            "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host",
            "dpp_philox_uniforms", "dpp_comm_init", "dpp_comm_destroy", "dpp_bcc_local_cols",
-           "dpp_dist_workspace_bytes", "dpp_sample_herm_d_dist", "dpp_sample_herm_z_dist", "dpp_profile_begin", "dpp_profile_end",
+           "dpp_dist_workspace_bytes", "dpp_sample_herm_d_dist", "dpp_sample_herm_z_dist", "dpp_profile_begin", "dpp_profile_begin_stages", "dpp_profile_end",
            "dpp_strerror", "dpp_version"]
 
 
@@ -294,6 +295,11 @@ STAGES = ("diag", "panel", "update_lookahead", "update_trailing", "aux")
 
 def dpp_profile_begin():
     _check(_lib.dpp_profile_begin())
+
+
+def dpp_profile_begin_stages(stage_mask: int):
+    """Record only the stages whose bit (1 << STAGES.index(name)) is set."""
+    _check(_lib.dpp_profile_begin_stages(stage_mask))
 
 
 def dpp_profile_end() -> dict:

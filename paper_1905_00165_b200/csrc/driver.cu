@@ -146,6 +146,7 @@ int check_device() {
 struct ProfRec { int stage; double flops; cudaEvent_t e0, e1; };
 struct Profiler {
   bool on = false;
+  unsigned mask = 0x1f;  // stages recorded
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
@@ -159,7 +160,7 @@ thread_local Profiler g_prof;
 struct ProfScope {  // brackets one launch with events on its stream
   int stage; double flops; cudaStream_t s; cudaEvent_t e1 = nullptr;
   ProfScope(int st, double fl, cudaStream_t str) : stage(st), flops(fl), s(str) {
-    if (g_prof.on) {
+    if (g_prof.on && (g_prof.mask >> st & 1u)) {
       cudaEvent_t e0 = g_prof.get();
       e1 = g_prof.get();
       cudaEventRecord(e0, s);
@@ -827,12 +828,16 @@ int dpp_philox_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, d
   return launch_uniforms(seed, j0, b, count, u, (cudaStream_t)stream) == cudaSuccess ? DPP_OK : DPP_ECUDA;
 }
 
-int dpp_profile_begin(void) {
+int dpp_profile_begin_stages(unsigned stage_mask) {
+  if (!(stage_mask & 0x1fu)) return DPP_EINVAL;
   g_prof.recs.clear();
   g_prof.used = 0;
+  g_prof.mask = stage_mask & 0x1fu;
   g_prof.on = true;
   return DPP_OK;
 }
+
+int dpp_profile_begin(void) { return dpp_profile_begin_stages(0x1fu); }
 
 int dpp_profile_end(dpp_profile_t* out) {
   g_prof.on = false;
