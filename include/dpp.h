@@ -233,6 +233,28 @@ int dpp_sample_lu_z_host(int64_t batch, int64_t n, const dpp_complex_t* K, int64
                          double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
                          size_t work_bytes, dpp_stream_t stream);
 
+/* ---- asynchronous host-buffer entry points (pipelined serving) ------------
+ * Same as *_host but stream-ordered: the H2D copy of K, the sample and the D2H
+ * copies of mask / loglik / info are ENQUEUED on `stream` and the call returns
+ * without waiting; results are valid once `stream` has completed.  Host buffers
+ * must be pinned (page-locked) and stay valid until then; `work` must not be
+ * reused by another call before then.  Two calls on two streams with two
+ * workspaces overlap the second call's H2D copy with the first call's
+ * factorization (the factorization itself runs on the library's per-device
+ * stream pair, in call order). */
+int dpp_sample_herm_d_host_async(int64_t batch, int64_t n, const double* K, int64_t ld,
+                                 int64_t strideK, uint64_t seed, uint64_t b0, uint8_t* mask,
+                                 double* loglik, dpp_info_t* info, const dpp_opts_t* opts,
+                                 void* work, size_t work_bytes, dpp_stream_t stream);
+int dpp_sample_herm_z_host_async(int64_t batch, int64_t n, const dpp_complex_t* K, int64_t ld,
+                                 int64_t strideK, uint64_t seed, uint64_t b0, uint8_t* mask,
+                                 double* loglik, dpp_info_t* info, const dpp_opts_t* opts,
+                                 void* work, size_t work_bytes, dpp_stream_t stream);
+int dpp_sample_lu_z_host_async(int64_t batch, int64_t n, const dpp_complex_t* K, int64_t ld,
+                               int64_t strideK, uint64_t seed, uint64_t b0, uint8_t* mask,
+                               double* loglik, dpp_info_t* info, const dpp_opts_t* opts,
+                               void* work, size_t work_bytes, dpp_stream_t stream);
+
 /* ---- device Philox uniforms (the generator the sampler uses) ---------------
  * u[i] = u(seed, j0 + i, b) for i < count, written to DEVICE u.  Exposed so the
  * generator can be checked against curand and the oracle (reading R2). */

@@ -61,7 +61,8 @@ for _n in ("dpp_sample_herm_d_batched", "dpp_sample_herm_z_batched", "dpp_sample
            "dpp_sample_herm_s_batched", "dpp_sample_lu_c_batched", "dpp_elementary_workspace_bytes",
            "dpp_elementary_herm_d", "dpp_lensemble_workspace_bytes", "dpp_lensemble_to_marginal_d",
            "dpp_lensemble_to_marginal_z",
-           "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host"):
+           "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host",
+           "dpp_sample_herm_d_host_async", "dpp_sample_herm_z_host_async", "dpp_sample_lu_z_host_async"):
     _sig(_n, ctypes.c_int, [_I64, _I64, _P, _I64, _I64, _U64, _U64, _P, _P, _P, _P, _P, _SZ, _P])
 _sig("dpp_elementary_workspace_bytes", _SZ, [_I64, _I64, _I64])
 _sig("dpp_lensemble_workspace_bytes", _SZ, [ctypes.c_int, _I64])
@@ -91,6 +92,7 @@ EXPORTS = ["dpp_workspace_bytes", "dpp_sample_herm_d", "dpp_sample_herm_z", "dpp
            "dpp_elementary_herm_d", "dpp_lensemble_workspace_bytes", "dpp_lensemble_to_marginal_d",
            "dpp_lensemble_to_marginal_z",
            "dpp_sample_herm_d_batched", "dpp_sample_herm_z_batched", "dpp_sample_lu_z_batched",
+           "dpp_sample_herm_d_host_async", "dpp_sample_herm_z_host_async", "dpp_sample_lu_z_host_async",
            "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host",
            "dpp_philox_uniforms", "dpp_comm_init", "dpp_comm_destroy", "dpp_bcc_local_cols",
            "dpp_dist_workspace_bytes", "dpp_sample_herm_d_dist", "dpp_sample_herm_z_dist", "dpp_profile_begin", "dpp_profile_begin_stages", "dpp_profile_end",
@@ -196,6 +198,9 @@ dpp_sample_lu_z_batched = _batched("dpp_sample_lu_z_batched")
 dpp_sample_herm_d_host = _batched("dpp_sample_herm_d_host")
 dpp_sample_herm_z_host = _batched("dpp_sample_herm_z_host")
 dpp_sample_lu_z_host = _batched("dpp_sample_lu_z_host")
+dpp_sample_herm_d_host_async = _batched("dpp_sample_herm_d_host_async")
+dpp_sample_herm_z_host_async = _batched("dpp_sample_herm_z_host_async")
+dpp_sample_lu_z_host_async = _batched("dpp_sample_lu_z_host_async")
 dpp_sample_herm_s_batched = _batched("dpp_sample_herm_s_batched")
 dpp_sample_lu_c_batched = _batched("dpp_sample_lu_c_batched")
 

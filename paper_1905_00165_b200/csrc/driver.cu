@@ -628,7 +628,7 @@ int sample_inplace(Kind kind, int64_t n, void* K, int64_t ld, uint64_t seed, uin
 
 int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t ld, int64_t strideK, uint64_t seed,
                    uint64_t b0, uint8_t* mask, double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
-                   size_t work_bytes, cudaStream_t st, bool host) {
+                   size_t work_bytes, cudaStream_t st, bool host, bool sync = true) {
   Opts o;
   int rc = resolve_opts(kind, opts, &o);
   if (rc) return rc;
@@ -748,7 +748,7 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
       if (info) CK(cudaMemcpyAsync(info + c0, ifo, sizeof(dpp_info_t) * (size_t)cb, cudaMemcpyDeviceToHost, st));
     }
   }
-  if (host) CK(cudaStreamSynchronize(st));
+  if (host && sync) CK(cudaStreamSynchronize(st));
   return DPP_OK;
 }
 
@@ -806,21 +806,24 @@ int dpp_map_lu_z(int64_t n, dpp_complex_t* K, int64_t ld, uint8_t* mask, double*
   return sample_inplace(LU_Z, n, K, ld, 0, mask, loglik, info, opts, work, work_bytes, (cudaStream_t)stream, true);
 }
 
-#define BATCHED(name, kind, T, host)                                                                          \
+#define BATCHED(name, kind, T, host, sync)                                                                    \
   int name(int64_t batch, int64_t n, const T* K, int64_t ld, int64_t strideK, uint64_t seed, uint64_t b0,     \
            uint8_t* mask, double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,                 \
            size_t work_bytes, dpp_stream_t stream) {                                                           \
     return sample_batched(kind, batch, n, K, ld, strideK, seed, b0, mask, loglik, info, opts, work, work_bytes, \
-                          (cudaStream_t)stream, host);                                                         \
+                          (cudaStream_t)stream, host, sync);                                                   \
   }
-BATCHED(dpp_sample_herm_d_batched, HERM_D, double, false)
-BATCHED(dpp_sample_herm_z_batched, HERM_Z, dpp_complex_t, false)
-BATCHED(dpp_sample_lu_z_batched, LU_Z, dpp_complex_t, false)
-BATCHED(dpp_sample_herm_d_host, HERM_D, double, true)
-BATCHED(dpp_sample_herm_z_host, HERM_Z, dpp_complex_t, true)
-BATCHED(dpp_sample_lu_z_host, LU_Z, dpp_complex_t, true)
-BATCHED(dpp_sample_herm_s_batched, HERM_S, float, false)
-BATCHED(dpp_sample_lu_c_batched, LU_C, dpp_complex64_t, false)
+BATCHED(dpp_sample_herm_d_batched, HERM_D, double, false, true)
+BATCHED(dpp_sample_herm_z_batched, HERM_Z, dpp_complex_t, false, true)
+BATCHED(dpp_sample_lu_z_batched, LU_Z, dpp_complex_t, false, true)
+BATCHED(dpp_sample_herm_d_host, HERM_D, double, true, true)
+BATCHED(dpp_sample_herm_z_host, HERM_Z, dpp_complex_t, true, true)
+BATCHED(dpp_sample_lu_z_host, LU_Z, dpp_complex_t, true, true)
+BATCHED(dpp_sample_herm_d_host_async, HERM_D, double, true, false)
+BATCHED(dpp_sample_herm_z_host_async, HERM_Z, dpp_complex_t, true, false)
+BATCHED(dpp_sample_lu_z_host_async, LU_Z, dpp_complex_t, true, false)
+BATCHED(dpp_sample_herm_s_batched, HERM_S, float, false, true)
+BATCHED(dpp_sample_lu_c_batched, LU_C, dpp_complex64_t, false, true)
 #undef BATCHED
 
 int dpp_philox_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, double* u, dpp_stream_t stream) {

@@ -174,6 +174,33 @@ def test_host_entry_point_matches_batched(oracle_mod):
         assert_loglik_close(float(ll[i]), o.loglik)
 
 
+@pytest.mark.parametrize("kind,n", [("herm_d", 1300), ("herm_z", 500), ("lu_z", 400)])
+def test_host_async_pipelined_matches_sync(kind, n):
+    """The stream-ordered host entry points (*_host_async), four calls in flight on two streams with
+    two workspaces (each call's H2D overlapping the previous call's factorization), give bit for bit
+    the samples of the synchronous *_host calls."""
+    K = _kernel(kind, n, seed=n)
+    npdt = np.float64 if kind == "herm_d" else np.complex128
+    Kh = torch.from_numpy(np.ascontiguousarray(np.asarray(K, dtype=npdt).T)).pin_memory()
+    op = {"herm_d": dpp.DPP_OP_HERM_D, "herm_z": dpp.DPP_OP_HERM_Z, "lu_z": dpp.DPP_OP_LU_Z}[kind] | dpp.DPP_OP_HOST
+    sync_fn = getattr(dpp, f"dpp_sample_{kind}_host")
+    async_fn = getattr(dpp, f"dpp_sample_{kind}_host_async")
+    works = [torch.empty(dpp.dpp_workspace_bytes(op, 1, n), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    strs = [torch.cuda.Stream(), torch.cuda.Stream()]
+    steps = 4
+    ma = [torch.empty((1, n), dtype=torch.uint8).pin_memory() for _ in range(steps)]
+    la = [torch.empty(1, dtype=torch.float64).pin_memory() for _ in range(steps)]
+    for i in range(steps):
+        async_fn(1, n, Kh, n, 0, 13, i, ma[i], la[i], None, None, works[i % 2], stream=strs[i % 2])
+    torch.cuda.synchronize()
+    ms = torch.empty((1, n), dtype=torch.uint8).pin_memory()
+    ls = torch.empty(1, dtype=torch.float64).pin_memory()
+    for i in range(steps):
+        sync_fn(1, n, Kh, n, 0, 13, i, ms, ls, None, None, works[0])
+        assert torch.equal(ma[i], ms), i
+        assert float(la[i][0]) == float(ls[0]), i
+
+
 def test_blocking_and_lookahead_invariance():
     """Blocked = unblocked decisions: nb and lookahead do not change the sample."""
     K = _kernel("herm_d", 900, seed=12)
