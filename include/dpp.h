@@ -308,8 +308,10 @@ int dpp_sample_herm_z_dist(dpp_comm_t comm, int64_t n, dpp_complex_t* K_local, i
  * counts 8, i.e. 4x the real count).  Not reentrant across host threads. */
 typedef struct {
   int64_t launches[5];
-  double ms[5];
+  double ms[5];        /* summed launch durations */
   double flops[5];
+  double ms_union[5];  /* length of the union of the launch intervals (launches of one stage that
+                          overlap -- calls in flight on several streams -- count once) */
 } dpp_profile_t;
 int dpp_profile_begin(void);
 /* The same, recording only the stages whose bit (1 << stage) is set in stage_mask

@@ -77,7 +77,8 @@ _sig("dpp_dist_workspace_bytes", _SZ, [ctypes.c_int, _I64, ctypes.c_int, _P])
 for _n in ("dpp_sample_herm_d_dist", "dpp_sample_herm_z_dist"):
     _sig(_n, ctypes.c_int, [_P, _I64, _P, _I64, _U64, _P, _P, _P, _P, _P, _SZ, _P])
 class dpp_profile_t(ctypes.Structure):
-    _fields_ = [("launches", ctypes.c_int64 * 5), ("ms", ctypes.c_double * 5), ("flops", ctypes.c_double * 5)]
+    _fields_ = [("launches", ctypes.c_int64 * 5), ("ms", ctypes.c_double * 5), ("flops", ctypes.c_double * 5),
+                ("ms_union", ctypes.c_double * 5)]
 
 
 _sig("dpp_profile_begin", ctypes.c_int, [])
@@ -310,8 +311,8 @@ def dpp_profile_begin_stages(stage_mask: int):
 def dpp_profile_end() -> dict:
     p = dpp_profile_t()
     _check(_lib.dpp_profile_end(ctypes.byref(p)))
-    return {st: dict(launches=int(p.launches[i]), ms=float(p.ms[i]), flops=float(p.flops[i]))
-            for i, st in enumerate(STAGES)}
+    return {st: dict(launches=int(p.launches[i]), ms=float(p.ms[i]), flops=float(p.flops[i]),
+                     ms_union=float(p.ms_union[i])) for i, st in enumerate(STAGES)}
 
 
 def dpp_version() -> str:

@@ -109,14 +109,29 @@ struct DeviceStreams {
   std::recursive_mutex mu;
   bool init = false;
 };
-DeviceStreams g_streams[64];
+// Per device, a few stream pairs (with their events): calls made on different caller streams get
+// different pairs, so independent samplers in flight on two caller streams run concurrently (one
+// step's copy and first block steps under the previous step's chain-bound tail); calls on the
+// same caller stream share a pair and stay in call order.
+constexpr int NPAIRS = 4;
+DeviceStreams g_streams[64][NPAIRS];
+cudaStream_t g_pair_owner[64][NPAIRS];
+int g_pair_next[64];
 std::mutex g_streams_mu;
 
-int get_streams(DeviceStreams** out) {
+int get_streams(DeviceStreams** out, cudaStream_t caller = nullptr) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return DPP_ECUDA;
-  DeviceStreams& d = g_streams[dev];
   std::lock_guard<std::mutex> lk(g_streams_mu);
+  int slot = -1;
+  for (int i = 0; i < NPAIRS && slot < 0; ++i)
+    if (g_streams[dev][i].init && g_pair_owner[dev][i] == caller) slot = i;
+  if (slot < 0) {  // a new caller stream: the next pair, round robin
+    slot = g_pair_next[dev];
+    g_pair_next[dev] = (slot + 1) % NPAIRS;
+    g_pair_owner[dev][slot] = caller;
+  }
+  DeviceStreams& d = g_streams[dev][slot];
   if (!d.init) {
     int lo = 0, hi = 0;
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return DPP_ECUDA;
@@ -333,7 +348,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
   void* state = work + L.state_off;
   if (n == 0) { CK(launch_zero_state(state, loglik, info, batch, caller)); return DPP_OK; }
   DeviceStreams* ds = nullptr;
-  int rc = get_streams(&ds);
+  int rc = get_streams(&ds, caller);
   if (rc) return rc;
   std::lock_guard<std::recursive_mutex> lk(ds->mu);
   const int nb = o.nb;
@@ -670,7 +685,7 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
     if (host && (cw > 0 || gated) && n > 0) {
       // pipelined: the copy of column chunk c (on s3) gates only chunk c of the factorization
       DeviceStreams* ds = nullptr;
-      if ((rc = get_streams(&ds))) return rc;
+      if ((rc = get_streams(&ds, st))) return rc;
       std::lock_guard<std::recursive_mutex> lk(ds->mu);
       CK(cudaEventRecord(ds->ev_copy_start, st));
       CK(cudaStreamWaitEvent(ds->s3, ds->ev_copy_start, 0));
@@ -846,13 +861,28 @@ int dpp_profile_end(dpp_profile_t* out) {
   g_prof.on = false;
   if (!out) return DPP_EINVAL;
   std::memset(out, 0, sizeof(*out));
+  std::vector<std::pair<double, double>> iv[5];  // launch intervals per stage, from the first event
+  const cudaEvent_t ref = g_prof.recs.empty() ? nullptr : g_prof.recs.front().e0;
   for (auto& r : g_prof.recs) {
     if (cudaEventSynchronize(r.e1) != cudaSuccess) return DPP_ECUDA;
-    float ms = 0.f;
+    float ms = 0.f, t0 = 0.f, t1 = 0.f;
     if (cudaEventElapsedTime(&ms, r.e0, r.e1) != cudaSuccess) return DPP_ECUDA;
+    if (cudaEventElapsedTime(&t0, ref, r.e0) != cudaSuccess) return DPP_ECUDA;
+    if (cudaEventElapsedTime(&t1, ref, r.e1) != cudaSuccess) return DPP_ECUDA;
     out->launches[r.stage] += 1;
     out->ms[r.stage] += ms;
     out->flops[r.stage] += r.flops;
+    iv[r.stage].push_back({(double)t0, (double)t1});
+  }
+  for (int st = 0; st < 5; ++st) {  // length of the union of the stage's launch intervals
+    std::sort(iv[st].begin(), iv[st].end());
+    double lo = 0.0, hi = -1.0, u = 0.0;
+    for (auto& p : iv[st]) {
+      if (p.first > hi) { if (hi > lo) u += hi - lo; lo = p.first; hi = p.second; }
+      else if (p.second > hi) hi = p.second;
+    }
+    if (hi > lo) u += hi - lo;
+    out->ms_union[st] = u;
   }
   g_prof.recs.clear();
   g_prof.used = 0;
