@@ -6,7 +6,7 @@ python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 |
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
-CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --streams 1"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 # the masked (trailing / lookahead) update launches: (a)0 (a)1 (b)1 (a)2 (a)3 (b)3 ... -> the 6th is the
 # paired trailing update of step 3 (K = 256)
