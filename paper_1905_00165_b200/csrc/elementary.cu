@@ -70,20 +70,17 @@ __global__ void elem_init_kernel(ElemArgs a) {
 }
 
 constexpr int SEL_T = 1024;
-constexpr int64_t ELEM_NARROW_MAX_K = 128;  // ranks up to this use 256-thread fused CTAs
 
-template <int NT>
 struct SelShared {
-  double wsum[NT / 32];
+  double wsum[SEL_T / 32];
   double S, target;
   long long t, last;
 };
 
-// Draw of pivot j for sample s by one CTA of NT threads (block-wide scan of d over the items,
+// Draw of pivot j for sample s by one CTA of SEL_T threads (block-wide scan of d over the items,
 // each thread a contiguous segment), the pivot bookkeeping, and the pivot's factor row L(t, 0:j)
 // copied next to the state.  Ends with the CTA synchronised.
-template <int NT>
-__device__ __forceinline__ void elem_select(const ElemArgs& a, int64_t s, int64_t j, SelShared<NT>& sh) {
+__device__ __forceinline__ void elem_select(const ElemArgs& a, int64_t s, int64_t j, SelShared& sh) {
   const double* d = a.d + s * a.n;
   uint8_t* ch = a.chosen + s * a.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -93,7 +90,7 @@ __device__ __forceinline__ void elem_select(const ElemArgs& a, int64_t s, int64_
   long long& sh_t = sh.t;
   long long& sh_last = sh.last;
   // contiguous segment of this thread
-  const int64_t per = (a.n + NT - 1) / NT;
+  const int64_t per = (a.n + SEL_T - 1) / SEL_T;
   const int64_t i0 = min((int64_t)a.n, (int64_t)tid * per), i1 = min((int64_t)a.n, i0 + per);
   double seg = 0.0;
   int64_t seg_last = -1;
@@ -113,14 +110,14 @@ __device__ __forceinline__ void elem_select(const ElemArgs& a, int64_t s, int64_
   if (tid == 0) { sh_t = LLONG_MAX; sh_last = -1; }
   __syncthreads();
   if (warp == 0) {
-    double w = lane < NT / 32 ? wsum[lane] : 0.0;
+    double w = wsum[lane];
     double wi = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const double v = __shfl_up_sync(0xffffffffu, wi, o);
       if (lane >= o) wi += v;
     }
-    if (lane < NT / 32) wsum[lane] = wi - w;  // exclusive prefix of the warps
+    wsum[lane] = wi - w;  // exclusive prefix of the warps
     if (lane == 31) {
       sh_S = wi;
       sh_target = uniform_u(a.seed, (uint64_t)j, a.b0 + (uint64_t)s) * wi;
@@ -158,7 +155,7 @@ __device__ __forceinline__ void elem_select(const ElemArgs& a, int64_t s, int64_
   }
   // pivot bookkeeping and the factor row L(t, 0:j)
   double* L = a.L + s * a.strideL;
-  for (int64_t m = tid; m < j; m += NT) a.lt[s * a.k + m] = L[t + m * a.ldL];
+  for (int64_t m = tid; m < j; m += SEL_T) a.lt[s * a.k + m] = L[t + m * a.ldL];
   if (tid == 0) {
     const double dt = d[t];
     ElemState& st = a.st[s];
@@ -177,24 +174,21 @@ __device__ __forceinline__ void elem_select(const ElemArgs& a, int64_t s, int64_
 }
 
 __global__ void __launch_bounds__(SEL_T) elem_select_kernel(ElemArgs a, int64_t j) {
-  __shared__ SelShared<SEL_T> sh;
-  elem_select<SEL_T>(a, blockIdx.x, j, sh);
+  __shared__ SelShared sh;
+  elem_select(a, blockIdx.x, j, sh);
 }
 
 // The whole sampler for one sample per CTA (all k steps in one launch): the draw, then the new
 // factor column, rows strided over the CTA's threads (for batches large enough to fill the GPU with
-// one CTA per sample; removes the 2k launches per call).  NT = 1024, or 256 for small ranks: the
-// per-step work is then a few rows per thread and the draw is latency-bound, so four times as
-// many samples resident per SM pay more than wide CTAs.
-template <int NT>
-__global__ void __launch_bounds__(NT) elem_fused_kernel(ElemArgs a) {
-  __shared__ SelShared<NT> sh;
+// one CTA per sample; removes the 2k launches per call).
+__global__ void __launch_bounds__(SEL_T) elem_fused_kernel(ElemArgs a) {
+  __shared__ SelShared sh;
   extern __shared__ double lt_s[];
   const int64_t s = blockIdx.x;
   double* L = a.L + s * a.strideL;
   const uint8_t* ch = a.chosen + s * a.n;
   double* d = a.d + s * a.n;
-  for (int64_t i = threadIdx.x; i < a.n; i += NT) {
+  for (int64_t i = threadIdx.x; i < a.n; i += SEL_T) {
     d[i] = a.K[i + i * a.ld];
     a.chosen[s * a.n + i] = 0;
   }
@@ -204,13 +198,13 @@ __global__ void __launch_bounds__(NT) elem_fused_kernel(ElemArgs a) {
   }
   __syncthreads();
   for (int64_t j = 0; j < a.k; ++j) {
-    elem_select<NT>(a, s, j, sh);
+    elem_select(a, s, j, sh);
     if (j + 1 == a.k) break;
-    for (int64_t m = threadIdx.x; m < j; m += NT) lt_s[m] = a.lt[s * a.k + m];
+    for (int64_t m = threadIdx.x; m < j; m += SEL_T) lt_s[m] = a.lt[s * a.k + m];
     __syncthreads();
     const int64_t t = a.st[s].t;
     const double Aj = a.st[s].Aj;
-    for (int64_t i = threadIdx.x; i < a.n; i += NT) {
+    for (int64_t i = threadIdx.x; i < a.n; i += SEL_T) {
       if (ch[i]) {
         if (i != t) L[i + j * a.ldL] = 0.0;
         continue;
@@ -326,17 +320,10 @@ int dpp_elementary_herm_d(int64_t batch, int64_t n, int64_t k, const double* K, 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const bool fused = fused_env >= 0 ? fused_env == 1 : batch >= sms;
   if (fused) {
-    // small ranks: 256-thread CTAs (DPP_ELEM_NT=256/1024 forces one)
-    static int nt_env = -2;
-    if (nt_env == -2) {
-      const char* e = getenv("DPP_ELEM_NT");
-      nt_env = e ? atoi(e) : -1;
-    }
-    const bool narrow = nt_env > 0 ? nt_env == 256 : k <= ELEM_NARROW_MAX_K;
-    auto* fn = narrow ? elem_fused_kernel<256> : elem_fused_kernel<SEL_T>;
-    if (smem > 48 * 1024 && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(elem_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return DPP_ECUDA;
-    fn<<<(unsigned)batch, narrow ? 256 : SEL_T, smem, st>>>(a);
+    elem_fused_kernel<<<(unsigned)batch, SEL_T, smem, st>>>(a);
     return cudaGetLastError() == cudaSuccess ? DPP_OK : DPP_ECUDA;
   }
   const dim3 rows((unsigned)((n + 255) / 256), (unsigned)batch);
