@@ -397,13 +397,13 @@ def main():
 
 def _traffic():
     """DRAM bytes per launch of the trailing-update kernel from the committed ncu capture
-    (profiles/r01g_update_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum averaged over
+    (profiles/r01h_update_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum averaged over
     the trailing-update launches of one n=16384 sample); None if absent."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r01g_update_traffic.json")))
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01h_update_traffic.json")))
         return {"bytes_per_launch": int(d["measured_bytes_per_launch"]),
                 "measured_over_algorithmic": d["ratio_measured_over_algorithmic"],
-                "source": "profiles/r01g_update_traffic.json (ncu)"}
+                "source": "profiles/r01h_update_traffic.json (ncu)"}
     except Exception:
         return None
 
