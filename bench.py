@@ -139,7 +139,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-streams", type=int, default=3, help="c4 e2e: streams (and workspaces) the host calls rotate over")
-    ap.add_argument("--streams", type=int, default=2, choices=[1, 2],
+    ap.add_argument("--streams", type=int, default=3, choices=[1, 2, 3, 4],
                     help="c4: caller streams the consecutive steps alternate between")
     ap.add_argument("--prof", choices=["trailing", "all"], default="trailing",
                     help="c4: stages bracketed by events inside the timed region")
@@ -187,7 +187,7 @@ def main():
     torch.cuda.synchronize()
     opts = dpp.make_opts(nb=NB, lookahead=1)
     op = dpp.DPP_OP_HERM_D | dpp.DPP_OP_BATCHED
-    # consecutive steps alternate between two caller streams with two workspaces (--streams 2): the
+    # consecutive steps rotate over three caller streams with three workspaces (--streams 3): the
     # library gives each caller stream its own internal stream pair, so one sample's copy and first
     # block steps run under the previous sample's chain-bound tail
     NS = args.streams
