@@ -138,6 +138,7 @@ def main():
     ap.add_argument("--n", type=int, default=N)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ust-streams", type=int, default=1, help="ust: streams consecutive batches rotate over")
     ap.add_argument("--e2e-streams", type=int, default=3, help="c4 e2e: streams (and workspaces) the host calls rotate over")
     ap.add_argument("--streams", type=int, default=3, choices=[1, 2, 3, 4],
                     help="c4: caller streams the consecutive steps alternate between")
@@ -408,7 +409,7 @@ def _traffic():
         return None
 
 
-def _timed(fn, steps, warmup, world, dist, prof_mask=0):
+def _timed(fn, steps, warmup, world, dist, prof_mask=0, streams=()):
     """Warm-up, then `steps` timed calls between CUDA events; with prof_mask the stages it names
     are bracketed by events inside the timed region (read with dpp.dpp_profile_end())."""
     import torch
@@ -425,8 +426,14 @@ def _timed(fn, steps, warmup, world, dist, prof_mask=0):
     if prof_mask:
         dpp.dpp_profile_begin_stages(prof_mask)
     e0.record()
+    for st_ in streams:  # extra streams the steps run on: they start with the timed region ...
+        st_.wait_event(e0)
     for i in range(steps):
         fn(warmup + i)
+    for st_ in streams:  # ... and it ends when all of them are done
+        ej = torch.cuda.Event()
+        ej.record(st_)
+        torch.cuda.current_stream().wait_event(ej)
     e1.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -476,14 +483,20 @@ def extra_workload(args):
         B = args.batch
         opts = dpp.make_opts(nb=args.nb, lookahead=args.lookahead, batch_chunk=min(B, args.batch_chunk))
         op = dpp.DPP_OP_HERM_D | dpp.DPP_OP_BATCHED
-        work = torch.empty(dpp.dpp_workspace_bytes(op, B, n, opts), dtype=torch.uint8, device="cuda")
-        mask = torch.empty((B, n), dtype=torch.uint8, device="cuda")
-        ll = torch.empty(B, dtype=torch.float64, device="cuda")
+        NSU = args.ust_streams  # consecutive steps rotate over this many streams (batches in flight)
+        works = [torch.empty(dpp.dpp_workspace_bytes(op, B, n, opts), dtype=torch.uint8, device="cuda")
+                 for _ in range(NSU)]
+        masks = [torch.empty((B, n), dtype=torch.uint8, device="cuda") for _ in range(NSU)]
+        lls = [torch.empty(B, dtype=torch.float64, device="cuda") for _ in range(NSU)]
+        ustreams = [torch.cuda.current_stream()] + [torch.cuda.Stream() for _ in range(NSU - 1)]
 
         def step(i):
             b0 = (rank * (args.warmup + args.steps) + i) * B
-            dpp.dpp_sample_herm_d_batched(B, n, Kc, n, 0, SEED, b0, mask, ll, None, opts, work)
-        ms, clocks = _timed(step, args.steps, args.warmup, world, dist)
+            k = i % NSU
+            dpp.dpp_sample_herm_d_batched(B, n, Kc, n, 0, SEED, b0, masks[k], lls[k], None, opts, works[k],
+                                          stream=ustreams[k])
+        ms, clocks = _timed(step, args.steps, args.warmup, world, dist, streams=ustreams[1:])
+        mask = torch.cat(masks)
         ok = bool((mask.sum(dim=1) == 1599).all())
         flops = model_flops(n) * B * args.steps * world
         line.update(value=round(flops / (ms / 1e3) / 1e9, 2), ms_per_step=round(ms / args.steps, 3), scaling="weak",
