@@ -695,14 +695,18 @@ def extra_workload(args):
             Kc = (Kc * dv[None, :]) / dv[:, None]  # storage (l, i) = K(i, l): K' = D^-1 K D
         opts = dpp.make_opts(nb=64, lookahead=1)
         op = (dpp.DPP_OP_HERM_Z if args.workload == "herm_z" else dpp.DPP_OP_LU_Z) | dpp.DPP_OP_BATCHED
-        work = torch.empty(dpp.dpp_workspace_bytes(op, 1, n, opts), dtype=torch.uint8, device="cuda")
-        mask = torch.empty((1, n), dtype=torch.uint8, device="cuda")
-        ll = torch.empty(1, dtype=torch.float64, device="cuda")
+        NSZ = args.streams  # consecutive samples rotate over this many streams (as the default workload)
+        works = [torch.empty(dpp.dpp_workspace_bytes(op, 1, n, opts), dtype=torch.uint8, device="cuda")
+                 for _ in range(NSZ)]
+        masks = [torch.empty((1, n), dtype=torch.uint8, device="cuda") for _ in range(NSZ)]
+        lls = [torch.empty(1, dtype=torch.float64, device="cuda") for _ in range(NSZ)]
+        zstreams = [torch.cuda.current_stream()] + [torch.cuda.Stream() for _ in range(NSZ - 1)]
         fn = dpp.dpp_sample_herm_z_batched if args.workload == "herm_z" else dpp.dpp_sample_lu_z_batched
 
         def step(i):
-            fn(1, n, Kc, n, 0, SEED, rank * 1000 + i, mask, ll, None, opts, work)
-        ms, clocks = _timed(step, args.steps, args.warmup, world, dist)
+            k = i % NSZ
+            fn(1, n, Kc, n, 0, SEED, rank * 1000 + i, masks[k], lls[k], None, opts, works[k], stream=zstreams[k])
+        ms, clocks = _timed(step, args.steps, args.warmup, world, dist, streams=zstreams[1:])
         mult = 4.0 if args.workload == "herm_z" else 8.0  # complex LDL^H 4n^3/3, complex LU 8n^3/3 (R11)
         flops = mult * n ** 3 / 3.0 * args.steps * world
         line.update(value=round(flops / (ms / 1e3) / 1e9, 2), ms_per_step=round(ms / args.steps, 3), scaling="weak",
