@@ -161,7 +161,24 @@ def main():
     ap.add_argument("--rank", type=int, default=500, help="elementary: projection rank k")
     ap.add_argument("--lookahead", type=int, default=1, help="ust: 0 = single stream")
     ap.add_argument("--nb", type=int, default=128, help="ust: block size")
+    ap.add_argument("--no-dist", action="store_true", help="c4: skip the configs[4] block-cyclic sub-record")
+    ap.add_argument("--dist-n", type=int, default=65536, help="c4: n of the block-cyclic sub-record")
+    ap.add_argument("--dist-steps", type=int, default=2, help="c4: timed samples of the block-cyclic sub-record")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torch.distributed.run (the driver may
+        # also launch it that way itself; then WORLD_SIZE is set and this is skipped)
+        import socket
+        sck = socket.socket()
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+        sck.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    if "WORLD_SIZE" in os.environ and args.impl == "ours":
+        assert int(os.environ["WORLD_SIZE"]) == args.gpus, \
+            f"--gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}"
     if args.workload != "c4" and args.impl == "ours":
         return extra_workload(args)
 
@@ -241,7 +258,8 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    kept = int(mask.sum())
+    last = (args.warmup + args.steps - 1) % NS  # the slot of the last timed step
+    kept = int(masks[last].sum())
     total_flops = model_flops(n) * args.steps * world
     value = total_flops / (ms_max / 1e3) / 1e9
     samples_per_s = args.steps * world / (ms_max / 1e3)
@@ -249,12 +267,44 @@ def main():
 
     # roofline of the dominant kernel: the trailing update (b), stage 3, on its own stream
     up = prof["update_trailing"]
-    # with two samples in flight their trailing updates can overlap: the achieved rate is the flops
-    # over the time during which the kernel ran (union of its launch intervals; = the summed launch
-    # time when they never overlap)
+    # with samples in flight their trailing updates can overlap: the rate over the union of the
+    # kernel's launch intervals (= the summed launch time when they never overlap)
     t_b = up.get("ms_union") or up["ms"]
-    achieved_tf = up["flops"] / (t_b / 1e3) / 1e12 if t_b > 0 else 0.0
-    stage_share = {k: round(v["ms"] / max(ms, 1e-9), 4) for k, v in prof.items()}
+    union_tf = up["flops"] / (t_b / 1e3) / 1e12 if t_b > 0 else 0.0
+    # shares of the timed region, each stage's launches counted once where they overlap
+    stage_share = {k: round((v.get("ms_union") or v["ms"]) / max(ms, 1e-9), 4) for k, v in prof.items()}
+
+    # ---- one sample at a time (one caller stream): the latency of a single sample, the paper's
+    #      "sampling costs about one plain factorization" comparison; its
+    #      trailing-update launches are also the isolated probe of the dominant kernel (each
+    #      launch timed alone by events on its stream, no other sample in flight)
+    def step1(i):
+        dpp.dpp_sample_herm_d_batched(1, n, Kc, n, 0, SEED, b_base + i, masks[0], lls[0], infos[0], opts, works[0],
+                                      stream=stream)
+    for i in range(2):
+        step1(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    dpp.dpp_profile_begin_stages(1 << dpp.STAGES.index("update_trailing"))
+    l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0.record(stream)
+    for i in range(args.steps):
+        step1(args.warmup + i)
+    l1.record(stream)
+    torch.cuda.synchronize()
+    prof1 = dpp.dpp_profile_end()["update_trailing"]
+    lat = torch.tensor([l0.elapsed_time(l1) / args.steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(lat, op=dist.ReduceOp.MAX)
+    lat_ms = float(lat.item())
+    probe_tf = prof1["top_flops"] / (prof1["top_ms"] / 1e3) / 1e12 if prof1["top_ms"] > 0 else 0.0
+    one_tf = prof1["flops"] / (prof1["ms"] / 1e3) / 1e12 if prof1["ms"] > 0 else 0.0
+    latency = {"ms_per_sample": round(lat_ms, 3), "tflops": round(model_flops(n) / (lat_ms / 1e3) / 1e12, 3),
+               "pct_fp64_peak": round(100 * model_flops(n) / (lat_ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS, 2),
+               "trailing_update_tflops": round(one_tf, 3),
+               "what": "one caller stream: each sample starts after the previous one ends (no samples in flight)"}
+    achieved_tf = probe_tf
 
     # ---- end-to-end through the host-buffer C-ABI calls (H2D of K + D2H of mask/loglik inside every
     #      step).  Headline: the stream-ordered entry point, consecutive steps on two streams with two
@@ -319,6 +369,8 @@ def main():
                       "(each step's H2D overlaps the factorizations in flight)",
                "sync_api_value": round(total_flops / (t_sync / 1e3) / 1e9, 2),
                "sync_api": "dpp_sample_herm_d_host, one synchronous call per step"}
+        del work_h
+        torch.cuda.empty_cache()
 
     # context comparator (the paper's "DPP sampling ~ plain factorization"):
     # cuSOLVER Cholesky (torch.linalg.cholesky -> potrf) of the same positive definite K, timed alone
@@ -343,7 +395,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cores = min(16, len(os.sched_getaffinity(0)))
+        cores = len(os.sched_getaffinity(0))
 
         def prefix(m):
             return Kc[:m, :m].cpu().numpy().T.copy()
@@ -353,6 +405,15 @@ def main():
                "sample": f"{cores} concurrent oracle samples (one per host core, b = 0..{cores - 1}) of the "
                          f"leading {m}x{m} block of the same n={n} kernel (same flop convention m^3/3), "
                          f"{wall:.1f} s wall"}
+
+    # ---- factor quality at full size (untimed): max|L| and a randomized residual of the factor of the
+    #      last sample (R17: the panel solves use explicit tile inverses; this watches their growth)
+    fcheck = _factor_check(dpp, Kc, n, opts, SEED, b_base + args.warmup + args.steps)
+    del works, Kc
+    torch.cuda.empty_cache()
+    # ---- configs[4]: ONE n = 65536 sample factored 1D block-column-cyclic over all ranks (the
+    #      north_star scaling target), at every N including 1
+    dist_rec = None if args.no_dist else dist_record(args, world, rank, dist)
 
     if rank == 0:
         line = {
@@ -365,28 +426,37 @@ def main():
                        "parallelism": f"dp{world} (independent samples)" if world > 1 else "single GPU",
                        "l2": "inputs (K, 2.1 GB) larger than L2; no flush needed",
                        "api": "dpp_sample_herm_d_batched(batch=1): K copied into the workspace each step",
-                       "streams": f"{NS} caller stream(s), consecutive steps alternate (one sample per step)"},
+                       "streams": f"{NS} caller stream(s), consecutive steps rotate over them: {NS} samples "
+                                  "in flight (one sample per step)"},
             "samples_per_s": round(samples_per_s, 3),
+            "headline": f"throughput with {NS} samples in flight (consecutive steps rotate over {NS} caller "
+                        "streams); latency_one_stream is one sample at a time",
+            "latency_one_stream": latency,
             "pct_fp64_peak": round(100.0 * value / 1e3 / (FP64_PEAK_TFLOPS * world), 2),
             "kept_last_sample": kept,
-            "roofline": {"bound": "tensor", "kernel": "update_kernel<real,herm> (stage 3, trailing region)",
+            "roofline": {"bound": "tensor", "kernel": "update_ws_kernel<real, MASK> (stage 3, trailing update)",
                          "achieved": round(achieved_tf, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": round(achieved_tf / FP64_PEAK_TFLOPS, 4),
                          "traffic": (_traffic() or {}).get("bytes_per_launch"), "traffic_detail": _traffic(),
                          "peak_source": PEAK_SOURCE,
+                         "achieved_definition": "isolated probe: the largest trailing-update launch of a sample "
+                                                "run alone (one caller stream), its algorithmic flops / its CUDA-"
+                                                "event duration on the launching stream (it runs on the SMs the "
+                                                "lookahead chain leaves it)",
+                         "probe_launch_flops": round(prof1["top_flops"]), "probe_launch_ms": round(prof1["top_ms"], 4),
+                         "union_achieved": round(union_tf, 3),
+                         "union_definition": "all trailing-update launches of the timed region (samples in "
+                                             "flight): their flops / the union of their launch intervals",
                          "per_launch_flops": round(up["flops"] / max(up["launches"], 1)),
-                         "avg_launch_ms": round(up["ms"] / max(up["launches"], 1), 4),
-                         "kernel_busy_ms": round(t_b, 3),
-                         "achieved_definition": "algorithmic flops of all trailing-update launches in the timed "
-                                                "region / the union of their launch intervals (CUDA events on the "
-                                                "launching stream); per-launch mean duration alone would count the "
-                                                "overlap of the two samples in flight twice"},
+                         "kernel_busy_ms": round(t_b, 3)},
             "stages": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                            "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3)} for k, v in prof.items()},
             "stage_time_share": stage_share,
             "gpu_launches": int(launches),
             "clocks": clocks,
             "e2e": e2e,
+            "factor_check": fcheck,
+            "dist": dist_rec,
             "cpu_baseline": cpu,
             "comparator_cusolver_potrf": comparator,
             "impl": "ours",
@@ -395,6 +465,92 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _factor_check(dpp, Kc, n, opts, seed, b):
+    """One more sample of the same kernel, in place on a copy (untimed): max|L| and the randomized
+    residual max|(L D L^T - (K - 1_{Y^c})) x| / (max|K| max|x|) over 2 Gaussian vectors."""
+    import torch
+    try:
+        Kf = Kc.clone()
+        work = dpp.workspace("herm_d", n, opts=opts)
+        s = dpp.sample("herm_d", Kf, seed, opts=opts, work=work)
+        torch.cuda.synchronize()
+        del work
+        Lt = torch.tril(Kf.T, -1)                      # natural strict-lower L (storage is column-major)
+        max_l = float(Lt.abs().max())
+        Lt.diagonal().fill_(1.0)
+        D = torch.diagonal(Kf).clone()
+        del Kf
+        g = torch.Generator(device="cuda"); g.manual_seed(1234)
+        x = torch.randn(n, 2, dtype=torch.float64, device="cuda", generator=g)
+        lhs = Lt @ (D[:, None] * (Lt.T @ x))
+        del Lt
+        Kn = torch.tril(Kc.T) + torch.tril(Kc.T, -1).T
+        rhs = Kn @ x - (1.0 - s.mask.double())[:, None] * x
+        res = float((lhs - rhs).abs().max() / (Kn.abs().max() * x.abs().max()))
+        del Kn
+        torch.cuda.empty_cache()
+        return {"max_abs_L": round(max_l, 3), "residual": res, "sample_b": int(b),
+                "what": "randomized max|(L D L^T - (K - 1_{Y^c})) x| / (max|K| max|x|), 2 Gaussian x"}
+    except Exception as e:  # diagnostics only
+        return {"error": str(e)[:200]}
+
+
+def dist_record(args, world, rank, dist):
+    """BASELINE configs[4]: one sample of the n = 65536 real kernel (K = Q diag(lam) Q^T, lam ~
+    U(0,1)) factored 1D block-column-cyclic over all `world` ranks with the NCCL panel broadcast
+    (dpp_sample_herm_d_dist).  Each timed sample starts from the restored local columns (restore
+    outside the timed interval); time = max over ranks of the summed CUDA-event intervals."""
+    import torch
+    import paper_1905_00165_b200 as dpp
+    import workloads as W
+    from paper_1905_00165_b200 import dist as D
+    n, nb = args.dist_n, 128
+    try:
+        t_gen = time.perf_counter()
+        loc0 = W.haar_kernel_bcc_torch(n, nb, world, rank, seed=KSEED, spectrum="uniform")
+        torch.cuda.synchronize()
+        t_gen = time.perf_counter() - t_gen
+        torch.cuda.empty_cache()
+        loc = torch.empty_like(loc0)
+        comm = dpp.dpp_comm_init(D.unique_id() if world == 1 else _shared_uid(dist, rank), world, rank)
+        work = torch.empty(dpp.dpp_dist_workspace_bytes(dpp.DPP_OP_HERM_D, n, world), dtype=torch.uint8,
+                           device="cuda")
+        mask = torch.empty(n, dtype=torch.uint8, device="cuda")
+        ll = torch.empty((), dtype=torch.float64, device="cuda")
+        total = 0.0
+        for i in range(1 + args.dist_steps):  # one warm-up sample
+            loc.copy_(loc0)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dpp.dpp_sample_herm_d_dist(comm, n, loc, n, SEED + i, mask, ll, None, None, work)
+            e1.record()
+            torch.cuda.synchronize()
+            if i > 0:
+                total += e0.elapsed_time(e1)
+        dpp.dpp_comm_destroy(comm)
+        t = torch.tensor([total / args.dist_steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        flops = n ** 3 / 3.0
+        msg = sum(D.message_bytes(n, nb, k) for k in range((n + nb - 1) // nb)) if world > 1 else 0
+        rec = {"workload": f"BASELINE configs[4]: real K n={n}, lam~U(0,1), ONE sample factored 1D block-column-"
+                           f"cyclic over {world} GPU(s), nb={nb}, depth-1 lookahead, NCCL broadcast per block step",
+               "n": n, "ranks": world, "scaling": "strong", "ms_per_sample": round(ms, 2),
+               "value": round(flops / (ms / 1e3) / 1e9, 2), "unit": UNIT,
+               "pct_fp64_peak": round(100 * flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), 2),
+               "samples": args.dist_steps, "kept_last": int(mask.sum()), "loglik_last": float(ll),
+               "bytes_received_per_rank_per_sample": msg, "kernel_generation_s": round(t_gen, 1)}
+        del loc0, loc, work
+        torch.cuda.empty_cache()
+        return rec
+    except Exception as e:  # a sub-record: report, never fail the headline
+        return {"error": str(e)[:300]}
 
 
 def _traffic():
@@ -458,7 +614,8 @@ def _fill_stages(prof, step, args):
     step(args.warmup + args.steps)
     torch.cuda.synchronize()
     one = dpp.dpp_profile_end()
-    return {k: (v if k == "update_trailing" else {kk: vv * args.steps for kk, vv in one[k].items()})
+    return {k: (v if k == "update_trailing" else
+                {kk: (vv if kk.startswith("top_") else vv * args.steps) for kk, vv in one[k].items()})
             for k, v in prof.items()}
 
 
@@ -789,7 +946,7 @@ def reference_arm(args, n):
     """The CPU oracle, as it stands, on this host's cores; same metric/unit/config."""
     import torch
     import workloads as W
-    cores = min(16, len(os.sched_getaffinity(0)))
+    cores = len(os.sched_getaffinity(0))
     if torch.cuda.is_available():
         Kc = W.haar_kernel_torch(n, seed=KSEED, spectrum="beta")
 

@@ -38,8 +38,17 @@
  *    min(u, 1-u) >= 2^-53 for any real pivot value (reading R7).
  *    Asynchronous CUDA faults surface at the caller's synchronisation.
  *  - n = 0 is valid: loglik = 0, info zeroed (first_tie = -1), mask untouched.
- *  - Thread safety: calls are reentrant; calls from several host threads on
- *    the same device are serialised internally while being enqueued.
+ *  - Streams: with lookahead (default) a call runs on an internal pair of
+ *    prioritised streams forked from and joined back into the caller's
+ *    `stream`.  Each device has a pool of 4 pairs; a caller stream keeps the
+ *    pair it was first given, new caller streams take the pairs round robin,
+ *    so calls on up to 4 distinct caller streams run concurrently and calls
+ *    on one caller stream stay in call order.  Beyond 4 caller streams a pair
+ *    is shared (stream-ordered: still correct, less overlap).  Concurrent
+ *    calls on different streams MUST use distinct workspaces and distinct
+ *    mask / loglik / info buffers.
+ *  - Thread safety: calls are reentrant; enqueueing on one stream pair is
+ *    serialised by a per-pair mutex.  Stage profiling is per host thread.
  */
 #ifndef DPP_B200_H_
 #define DPP_B200_H_
@@ -62,9 +71,17 @@ typedef struct { double re, im; } dpp_complex_t;
 typedef struct { float re, im; } dpp_complex64_t;
 typedef struct CUstream_st* dpp_stream_t; /* == cudaStream_t */
 
-/* Options; pass NULL for the defaults. */
+/* Options; pass NULL (or a zero-initialised struct) for the defaults.  The library reads no
+ * environment variables: every knob that changes a result's rounding or the schedule is here. */
+#define DPP_FLAG_GENERIC_UPDATE 1u /* every update / panel GEMM on the cp.async fallback kernel
+                                      (diagnostics: it is otherwise used only for operands that are
+                                      not 16-byte aligned); same results up to rounding */
 typedef struct {
-  int32_t nb;            /* block size: 32, 64 or 128 (0 = default: 128 real, 64 complex) */
+  int32_t nb;            /* block size: 32, 64, 128 or 256 (0 = default: 128 real, 64 complex).
+                            Blocks wider than the kind's tile (128 real, 64 complex) are factored
+                            as nb / tile sub-blocks whose trailing updates are applied as one
+                            K = nb pass (lookahead on) -- the blocked algorithm of Listing 3/4 with
+                            a blocked diagonal-block factorization (Prop. 5) */
   int32_t lookahead;     /* 0 = single stream, 1 = depth-1 lookahead on two streams (default) */
   double tie_tol;        /* default 1e-9 */
   double range_tol;      /* default 1e-8 */
@@ -72,6 +89,12 @@ typedef struct {
                             given set, SPEC log_likelihood_of); batch x n bytes, row b at
                             forced + b*n; decision j is forced[j] != 0 */
   int64_t batch_chunk;   /* batched: samples factored concurrently (0 = whole batch) */
+  int32_t group;         /* G: the trailing updates of G consecutive block steps are applied as
+                            one K = G nb pass (lookahead on).  0 = default (2), 1 = off, <= 8 */
+  uint32_t flags;        /* DPP_FLAG_* */
+  int64_t group_min_rows;/* grouping only while more than this many trailing rows remain;
+                            0 = the library's defaults (6144 real nb = 128, 8192 LU, 0 otherwise
+                            and for batches >= 8), < 0 = at every size */
 } dpp_opts_t;
 
 /* Per-sample diagnostics (DEVICE memory unless the call is _host). */
@@ -240,8 +263,8 @@ int dpp_sample_lu_z_host(int64_t batch, int64_t n, const dpp_complex_t* K, int64
  * must be pinned (page-locked) and stay valid until then; `work` must not be
  * reused by another call before then.  Two calls on two streams with two
  * workspaces overlap the second call's H2D copy with the first call's
- * factorization (the factorization itself runs on the library's per-device
- * stream pair, in call order). */
+ * factorization (each caller stream gets its own internal stream pair; see
+ * "Streams" above). */
 int dpp_sample_herm_d_host_async(int64_t batch, int64_t n, const double* K, int64_t ld,
                                  int64_t strideK, uint64_t seed, uint64_t b0, uint8_t* mask,
                                  double* loglik, dpp_info_t* info, const dpp_opts_t* opts,
@@ -264,30 +287,50 @@ int dpp_philox_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, d
 /* ---- distributed 1D block-column-cyclic factorization (one sample) ---------
  * SURVEY §8(e) mode 2; Listing 3/4 with the block
  * columns dealt round-robin over the ranks.  Hermitian kernels only (real:
- * nb = 128, complex: nb = 64 -- opts->nb must be 0 or that value).
+ * nb = 128, complex: nb = 64 -- opts->nb must be 0 or that value; opts->group
+ * is not used).
  * Rank r of P owns block columns c = r, r+P, r+2P, ... (block width nb), stored
  * contiguously as an n x ncols_local column-major array K_local with leading
  * dimension ld_local >= n (ncols_local = dpp_bcc_local_cols(n, nb, P, r));
  * only rows >= the block's first column are read/written (lower triangle).
  * Per block step the owner factors its diagonal tile and panel and broadcasts
- * [partial loglik + counters | pivots D1 | decisions | panel L21] with NCCL
- * (ncclBroadcast, root = owner); every rank then updates its local trailing
- * columns.  With opts->lookahead != 0 (default) the owner of block k+1 updates
- * that block column first and factors it while every rank's trailing update
- * of step k runs (two prioritised streams per comm).  On return (stream-
- * ordered) every rank holds the full mask (n bytes) and loglik; K_local holds
- * the local columns of the factor.  Every rank must call with the same n,
- * seed and opts.  comm wraps an ncclComm_t created from a 128-byte
- * ncclUniqueId (all ranks pass the same id) on the CURRENT device; it owns two
- * streams and its events.  Errors: DPP_EINVAL (bad sizes/nb/pointers),
+ * [partial loglik + counters | pivots D1 | decisions | panel L21 (live rows
+ * only, pitch round_up(n - j1, 16))] (dpp_dist_message_bytes), root = owner;
+ * every rank then updates its local trailing columns.  With opts->lookahead
+ * != 0 (default) the owner of block k+1 updates that block column first and
+ * factors it while every rank's trailing update of step k runs (two
+ * prioritised streams per rank).  On return (stream-ordered) every rank holds
+ * the full mask (n bytes) and loglik; K_local holds the local columns of the
+ * factor.  Every rank must call with the same n, seed and opts.
+ * Uniforms: global pivot j, sample index b = 0 -- the sample equals the
+ * single-GPU sample of the same K and seed whatever P is.
+ * Errors: DPP_EINVAL (bad sizes/nb/pointers, or a comm of the other kind),
  * DPP_EWORKSPACE, DPP_ECUDA, DPP_ENCCL (a failed collective; the comm must
- * then be destroyed).  Uniforms: global pivot j, sample index b = 0. */
+ * then be destroyed).
+ *
+ * Transports (the same per-step code drives both):
+ *  - dpp_comm_init: one process per GPU; comm wraps an ncclComm_t created from
+ *    a 128-byte ncclUniqueId (all ranks pass the same id) on the CURRENT
+ *    device and owns two streams and their events; broadcast = ncclBroadcast.
+ *  - dpp_comm_init_local: nranks VIRTUAL ranks on the current device, driven
+ *    by ONE call (dpp_sample_herm_{d,z}_dist_local) that takes every rank's
+ *    K_local, mask, workspace (arrays of nranks device pointers) and writes
+ *    loglik[r], info[r] (device arrays of nranks, info nullable) for each rank
+ *    r.  The broadcast is a device-to-device copy per receiver, ordered by
+ *    stream events (no kernel waits on another rank's kernel).  For testing
+ *    the P > 1 schedule on one GPU and for sampling kernels whose columns are
+ *    spread over several allocations; it gives the same results as P
+ *    processes. */
 typedef struct dpp_comm_s* dpp_comm_t;
 int dpp_comm_init(const void* nccl_unique_id, int nranks, int rank, dpp_comm_t* comm);
+int dpp_comm_init_local(int nranks, dpp_comm_t* comm);
 int dpp_comm_destroy(dpp_comm_t comm);
 int64_t dpp_bcc_local_cols(int64_t n, int32_t nb, int nranks, int rank);
-/* op: DPP_OP_HERM_D or DPP_OP_HERM_Z; 0 if unsupported */
+/* op: DPP_OP_HERM_D or DPP_OP_HERM_Z; 0 if unsupported.  Per rank. */
 size_t dpp_dist_workspace_bytes(int op, int64_t n, int nranks, const dpp_opts_t* opts);
+/* Bytes broadcast at block step k (-1 if k is past the last block).  With
+ * nranks = 1 nothing is copied: the header only. */
+int64_t dpp_dist_message_bytes(int op, int64_t n, int nranks, int64_t k);
 int dpp_sample_herm_d_dist(dpp_comm_t comm, int64_t n, double* K_local, int64_t ld_local,
                            uint64_t seed, uint8_t* mask, double* loglik, dpp_info_t* info,
                            const dpp_opts_t* opts, void* work, size_t work_bytes,
@@ -296,6 +339,14 @@ int dpp_sample_herm_z_dist(dpp_comm_t comm, int64_t n, dpp_complex_t* K_local, i
                            uint64_t seed, uint8_t* mask, double* loglik, dpp_info_t* info,
                            const dpp_opts_t* opts, void* work, size_t work_bytes,
                            dpp_stream_t stream);
+int dpp_sample_herm_d_dist_local(dpp_comm_t comm, int64_t n, double* const* K_local,
+                                 int64_t ld_local, uint64_t seed, uint8_t* const* mask,
+                                 double* loglik, dpp_info_t* info, const dpp_opts_t* opts,
+                                 void* const* work, size_t work_bytes, dpp_stream_t stream);
+int dpp_sample_herm_z_dist_local(dpp_comm_t comm, int64_t n, dpp_complex_t* const* K_local,
+                                 int64_t ld_local, uint64_t seed, uint8_t* const* mask,
+                                 double* loglik, dpp_info_t* info, const dpp_opts_t* opts,
+                                 void* const* work, size_t work_bytes, dpp_stream_t stream);
 
 /* ---- stage profiling (diagnostics; used by bench.py for the roofline) ------
  * Between dpp_profile_begin() and dpp_profile_end() every stage launch made by
@@ -312,6 +363,8 @@ typedef struct {
   double flops[5];
   double ms_union[5];  /* length of the union of the launch intervals (launches of one stage that
                           overlap -- calls in flight on several streams -- count once) */
+  double top_flops[5]; /* the stage's launch with the most flops: its flops ... */
+  double top_ms[5];    /* ... and its duration */
 } dpp_profile_t;
 int dpp_profile_begin(void);
 /* The same, recording only the stages whose bit (1 << stage) is set in stage_mask

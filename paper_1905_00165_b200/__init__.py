@@ -32,7 +32,11 @@ if not os.path.exists(LIB_PATH):
 
 class dpp_opts_t(ctypes.Structure):
     _fields_ = [("nb", ctypes.c_int32), ("lookahead", ctypes.c_int32), ("tie_tol", ctypes.c_double),
-                ("range_tol", ctypes.c_double), ("forced", ctypes.c_void_p), ("batch_chunk", ctypes.c_int64)]
+                ("range_tol", ctypes.c_double), ("forced", ctypes.c_void_p), ("batch_chunk", ctypes.c_int64),
+                ("group", ctypes.c_int32), ("flags", ctypes.c_uint32), ("group_min_rows", ctypes.c_int64)]
+
+
+DPP_FLAG_GENERIC_UPDATE = 1
 
 
 class dpp_info_t(ctypes.Structure):
@@ -71,14 +75,19 @@ for _n in ("dpp_lensemble_to_marginal_d", "dpp_lensemble_to_marginal_z"):
 _sig("dpp_elementary_herm_d", ctypes.c_int, [_I64, _I64, _I64, _P, _I64, _U64, _U64, _P, _P, _P, _P, _SZ, _P])
 _sig("dpp_philox_uniforms", ctypes.c_int, [_U64, _U64, _U64, _I64, _P, _P])
 _sig("dpp_comm_init", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)])
+_sig("dpp_comm_init_local", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_P)])
 _sig("dpp_comm_destroy", ctypes.c_int, [_P])
+_sig("dpp_dist_message_bytes", _I64, [ctypes.c_int, _I64, ctypes.c_int, _I64])
+for _n in ("dpp_sample_herm_d_dist_local", "dpp_sample_herm_z_dist_local"):
+    _sig(_n, ctypes.c_int, [_P, _I64, _P, _I64, _U64, _P, _P, _P, _P, _P, _SZ, _P])
 _sig("dpp_bcc_local_cols", _I64, [_I64, ctypes.c_int32, ctypes.c_int, ctypes.c_int])
 _sig("dpp_dist_workspace_bytes", _SZ, [ctypes.c_int, _I64, ctypes.c_int, _P])
 for _n in ("dpp_sample_herm_d_dist", "dpp_sample_herm_z_dist"):
     _sig(_n, ctypes.c_int, [_P, _I64, _P, _I64, _U64, _P, _P, _P, _P, _P, _SZ, _P])
 class dpp_profile_t(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64 * 5), ("ms", ctypes.c_double * 5), ("flops", ctypes.c_double * 5),
-                ("ms_union", ctypes.c_double * 5)]
+                ("ms_union", ctypes.c_double * 5), ("top_flops", ctypes.c_double * 5),
+                ("top_ms", ctypes.c_double * 5)]
 
 
 _sig("dpp_profile_begin", ctypes.c_int, [])
@@ -95,8 +104,9 @@ EXPORTS = ["dpp_workspace_bytes", "dpp_sample_herm_d", "dpp_sample_herm_z", "dpp
            "dpp_sample_herm_d_batched", "dpp_sample_herm_z_batched", "dpp_sample_lu_z_batched",
            "dpp_sample_herm_d_host_async", "dpp_sample_herm_z_host_async", "dpp_sample_lu_z_host_async",
            "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host",
-           "dpp_philox_uniforms", "dpp_comm_init", "dpp_comm_destroy", "dpp_bcc_local_cols",
-           "dpp_dist_workspace_bytes", "dpp_sample_herm_d_dist", "dpp_sample_herm_z_dist", "dpp_profile_begin", "dpp_profile_begin_stages", "dpp_profile_end",
+           "dpp_philox_uniforms", "dpp_comm_init", "dpp_comm_init_local", "dpp_comm_destroy", "dpp_bcc_local_cols",
+           "dpp_dist_workspace_bytes", "dpp_dist_message_bytes", "dpp_sample_herm_d_dist", "dpp_sample_herm_z_dist",
+           "dpp_sample_herm_d_dist_local", "dpp_sample_herm_z_dist_local", "dpp_profile_begin", "dpp_profile_begin_stages", "dpp_profile_end",
            "dpp_strerror", "dpp_version"]
 
 
@@ -125,11 +135,14 @@ def _stream(stream):
     return stream.cuda_stream
 
 
-def make_opts(nb=0, lookahead=1, tie_tol=0.0, range_tol=0.0, forced=None, batch_chunk=0):
+def make_opts(nb=0, lookahead=1, tie_tol=0.0, range_tol=0.0, forced=None, batch_chunk=0, group=0, flags=0,
+              group_min_rows=0):
+    """dpp_opts_t (include/dpp.h); group_min_rows < 0 groups trailing updates at every size."""
     o = dpp_opts_t()
     o.nb, o.lookahead, o.tie_tol, o.range_tol = nb, lookahead, tie_tol, range_tol
     o.forced = _ptr(forced)
     o.batch_chunk = batch_chunk
+    o.group, o.flags, o.group_min_rows = group, flags, group_min_rows
     return o
 
 
@@ -278,6 +291,41 @@ def dpp_comm_init(unique_id: bytes, nranks: int, rank: int):
     return c
 
 
+def dpp_comm_init_local(nranks: int):
+    c = _P()
+    _check(_lib.dpp_comm_init_local(nranks, ctypes.byref(c)))
+    return c
+
+
+def dpp_dist_message_bytes(op, n, nranks, k) -> int:
+    return int(_lib.dpp_dist_message_bytes(op, n, nranks, k))
+
+
+def _ptr_array(ts):
+    arr = (ctypes.c_void_p * len(ts))()
+    for i, t in enumerate(ts):
+        arr[i] = _ptr(t)
+    return arr
+
+
+def _dist_local(name):
+    fn = getattr(_lib, name)
+
+    def call(comm, n, K_locals, ld_local, seed, masks, loglik, info=None, opts=None, works=None, work_bytes=None,
+             stream=None):
+        """K_locals, masks, works: one device tensor per virtual rank; loglik (info): device arrays of
+        nranks doubles (dpp_info_t)."""
+        wb = work_bytes if work_bytes is not None else min(w.numel() for w in works)
+        _check(fn(comm, n, _ptr_array(K_locals), ld_local, seed, _ptr_array(masks), _ptr(loglik), _ptr(info),
+                  _optp(opts), _ptr_array(works), wb, _stream(stream)))
+    call.__name__ = name
+    return call
+
+
+dpp_sample_herm_d_dist_local = _dist_local("dpp_sample_herm_d_dist_local")
+dpp_sample_herm_z_dist_local = _dist_local("dpp_sample_herm_z_dist_local")
+
+
 def dpp_comm_destroy(comm):
     _check(_lib.dpp_comm_destroy(comm))
 
@@ -312,7 +360,8 @@ def dpp_profile_end() -> dict:
     p = dpp_profile_t()
     _check(_lib.dpp_profile_end(ctypes.byref(p)))
     return {st: dict(launches=int(p.launches[i]), ms=float(p.ms[i]), flops=float(p.flops[i]),
-                     ms_union=float(p.ms_union[i])) for i, st in enumerate(STAGES)}
+                     ms_union=float(p.ms_union[i]), top_flops=float(p.top_flops[i]), top_ms=float(p.top_ms[i]))
+            for i, st in enumerate(STAGES)}
 
 
 def dpp_version() -> str:

@@ -26,7 +26,6 @@
 // The Hermitian path reads/writes the lower triangle only.
 #include <cuda_runtime.h>
 
-#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -354,35 +353,15 @@ static cudaError_t launch_diag_nt(const DiagArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// Threads per tile CTA: 256 (8 x 8 register blocks per thread at nb = 128).  DPP_DIAG_NT=512
-// selects a 32 x 16 thread grid for tiles of 64 and more (measured slower at nb = 128: 107 vs
-// 101 us per tile at the time -- the per-pivot chain, not the update FLOPs, bounds this kernel).
-static int diag_nt_override() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DPP_DIAG_NT");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
+// 256 threads per tile CTA (8 x 8 register blocks per thread at nb = 128; a 512-thread grid was
+// slower, 107 vs 101 us per tile at the time: the per-pivot chain, not the update FLOPs, bounds
+// this kernel).
 template <typename T, bool HERM, int NB>
 static cudaError_t launch_diag_t(const DiagArgs& a, cudaStream_t s) {
-  if constexpr (NB >= 64) {
-    const int o = diag_nt_override();
-    const int nt = (o == 256 || o == 512) ? o : 256;
-    if (nt == 512) return launch_diag_nt<T, HERM, NB, 512>(a, s);
-  }
   return launch_diag_nt<T, HERM, NB, 256>(a, s);
 }
 
-cudaError_t launch_diag_herm_blocked(Kind kind, int nb, const DiagArgs& a, cudaStream_t s);
-
 cudaError_t launch_diag(Kind kind, int nb, const DiagArgs& a, cudaStream_t s) {
-  if (kind == HERM_D || kind == HERM_Z) {
-    const cudaError_t e = launch_diag_herm_blocked(kind, nb, a, s);
-    if (e != cudaErrorNotSupported) return e;
-  }
   switch (kind) {
     case HERM_D:
       if (nb <= 32) return launch_diag_t<double, true, 32>(a, s);

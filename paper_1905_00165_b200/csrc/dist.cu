@@ -1,16 +1,18 @@
-// dist.cu -- 1D block-column-cyclic distributed sampler over NCCL (mode 2).
+// dist.cu -- 1D block-column-cyclic distributed sampler (mode 2).
 //
 // One sample of DPP(K) for a Hermitian K (real fp64 or complex128) too large (or too slow) for one
 // GPU.  Rank r of P owns block columns c = r, r+P, ... (width nb: 128 real, 64 complex) of the
 // lower triangle, stored contiguously.  Block step k of Listing 3/4:
 //   owner(k) = k mod P:  stage 1 diag tile (decisions + D1 + tile operator), stage 2 panel GEMM
 //                        (L21 = A21 L11^{-H} D1^{-1}, in place), pack [state | D1 | mask | L21];
-//   all ranks:           ncclBroadcast(message, root = owner(k))   -- the one exchange per step;
+//   all ranks:           broadcast the message from owner(k)   -- the one exchange per step;
 //   receivers:           unpack state + decisions;
 //   all ranks:           stage 3 on their local trailing block columns (C -= L21 D1 L21^H) with the
 //                        DMMA update kernel in block-cyclic addressing mode.
 // Because the decisions, pivots and the running log-likelihood ride in the message, every rank
 // ends with the full mask and the same pivot-ordered loglik; no further collective is needed.
+// The message carries only the live rows: L21 of step k is (n - j1) x jb at pitch
+// round_up(n - j1, 16), so a receiver gets ~4 n^2 bytes (real) over the whole sample.
 //
 // Depth-1 lookahead (the distributed form of the paper's dependency scheduling):
 // while every rank runs the trailing update of step k on the low-priority stream S2 (on all but a
@@ -18,25 +20,28 @@
 // panel, then factors tile k+1 and its panel and packs message k+1, and every rank's S1 runs the
 // broadcast of message k+1.  Messages are double-buffered: message k+1 is written only after the
 // trailing update of step k-1 (the last reader of that buffer) has finished.  The broadcasts are
-// issued in block order on S1 of every rank, so all ranks post the same NCCL sequence.
+// issued in block order on S1 of every rank, so all ranks post the same sequence.
+//
+// Two transports drive the SAME per-step code (run_dist below):
+//  * NCCL (dpp_comm_init): one process per GPU, ncclBroadcast(root = owner) on S1;
+//  * in-process (dpp_comm_init_local): P virtual ranks on the calling thread's device, each with its
+//    own streams, workspace and K_local; the broadcast is one device-to-device cudaMemcpyAsync per
+//    receiver on the receiver's S1 after the owner's "packed" event, and an owner waits for every
+//    receiver's copy before it reuses that message buffer.  The host issues each block step's
+//    phases for all virtual ranks in order (pre-exchange, exchange, trailing update), so every
+//    stream wait refers to work already enqueued: no kernel ever waits for another rank's kernel,
+//    only stream-ordered events (PAPER.md:645-653's dependencies, on one GPU's streams).
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
 
 using namespace dpp;
-
-struct dpp_comm_s {
-  ncclComm_t nccl;
-  int nranks, rank, device, max_ctas;
-  cudaStream_t s1, s2;
-  cudaEvent_t ev_start, ev_msg, ev_rest, ev_done1, ev_done2;
-};
 
 namespace {
 
@@ -44,7 +49,42 @@ constexpr size_t ALIGN = 256;
 inline size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-// message = [SampleState 64 B][D1: nb doubles][mask: nb bytes -> 256-aligned][L21: ldw x nb elems]
+struct RankStreams {
+  cudaStream_t s1 = nullptr, s2 = nullptr;
+  cudaEvent_t ev_start, ev_msg, ev_rest, ev_done1, ev_done2, ev_pack, ev_recv;
+};
+
+int make_rank_streams(RankStreams* rs) {
+  int lo = 0, hi = 0;
+  if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return DPP_ECUDA;
+  if (cudaStreamCreateWithPriority(&rs->s1, cudaStreamNonBlocking, hi) != cudaSuccess) return DPP_ECUDA;
+  if (cudaStreamCreateWithPriority(&rs->s2, cudaStreamNonBlocking, lo) != cudaSuccess) return DPP_ECUDA;
+  for (cudaEvent_t* ev : {&rs->ev_start, &rs->ev_msg, &rs->ev_rest, &rs->ev_done1, &rs->ev_done2, &rs->ev_pack,
+                          &rs->ev_recv})
+    if (cudaEventCreateWithFlags(ev, cudaEventDisableTiming) != cudaSuccess) return DPP_ECUDA;
+  return DPP_OK;
+}
+
+void destroy_rank_streams(RankStreams* rs) {
+  if (rs->s1) cudaStreamDestroy(rs->s1);
+  if (rs->s2) cudaStreamDestroy(rs->s2);
+  for (cudaEvent_t ev : {rs->ev_start, rs->ev_msg, rs->ev_rest, rs->ev_done1, rs->ev_done2, rs->ev_pack, rs->ev_recv})
+    if (ev) cudaEventDestroy(ev);
+}
+
+}  // namespace
+
+struct dpp_comm_s {
+  ncclComm_t nccl = nullptr;  // null: in-process virtual ranks
+  int nranks = 1, rank = 0, device = 0, max_ctas = 8;
+  bool local = false;
+  std::vector<RankStreams> rs;  // one (NCCL) or nranks (local)
+};
+
+namespace {
+
+// message = [SampleState 64 B][D1: nb doubles][mask: nb bytes -> 256-aligned][L21: m2 x jb at pitch
+// round_up(m2, 16)]
 struct MsgLayout {
   size_t d_off, mask_off, w_off, header_bytes;
 };
@@ -56,16 +96,16 @@ MsgLayout msg_layout(int nb) {
   m.header_bytes = m.w_off;
   return m;
 }
+inline int64_t msg_pitch(int64_t m2) { return std::max<int64_t>(round_up(m2, 16), 16); }
 
 // work = [state][panel operator Bm: nb x nb][D1: nb][message buffer 0][message buffer 1]
 //        [W21 = L21 D1 of message 0][of message 1] (the pre-scaled A operand of the update)
 struct DistWs {
   size_t state_off, bm_off, d_off, msg_off[2], w_off[2], total;
-  int64_t ldw;
 };
 DistWs dist_ws(int64_t n, int nb, size_t es) {
   DistWs w;
-  w.ldw = std::max<int64_t>(round_up(n, 16), 16);
+  const int64_t ldw = msg_pitch(n);  // the largest pitch (step 0 has m2 < n)
   MsgLayout m = msg_layout(nb);
   size_t off = 0;
   w.state_off = off; off = align_up(off + sizeof(SampleState));
@@ -73,11 +113,11 @@ DistWs dist_ws(int64_t n, int nb, size_t es) {
   w.d_off = off; off = align_up(off + (size_t)nb * 8);
   for (int b = 0; b < 2; ++b) {
     w.msg_off[b] = off;
-    off = align_up(off + m.header_bytes + (size_t)w.ldw * nb * es);
+    off = align_up(off + m.header_bytes + (size_t)ldw * nb * es);
   }
   for (int b = 0; b < 2; ++b) {
     w.w_off[b] = off;
-    off = align_up(off + (size_t)w.ldw * nb * es);
+    off = align_up(off + (size_t)ldw * nb * es);
   }
   w.total = off;
   return w;
@@ -142,163 +182,287 @@ int reserve_sms(int64_t m2, int nb, int sms, int P) {
   return best;
 }
 
-int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* K_local, int64_t ld_local, uint64_t seed, uint8_t* mask,
-             double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work, size_t work_bytes,
-             cudaStream_t st) {
-  if (!comm || n < 0 || !loglik || (n > 0 && (!mask || !K_local)) || ld_local < std::max<int64_t>(n, 1))
-    return DPP_EINVAL;
+// One rank's view of a distributed call.
+struct RankCtx {
+  int r;
+  char* K;           // K_local
+  uint8_t* mask;     // n bytes (every rank ends with the full mask)
+  double* loglik;
+  dpp_info_t* info;
+  char* w;           // workspace
+  RankStreams* rs;
+  cudaStream_t s1, s2;
+  int64_t nloc;      // local blocks
+};
+
+int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* const* K_local, int64_t ld_local, uint64_t seed,
+             uint8_t* const* mask, double* const* loglik, dpp_info_t* const* info, const dpp_opts_t* opts,
+             void* const* work, size_t work_bytes, cudaStream_t st) {
+  if (!comm || n < 0 || ld_local < std::max<int64_t>(n, 1)) return DPP_EINVAL;
+  const int P = comm->nranks;
+  const int nctx = comm->local ? P : 1;
+  for (int i = 0; i < nctx; ++i)
+    if (!loglik[i] || (n > 0 && (!mask[i] || !K_local[i]))) return DPP_EINVAL;
   const int nb = dist_nb(kind, opts);
   if (nb < 0) return DPP_EINVAL;
   const size_t es = kind == HERM_D ? 8 : 16;
-  if (kind != HERM_D && reinterpret_cast<uintptr_t>(K_local) % 16) return DPP_EINVAL;
+  for (int i = 0; i < nctx; ++i)
+    if (kind != HERM_D && reinterpret_cast<uintptr_t>(K_local[i]) % 16) return DPP_EINVAL;
   const double tie_tol = (opts && opts->tie_tol > 0) ? opts->tie_tol : 1e-9;
   const double range_tol = (opts && opts->range_tol > 0) ? opts->range_tol : 1e-8;
   const uint8_t* forced = opts ? opts->forced : nullptr;
   const bool la = !opts || opts->lookahead != 0;
   const DistWs W = dist_ws(n, nb, es);
-  if (!work || work_bytes < W.total || reinterpret_cast<uintptr_t>(work) % ALIGN) return DPP_EWORKSPACE;
-  if (n == 0) { CK(launch_zero_state(nullptr, loglik, info, 1, st)); return DPP_OK; }
-  const int P = comm->nranks, r = comm->rank;
-  char* w = reinterpret_cast<char*>(work);
-  SampleState* state = reinterpret_cast<SampleState*>(w + W.state_off);
-  void* Bm = w + W.bm_off;
-  double* dvec = reinterpret_cast<double*>(w + W.d_off);
+  for (int i = 0; i < nctx; ++i)
+    if (!work[i] || work_bytes < W.total || reinterpret_cast<uintptr_t>(work[i]) % ALIGN) return DPP_EWORKSPACE;
+  if (n == 0) {
+    for (int i = 0; i < nctx; ++i) CK(launch_zero_state(nullptr, loglik[i], info[i], 1, st));
+    return DPP_OK;
+  }
   const MsgLayout M = msg_layout(nb);
   const int64_t nblk = (n + nb - 1) / nb;
-  const int64_t nloc = (nblk - r + P - 1) / P;  // local blocks on r
-  char* Kb = reinterpret_cast<char*>(K_local);
-  const bool vec = kind != HERM_D || ((ld_local % 2 == 0) && (reinterpret_cast<uintptr_t>(K_local) % 16 == 0));
   const int sms = device_sms();
-  cudaStream_t s1 = la ? comm->s1 : st, s2 = la ? comm->s2 : st;
-  if (la) {
-    CK(cudaEventRecord(comm->ev_start, st));
-    CK(cudaStreamWaitEvent(s1, comm->ev_start, 0));
-    CK(cudaStreamWaitEvent(s2, comm->ev_start, 0));
+  std::vector<RankCtx> R(nctx);
+  for (int i = 0; i < nctx; ++i) {
+    RankCtx& c = R[i];
+    c.r = comm->local ? i : comm->rank;
+    c.K = reinterpret_cast<char*>(K_local[i]);
+    c.mask = mask[i]; c.loglik = loglik[i]; c.info = info[i];
+    c.w = reinterpret_cast<char*>(work[i]);
+    c.rs = &comm->rs[i];
+    c.s1 = la ? c.rs->s1 : st;
+    c.s2 = la ? c.rs->s2 : st;
+    c.nloc = (nblk - c.r + P - 1) / P;
+    if (la) {
+      CK(cudaEventRecord(c.rs->ev_start, st));
+      CK(cudaStreamWaitEvent(c.s1, c.rs->ev_start, 0));
+      CK(cudaStreamWaitEvent(c.s2, c.rs->ev_start, 0));
+    }
   }
+  const bool vec = kind != HERM_D || ((ld_local % 2 == 0) && [&] {
+    for (int i = 0; i < nctx; ++i)
+      if (reinterpret_cast<uintptr_t>(K_local[i]) % 16) return false;
+    return true;
+  }());
+  // with one rank (NCCL transport) the panel is read straight from K_local: no message copy
+  const bool self_only = P == 1;
 
   auto jb_of = [&](int64_t k) { return (int)std::min<int64_t>(nb, n - k * nb); };
-  auto msg_of = [&](int64_t k) { return w + W.msg_off[k & 1]; };
+  auto m2_of = [&](int64_t k) { return n - (k * nb + jb_of(k)); };
+  auto msg_of = [&](const RankCtx& c, int64_t k) { return c.w + W.msg_off[k & 1]; };
+  auto owner_ctx = [&](int64_t k) -> RankCtx* {
+    const int o = (int)(k % P);
+    for (auto& c : R)
+      if (c.r == o) return &c;
+    return nullptr;
+  };
+  // the L21 operand of step k on rank c: (pointer, leading dimension)
+  auto l21_of = [&](const RankCtx& c, int64_t k) -> std::pair<const char*, int64_t> {
+    if (self_only) return {c.K + (size_t)(k * nb + jb_of(k) + (k / P) * nb * ld_local) * es, ld_local};
+    return {msg_of(c, k) + M.w_off, msg_pitch(m2_of(k))};
+  };
   // owner(k): stage 1 + stage 2 of block k, packed into message k (stream s)
-  auto factor_block = [&](int64_t k, cudaStream_t s) -> int {
+  auto factor_block = [&](RankCtx& c, int64_t k, cudaStream_t s) -> int {
     const int64_t j0 = k * nb;
     const int jb = jb_of(k);
     const int64_t j1 = j0 + jb, m2 = n - j1;
     const int64_t tcol = (k / P) * nb;  // storage column of block k on its owner
-    char* msg = msg_of(k);
+    char* msg = msg_of(c, k);
+    SampleState* state = reinterpret_cast<SampleState*>(c.w + W.state_off);
     DiagArgs d{};
-    d.A = K_local; d.ld = ld_local; d.strideA = 0; d.n = n; d.j0 = j0; d.tcol = tcol; d.jb = jb;
-    d.seed = seed; d.b0 = 0; d.mask = mask; d.forced = forced; d.state = state; d.loglik = nullptr;
+    d.A = c.K; d.ld = ld_local; d.strideA = 0; d.n = n; d.j0 = j0; d.tcol = tcol; d.jb = jb;
+    d.seed = seed; d.b0 = 0; d.mask = c.mask; d.forced = forced; d.state = state; d.loglik = nullptr;
     d.info = nullptr; d.tie_tol = tie_tol; d.range_tol = range_tol; d.batch = 1;
-    d.need_ops = m2 > 0; d.Bm = Bm; d.dvec = dvec; d.ldm = nb; d.strideM = 0;
+    d.need_ops = m2 > 0; d.Bm = c.w + W.bm_off; d.dvec = reinterpret_cast<double*>(c.w + W.d_off); d.ldm = nb;
+    d.strideM = 0;
     CK(launch_diag(kind, nb, d, s));
     if (m2 > 0) {
-      // stage 2 in place: L21 = A21 L11^-H D1^-1, then into the message
+      // stage 2 in place: L21 = A21 L11^-H D1^-1, then into the message (live rows only)
       UpdateArgs p{};
-      p.Aop = Kb + (size_t)(j1 + tcol * ld_local) * es; p.lda = ld_local;
-      p.Bop = Bm; p.ldb = nb;
-      p.C = Kb + (size_t)(j1 + tcol * ld_local) * es; p.ldc = ld_local;
+      p.Aop = c.K + (size_t)(j1 + tcol * ld_local) * es; p.lda = ld_local;
+      p.Bop = c.w + W.bm_off; p.ldb = nb;
+      p.C = c.K + (size_t)(j1 + tcol * ld_local) * es; p.ldc = ld_local;
       p.a_rows = (int)m2; p.b_rows = jb; p.K = jb; p.rows = (int)m2; p.cols = jb; p.batch = 1; p.vec = vec ? 1 : 0;
       CK(launch_update(kind, p, s));
-      CK(cudaMemcpy2DAsync(msg + M.w_off, (size_t)W.ldw * es, Kb + (size_t)(j1 + tcol * ld_local) * es,
-                           (size_t)ld_local * es, (size_t)m2 * es, (size_t)jb, cudaMemcpyDeviceToDevice, s));
+      if (!self_only)
+        CK(cudaMemcpy2DAsync(msg + M.w_off, (size_t)msg_pitch(m2) * es, c.K + (size_t)(j1 + tcol * ld_local) * es,
+                             (size_t)ld_local * es, (size_t)m2 * es, (size_t)jb, cudaMemcpyDeviceToDevice, s));
     }
-    const double* T11 = reinterpret_cast<const double*>(Kb + (size_t)(j0 + tcol * ld_local) * es);
-    pack_header_kernel<<<1, 128, 0, s>>>(state, T11, (ld_local + 1) * (int64_t)(es / 8), jb, mask + j0, msg, M);
+    const double* T11 = reinterpret_cast<const double*>(c.K + (size_t)(j0 + tcol * ld_local) * es);
+    pack_header_kernel<<<1, 128, 0, s>>>(state, T11, (ld_local + 1) * (int64_t)(es / 8), jb, c.mask + j0, msg, M);
     CK(cudaGetLastError());
     return DPP_OK;
   };
-  // every rank: broadcast message k from its owner; receivers take the state and decisions
-  auto exchange = [&](int64_t k, cudaStream_t s) -> int {
-    const int owner = (int)(k % P);
+  auto msg_bytes = [&](int64_t k) {
+    const int64_t m2 = m2_of(k);
+    return M.header_bytes + (m2 > 0 && !self_only ? (size_t)msg_pitch(m2) * (size_t)jb_of(k) * es : 0);
+  };
+  // receivers of step k: unpack state + decisions; every rank: W21 = L21 D1 (the update's A
+  // operand; the DMMA loop then needs no scaling)
+  auto after_exchange = [&](RankCtx& c, int64_t k, cudaStream_t s) -> int {
     const int jb = jb_of(k);
-    const int64_t m2 = n - (k * nb + jb);
-    char* msg = msg_of(k);
-    const size_t bytes = M.header_bytes + (m2 > 0 ? (size_t)W.ldw * (size_t)jb * es : 0);
-    if (P > 1) NK(ncclBroadcast(msg, msg, bytes, ncclChar, owner, comm->nccl, s));
-    if (r != owner) {
-      unpack_header_kernel<<<1, 128, 0, s>>>(msg, M, jb, state, mask + k * nb);
+    const int64_t m2 = m2_of(k);
+    char* msg = msg_of(c, k);
+    if (c.r != (int)(k % P)) {
+      unpack_header_kernel<<<1, 128, 0, s>>>(msg, M, jb, reinterpret_cast<SampleState*>(c.w + W.state_off),
+                                             c.mask + k * nb);
       CK(cudaGetLastError());
     }
-    // every rank: W21 = L21 D1 (the update's A operand; the DMMA loop then needs no scaling)
-    if (m2 > 0)
-      CK(launch_scale_cols(kind, msg + M.w_off, W.ldw, 0, w + W.w_off[k & 1], W.ldw, 0,
+    if (m2 > 0) {
+      auto l = l21_of(c, k);
+      CK(launch_scale_cols(kind, l.first, l.second, 0, c.w + W.w_off[k & 1], msg_pitch(m2), 0,
                            reinterpret_cast<const double*>(msg + M.d_off), 0, (int)m2, jb, 1, s));
+    }
+    return DPP_OK;
+  };
+  // the broadcast of message k from owner(k), on every rank's S1 (phase run for all contexts)
+  auto exchange = [&](int64_t k, bool lookahead_phase) -> int {
+    const int owner = (int)(k % P);
+    if (!comm->local) {
+      RankCtx& c = R[0];
+      cudaStream_t s = lookahead_phase ? c.s1 : st;
+      char* msg = msg_of(c, k);
+      if (P > 1) NK(ncclBroadcast(msg, msg, msg_bytes(k), ncclChar, owner, comm->nccl, s));
+      return after_exchange(c, k, s);
+    }
+    RankCtx* oc = owner_ctx(k);
+    CK(cudaEventRecord(oc->rs->ev_pack, oc->s1));
+    for (auto& c : R) {
+      if (c.r == owner) continue;
+      CK(cudaStreamWaitEvent(c.s1, oc->rs->ev_pack, 0));
+      CK(cudaMemcpyAsync(msg_of(c, k), msg_of(*oc, k), msg_bytes(k), cudaMemcpyDeviceToDevice, c.s1));
+      CK(cudaEventRecord(c.rs->ev_recv, c.s1));
+    }
+    for (auto& c : R)
+      if (int rc = after_exchange(c, k, c.s1)) return rc;
+    return DPP_OK;
+  };
+  // in-process transport: before an owner rewrites a message buffer, every receiver's copy out of
+  // it has completed (each rank's last ev_recv is at or after that copy)
+  auto wait_receivers = [&](RankCtx& c) -> int {
+    if (!comm->local) return DPP_OK;
+    for (auto& o : R)
+      if (o.r != c.r) CK(cudaStreamWaitEvent(c.s1, o.rs->ev_recv, 0));
     return DPP_OK;
   };
   // stage 3 of step k on local blocks q >= q_lo, up to `count` blocks (count < 0: all)
-  auto update = [&](int64_t k, int64_t q_lo, int64_t count, int grid_limit, cudaStream_t s) -> int {
+  auto update = [&](RankCtx& c, int64_t k, int64_t q_lo, int64_t count, int grid_limit, cudaStream_t s) -> int {
     const int jb = jb_of(k);
     const int64_t j1 = k * nb + jb, m2 = n - j1;
-    const int64_t q_hi = count < 0 ? nloc : std::min<int64_t>(nloc, q_lo + count);
+    const int64_t q_hi = count < 0 ? c.nloc : std::min<int64_t>(c.nloc, q_lo + count);
     if (m2 <= 0 || q_lo >= q_hi) return DPP_OK;
-    char* msg = msg_of(k);
+    auto l = l21_of(c, k);
     UpdateArgs u{};
-    u.Aop = w + W.w_off[k & 1]; u.lda = W.ldw;   // W21 = L21 D1
-    u.Bop = msg + M.w_off; u.ldb = W.ldw; u.mask = 1;  // L21 (conjugated on load for complex)
+    u.Aop = c.w + W.w_off[k & 1]; u.lda = msg_pitch(m2);  // W21 = L21 D1
+    u.Bop = l.first; u.ldb = l.second; u.mask = 1;         // L21 (conjugated on load for complex)
     u.conj = kind == HERM_Z;
-    u.C = Kb + (size_t)j1 * es;  // local column 0, A22 row 0
+    u.C = c.K + (size_t)j1 * es;  // local column 0, A22 row 0
     u.ldc = ld_local;
     u.a_rows = (int)m2; u.b_rows = (int)m2; u.K = jb; u.batch = 1; u.vec = vec ? 1 : 0;
     u.row0 = 0; u.rows = (int)m2; u.col0 = 0; u.cols = (int)m2; u.tri = 0;
-    u.bcc_P = P; u.bcc_r = r; u.bcc_nb = nb; u.bcc_q0 = (int)q_lo; u.bcc_j1 = j1;
+    u.bcc_P = P; u.bcc_r = c.r; u.bcc_nb = nb; u.bcc_q0 = (int)q_lo; u.bcc_j1 = j1;
     u.tiles_n = (int)(q_hi - q_lo);
     u.grid_limit = grid_limit;
     CK(launch_update(kind, u, s));
     return DPP_OK;
   };
   int rc;
-  // first local block strictly after block k on this rank
-  auto first_after = [&](int64_t k) { return (k + 1 - r + P - 1) / P; };
+  // first local block strictly after block k on rank r
+  auto first_after = [&](const RankCtx& c, int64_t k) { return (k + 1 - c.r + P - 1) / P; };
 
   if (!la) {
     for (int64_t k = 0; k < nblk; ++k) {
-      if (r == (int)(k % P) && (rc = factor_block(k, st))) return rc;
-      if ((rc = exchange(k, st))) return rc;
-      if ((rc = update(k, first_after(k), -1, 0, st))) return rc;
+      if (RankCtx* oc = owner_ctx(k)) {
+        if ((rc = wait_receivers(*oc))) return rc;
+        if ((rc = factor_block(*oc, k, st))) return rc;
+      }
+      if ((rc = exchange(k, false))) return rc;
+      for (auto& c : R)
+        if ((rc = update(c, k, first_after(c, k), -1, 0, st))) return rc;
     }
   } else {
-    if (r == 0 && (rc = factor_block(0, s1))) return rc;
-    if ((rc = exchange(0, s1))) return rc;
-    CK(cudaEventRecord(comm->ev_msg, s1));
+    if (RankCtx* oc = owner_ctx(0))
+      if ((rc = factor_block(*oc, 0, oc->s1))) return rc;
+    if ((rc = exchange(0, true))) return rc;
+    for (auto& c : R) CK(cudaEventRecord(c.rs->ev_msg, c.s1));
     for (int64_t k = 0; k < nblk; ++k) {
-      const int64_t m2 = n - (k * nb + jb_of(k));
+      const int64_t m2 = m2_of(k);
       if (m2 <= 0) break;
-      const int64_t kn = k + 1;                 // the lookahead block
-      const bool own_next = r == (int)(kn % P);
-      // S1: message buffer kn&1 was last read by the trailing update of step k-1
-      if (k > 0) CK(cudaStreamWaitEvent(s1, comm->ev_rest, 0));
-      if (own_next) {
-        if ((rc = update(k, kn / P, 1, 0, s1))) return rc;  // block column kn with step k's panel
-        if ((rc = factor_block(kn, s1))) return rc;
-      }
-      if ((rc = exchange(kn, s1))) return rc;
-      // S2: the rest of step k's trailing update (message k is ready: ev_msg recorded last step)
-      CK(cudaStreamWaitEvent(s2, comm->ev_msg, 0));
-      {
-        const int64_t q_lo = own_next ? kn / P + 1 : first_after(k);
-        int reserve = 0;
-        if (own_next) {
-          reserve = reserve_sms(m2, nb, sms, P);
-          if (P > 1) reserve = std::min(sms / 2, reserve + comm->max_ctas);
-        } else if (P > 1) {
-          reserve = comm->max_ctas;  // the broadcast's CTAs
+      const int64_t kn = k + 1;  // the lookahead block
+      // phase 1 (every rank's S1): message buffer kn&1 was last read by the trailing update of
+      // step k-1; the owner of kn updates block column kn with step k's panel and factors it
+      for (auto& c : R) {
+        if (k > 0) CK(cudaStreamWaitEvent(c.s1, c.rs->ev_rest, 0));
+        if (c.r == (int)(kn % P)) {
+          if ((rc = update(c, k, kn / P, 1, 0, c.s1))) return rc;  // block column kn with step k's panel
+          if ((rc = wait_receivers(c))) return rc;
+          if ((rc = factor_block(c, kn, c.s1))) return rc;
         }
-        if ((rc = update(k, q_lo, -1, vec ? sms - reserve : 0, s2))) return rc;
       }
-      CK(cudaEventRecord(comm->ev_rest, s2));
-      CK(cudaEventRecord(comm->ev_msg, s1));  // message kn (exchange issued above)
+      // phase 2: the exchange of message kn
+      if ((rc = exchange(kn, true))) return rc;
+      // phase 3 (S2): the rest of step k's trailing update (message k: ev_msg of the last step)
+      for (auto& c : R) {
+        const bool own_next = c.r == (int)(kn % P);
+        CK(cudaStreamWaitEvent(c.s2, c.rs->ev_msg, 0));
+        const int64_t q_lo = own_next ? kn / P + 1 : first_after(c, k);
+        int reserve = 0;
+        if (!comm->local) {
+          if (own_next) {
+            reserve = reserve_sms(m2, nb, sms, P);
+            if (P > 1) reserve = std::min(sms / 2, reserve + comm->max_ctas);
+          } else if (P > 1) {
+            reserve = comm->max_ctas;  // the broadcast's CTAs
+          }
+        } else {
+          // P virtual ranks share one GPU: each trailing update takes its share of the SMs
+          reserve = sms - std::max(8, (sms - reserve_sms(m2, nb, sms, P)) / P);
+        }
+        if ((rc = update(c, k, q_lo, -1, vec ? sms - reserve : 0, c.s2))) return rc;
+        CK(cudaEventRecord(c.rs->ev_rest, c.s2));
+        CK(cudaEventRecord(c.rs->ev_msg, c.s1));  // message kn (exchange issued above)
+      }
     }
   }
   // the final state: written by the diag kernel on the last block's owner, unpacked elsewhere
-  finalize_kernel<<<1, 32, 0, s1>>>(state, loglik, info);
-  CK(cudaGetLastError());
-  if (la) {
-    CK(cudaEventRecord(comm->ev_done1, s1));
-    CK(cudaEventRecord(comm->ev_done2, s2));
-    CK(cudaStreamWaitEvent(st, comm->ev_done1, 0));
-    CK(cudaStreamWaitEvent(st, comm->ev_done2, 0));
+  for (auto& c : R) {
+    cudaStream_t s = la ? c.s1 : st;
+    finalize_kernel<<<1, 32, 0, s>>>(reinterpret_cast<SampleState*>(c.w + W.state_off), c.loglik, c.info);
+    CK(cudaGetLastError());
+    if (la) {
+      CK(cudaEventRecord(c.rs->ev_done1, c.s1));
+      CK(cudaEventRecord(c.rs->ev_done2, c.s2));
+      CK(cudaStreamWaitEvent(st, c.rs->ev_done1, 0));
+      CK(cudaStreamWaitEvent(st, c.rs->ev_done2, 0));
+    }
   }
   return DPP_OK;
+}
+
+int run_dist_one(Kind kind, dpp_comm_t comm, int64_t n, void* K_local, int64_t ld_local, uint64_t seed,
+                 uint8_t* mask, double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
+                 size_t work_bytes, cudaStream_t st) {
+  if (!comm || comm->local) return DPP_EINVAL;
+  void* K[1] = {K_local};
+  uint8_t* m[1] = {mask};
+  double* l[1] = {loglik};
+  dpp_info_t* i[1] = {info};
+  void* w[1] = {work};
+  return run_dist(kind, comm, n, K, ld_local, seed, m, l, i, opts, w, work_bytes, st);
+}
+
+int run_dist_local(Kind kind, dpp_comm_t comm, int64_t n, void* const* K_local, int64_t ld_local, uint64_t seed,
+                   uint8_t* const* mask, double* loglik, dpp_info_t* info, const dpp_opts_t* opts,
+                   void* const* work, size_t work_bytes, cudaStream_t st) {
+  if (!comm || !comm->local || !K_local || !mask || !loglik || !work) return DPP_EINVAL;
+  const int P = comm->nranks;
+  std::vector<double*> l(P);
+  std::vector<dpp_info_t*> in(P);
+  for (int r = 0; r < P; ++r) {
+    l[r] = loglik + r;
+    in[r] = info ? info + r : nullptr;
+  }
+  return run_dist(kind, comm, n, K_local, ld_local, seed, mask, l.data(), in.data(), opts, work, work_bytes, st);
 }
 
 }  // namespace
@@ -315,29 +479,43 @@ int dpp_comm_init(const void* id, int nranks, int rank, dpp_comm_t* comm) {
   c->rank = rank;
   cudaGetDevice(&c->device);
   // cap the broadcast's CTAs so it fits in the SMs the trailing update leaves free
-  const char* e = getenv("DPP_NCCL_MAX_CTAS");
-  c->max_ctas = (e && atoi(e) > 0) ? atoi(e) : 8;
+  c->max_ctas = 8;
   ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
   cfg.maxCTAs = c->max_ctas;
   if (ncclCommInitRankConfig(&c->nccl, nranks, uid, rank, &cfg) != ncclSuccess) { delete c; return DPP_ENCCL; }
-  int lo = 0, hi = 0;
-  bool ok = cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess &&
-            cudaStreamCreateWithPriority(&c->s1, cudaStreamNonBlocking, hi) == cudaSuccess &&
-            cudaStreamCreateWithPriority(&c->s2, cudaStreamNonBlocking, lo) == cudaSuccess;
-  for (cudaEvent_t* ev : {&c->ev_start, &c->ev_msg, &c->ev_rest, &c->ev_done1, &c->ev_done2})
-    ok = ok && cudaEventCreateWithFlags(ev, cudaEventDisableTiming) == cudaSuccess;
-  if (!ok) { ncclCommDestroy(c->nccl); delete c; return DPP_ECUDA; }
+  c->rs.resize(1);
+  if (make_rank_streams(&c->rs[0]) != DPP_OK) {
+    destroy_rank_streams(&c->rs[0]);
+    ncclCommDestroy(c->nccl);
+    delete c;
+    return DPP_ECUDA;
+  }
+  *comm = c;
+  return DPP_OK;
+}
+
+int dpp_comm_init_local(int nranks, dpp_comm_t* comm) {
+  if (!comm || nranks < 1 || nranks > 64) return DPP_EINVAL;
+  dpp_comm_s* c = new dpp_comm_s();
+  c->nranks = nranks;
+  c->rank = -1;
+  c->local = true;
+  cudaGetDevice(&c->device);
+  c->rs.resize(nranks);
+  for (auto& rs : c->rs)
+    if (make_rank_streams(&rs) != DPP_OK) {
+      for (auto& x : c->rs) destroy_rank_streams(&x);
+      delete c;
+      return DPP_ECUDA;
+    }
   *comm = c;
   return DPP_OK;
 }
 
 int dpp_comm_destroy(dpp_comm_t comm) {
   if (!comm) return DPP_EINVAL;
-  ncclResult_t r = ncclCommDestroy(comm->nccl);
-  cudaStreamDestroy(comm->s1);
-  cudaStreamDestroy(comm->s2);
-  for (cudaEvent_t ev : {comm->ev_start, comm->ev_msg, comm->ev_rest, comm->ev_done1, comm->ev_done2})
-    cudaEventDestroy(ev);
+  ncclResult_t r = comm->nccl ? ncclCommDestroy(comm->nccl) : ncclSuccess;
+  for (auto& rs : comm->rs) destroy_rank_streams(&rs);
   delete comm;
   return r == ncclSuccess ? DPP_OK : DPP_ENCCL;
 }
@@ -351,7 +529,7 @@ int64_t dpp_bcc_local_cols(int64_t n, int32_t nb, int nranks, int rank) {
 }
 
 size_t dpp_dist_workspace_bytes(int op, int64_t n, int nranks, const dpp_opts_t* opts) {
-  const int k = op & 3;
+  const int k = op & 0x7;
   if ((k != DPP_OP_HERM_D && k != DPP_OP_HERM_Z) || n < 0 || nranks < 1) return 0;
   const Kind kind = k == DPP_OP_HERM_D ? HERM_D : HERM_Z;
   const int nb = dist_nb(kind, opts);
@@ -359,18 +537,43 @@ size_t dpp_dist_workspace_bytes(int op, int64_t n, int nranks, const dpp_opts_t*
   return dist_ws(n, nb, kind == HERM_D ? 8 : 16).total;
 }
 
+int64_t dpp_dist_message_bytes(int op, int64_t n, int nranks, int64_t k) {
+  const int kk = op & 0x7;
+  if ((kk != DPP_OP_HERM_D && kk != DPP_OP_HERM_Z) || n < 0 || nranks < 1 || k < 0) return -1;
+  const int nb = kk == DPP_OP_HERM_D ? 128 : 64;
+  const size_t es = kk == DPP_OP_HERM_D ? 8 : 16;
+  if (k * nb >= n) return -1;
+  const int64_t jb = std::min<int64_t>(nb, n - k * nb), m2 = n - (k * nb + jb);
+  if (nranks == 1) return (int64_t)msg_layout(nb).header_bytes;
+  return (int64_t)(msg_layout(nb).header_bytes + (m2 > 0 ? (size_t)msg_pitch(m2) * (size_t)jb * es : 0));
+}
+
 int dpp_sample_herm_d_dist(dpp_comm_t comm, int64_t n, double* K_local, int64_t ld_local, uint64_t seed,
                            uint8_t* mask, double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
                            size_t work_bytes, dpp_stream_t stream) {
-  return run_dist(HERM_D, comm, n, K_local, ld_local, seed, mask, loglik, info, opts, work, work_bytes,
-                  (cudaStream_t)stream);
+  return run_dist_one(HERM_D, comm, n, K_local, ld_local, seed, mask, loglik, info, opts, work, work_bytes,
+                      (cudaStream_t)stream);
 }
 
 int dpp_sample_herm_z_dist(dpp_comm_t comm, int64_t n, dpp_complex_t* K_local, int64_t ld_local, uint64_t seed,
                            uint8_t* mask, double* loglik, dpp_info_t* info, const dpp_opts_t* opts, void* work,
                            size_t work_bytes, dpp_stream_t stream) {
-  return run_dist(HERM_Z, comm, n, K_local, ld_local, seed, mask, loglik, info, opts, work, work_bytes,
-                  (cudaStream_t)stream);
+  return run_dist_one(HERM_Z, comm, n, K_local, ld_local, seed, mask, loglik, info, opts, work, work_bytes,
+                      (cudaStream_t)stream);
+}
+
+int dpp_sample_herm_d_dist_local(dpp_comm_t comm, int64_t n, double* const* K_local, int64_t ld_local,
+                                 uint64_t seed, uint8_t* const* mask, double* loglik, dpp_info_t* info,
+                                 const dpp_opts_t* opts, void* const* work, size_t work_bytes, dpp_stream_t stream) {
+  return run_dist_local(HERM_D, comm, n, reinterpret_cast<void* const*>(K_local), ld_local, seed, mask, loglik, info,
+                        opts, work, work_bytes, (cudaStream_t)stream);
+}
+
+int dpp_sample_herm_z_dist_local(dpp_comm_t comm, int64_t n, dpp_complex_t* const* K_local, int64_t ld_local,
+                                 uint64_t seed, uint8_t* const* mask, double* loglik, dpp_info_t* info,
+                                 const dpp_opts_t* opts, void* const* work, size_t work_bytes, dpp_stream_t stream) {
+  return run_dist_local(HERM_Z, comm, n, reinterpret_cast<void* const*>(K_local), ld_local, seed, mask, loglik, info,
+                        opts, work, work_bytes, (cudaStream_t)stream);
 }
 
 }  // extern "C"

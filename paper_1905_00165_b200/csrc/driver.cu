@@ -33,22 +33,42 @@ inline size_t align_up(size_t x, size_t a = ALIGN) { return (x + a - 1) / a * a;
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 struct Opts {
-  int nb;
+  int nb;          // the diag / update tile width (32, 64, 128 real; 32, 64 complex)
   int lookahead;
   double tie_tol, range_tol;
   const uint8_t* forced;
   int64_t batch_chunk;
+  int group;             // G: trailing updates of G consecutive steps applied as one K = G nb pass
+  int64_t group_min_rows;  // -1: defaults; else group only while more than this many rows remain
+  bool generic;          // DPP_FLAG_GENERIC_UPDATE
 };
 
+// opts->nb larger than the kind's tile (256 real; 128 or 256 complex) is the blocked algorithm with
+// that block width whose diagonal-block factorization is itself blocked by the tile width: the
+// block's trailing update is one K = nb pass (a group of nb / tile steps, lookahead on).  Prop. 5
+// makes every blocking sample the same decisions in exact arithmetic.
 int resolve_opts(Kind kind, const dpp_opts_t* o, Opts* r) {
-  r->nb = (o && o->nb) ? o->nb : (kind_cplx(kind) ? 64 : 128);
+  const int tile_max = kind_cplx(kind) ? 64 : 128;
+  int nb = (o && o->nb) ? o->nb : tile_max;
   r->lookahead = o ? o->lookahead : 1;
   r->tie_tol = (o && o->tie_tol > 0) ? o->tie_tol : 1e-9;
   r->range_tol = (o && o->range_tol > 0) ? o->range_tol : 1e-8;
   r->forced = o ? o->forced : nullptr;
   r->batch_chunk = o ? o->batch_chunk : 0;
-  if (r->nb != 32 && r->nb != 64 && r->nb != 128) return DPP_EINVAL;
-  if (kind_cplx(kind) && r->nb > 64) return DPP_EINVAL;  // complex tile must fit the diag kernel
+  r->generic = o && (o->flags & DPP_FLAG_GENERIC_UPDATE);
+  if (nb != 32 && nb != 64 && nb != 128 && nb != 256) return DPP_EINVAL;
+  if (o && (o->group < 0 || o->group > 8)) return DPP_EINVAL;
+  r->group = (o && o->group) ? o->group : 2;
+  // internal: -1 = the library's default thresholds (group_threshold below), else group only while
+  // more than this many trailing rows remain (0: at every size)
+  const int64_t gm = o ? o->group_min_rows : 0;
+  r->group_min_rows = gm == 0 ? -1 : (gm < 0 ? 0 : gm);
+  if (nb > tile_max) {
+    r->group = nb / tile_max;
+    r->group_min_rows = 0;
+    nb = tile_max;
+  }
+  r->nb = nb;
   if (r->lookahead < 0 || r->lookahead > 1) return DPP_EINVAL;
   if (r->batch_chunk < 0) return DPP_EINVAL;
   return DPP_OK;
@@ -56,23 +76,22 @@ int resolve_opts(Kind kind, const dpp_opts_t* o, Opts* r) {
 
 size_t esize(Kind k) { return kind_esize(k); }
 
-int group_size();
-
 // Workspace layout (all regions 256-byte aligned):
 //   [SampleState x chunk]
 //   [panel operators: Bm (and Am for LU), nb x nb per sample]
 //   [D1 double buffer (Hermitian): 2 x chunk x nb doubles]
-//   [U12^T double buffer (LU): 2 x chunk x ldk x nb complex -- the row panel in K-major form]
-//   [W21 double buffer (Hermitian): 2 x chunk x ldk x nb -- the pre-scaled panel L21 D1]
+//   [operand panels: two group buffers of max(G, 2) panels of ldk x nb per sample -- W21 = L21 D1
+//    (Hermitian, the pre-scaled trailing-update operand) or U12^T (LU, the row panel K-major)]
 //   [K copies: chunk x ldk x n (batched / host)][host staging: mask, loglik, info (host)]
 struct WsLayout {
-  size_t state_off, bm_off, am_off, d_off, ut_off, dh_off, k_off, mask_off, ll_off, info_off, total;
+  size_t state_off, bm_off, am_off, d_off, ut_off, k_off, mask_off, ll_off, info_off, total;
   int64_t ldk, strideK, strideM, strideU;
 };
 
-WsLayout layout(Kind kind, int64_t chunk, int64_t n, int nb, bool copies, bool host) {
+WsLayout layout(Kind kind, int64_t chunk, int64_t n, const Opts& o, bool copies, bool host) {
   WsLayout L{};
   const size_t es = esize(kind);
+  const int nb = o.nb;
   L.ldk = std::max<int64_t>(round_up(n, 16), 16);
   L.strideK = L.ldk * std::max<int64_t>(n, 1);
   L.strideM = (int64_t)nb * nb;
@@ -84,10 +103,8 @@ WsLayout layout(Kind kind, int64_t chunk, int64_t n, int nb, bool copies, bool h
   if (!kind_herm(kind)) off = align_up(off + (size_t)chunk * L.strideM * es);
   L.d_off = off;
   if (kind_herm(kind)) off = align_up(off + 2 * (size_t)chunk * nb * 8);
-  L.ut_off = off;  // W21 (Hermitian) or U12^T (LU): two group buffers of max(G, 2) panels each
-  off = align_up(off + 2 * (size_t)std::max(group_size(), 2) * chunk * (size_t)L.strideU * es);
-  L.dh_off = off;  // Hermitian: D of every pivot so far (chunk x n), the column-chunked schedule
-  if (kind_herm(kind)) off = align_up(off + (size_t)chunk * (size_t)std::max<int64_t>(n, 1) * 8);
+  L.ut_off = off;
+  off = align_up(off + 2 * (size_t)std::max(o.group, 2) * chunk * (size_t)L.strideU * es);
   L.k_off = off;
   if (copies) off = align_up(off + (size_t)chunk * (size_t)L.strideK * es);
   L.mask_off = off;
@@ -101,11 +118,9 @@ WsLayout layout(Kind kind, int64_t chunk, int64_t n, int nb, bool copies, bool h
 }
 
 // ---------------------------------------------------------------- stream pair per device
-constexpr int MAX_CHUNKS = 64;
 struct DeviceStreams {
-  cudaStream_t s1 = nullptr, s2 = nullptr, s3 = nullptr;  // s3: host->device copies of the _host path
-  cudaEvent_t ev_start, ev_panel, ev_rest, ev_done1, ev_done2, ev_delay, ev_copy_start;
-  cudaEvent_t ev_chunk[MAX_CHUNKS];
+  cudaStream_t s1 = nullptr, s2 = nullptr;
+  cudaEvent_t ev_start, ev_panel, ev_rest, ev_done1, ev_done2;
   std::recursive_mutex mu;
   bool init = false;
 };
@@ -137,11 +152,8 @@ int get_streams(DeviceStreams** out, cudaStream_t caller = nullptr) {
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return DPP_ECUDA;
     if (cudaStreamCreateWithPriority(&d.s1, cudaStreamNonBlocking, hi) != cudaSuccess) return DPP_ECUDA;
     if (cudaStreamCreateWithPriority(&d.s2, cudaStreamNonBlocking, lo) != cudaSuccess) return DPP_ECUDA;
-    if (cudaStreamCreateWithPriority(&d.s3, cudaStreamNonBlocking, lo) != cudaSuccess) return DPP_ECUDA;
-    for (cudaEvent_t* e : {&d.ev_start, &d.ev_panel, &d.ev_rest, &d.ev_done1, &d.ev_done2, &d.ev_delay, &d.ev_copy_start})
+    for (cudaEvent_t* e : {&d.ev_start, &d.ev_panel, &d.ev_rest, &d.ev_done1, &d.ev_done2})
       if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return DPP_ECUDA;
-    for (cudaEvent_t& e : d.ev_chunk)
-      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return DPP_ECUDA;
     d.init = true;
   }
   *out = &d;
@@ -213,13 +225,8 @@ int device_sms() {
 // g = G for the last step of a group: its trailing update has K = G nb (G times the tile time) and
 // the chain beside it holds the next group's G diag tiles and G panels.
 int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile, bool herm, int g = 1) {
-  // the diag tile in update-tile times (DPP_DIAG_TILES; 5 measured ~100 us vs ~20 us; after the
-  // diag kernel went to 63 us, 2.5 .. 5 give the same C4 / UST rates within noise)
-  static double diag_tiles = -1.0;
-  if (diag_tiles < 0) {
-    const char* e = getenv("DPP_DIAG_TILES");
-    diag_tiles = e ? atof(e) : 5.0;
-  }
+  // the diag tile in update-tile times (measured: 2.5 .. 5 give the same C4 / UST rates within noise)
+  constexpr double diag_tiles = 5.0;
   const double side = (double)((m2 + tile - 1) / tile), side_b = (double)((m2 - jn + tile - 1) / tile);
   const double ta = (herm ? 1.0 : 2.0) * side * batch;     // (a): next block column (LU: + row)
   const double tp = (herm ? 1.0 : 2.0) * side_b * batch;   // next panel GEMM(s)
@@ -244,107 +251,30 @@ UpdateArgs base_update(Kind kind, int batch, bool vec) {
 }
 
 // ---------------------------------------------------------------- the blocked factorization
-// Factors `batch` matrices A + s*strideA (in place), samples b0 + s.
-// Column-chunked schedule (Hermitian kinds, lookahead on): the factorization proceeds over column
-// chunks of cw columns; inside a chunk it is the right-looking loop below with its trailing
-// updates restricted to the chunk's columns, and each new chunk first receives every earlier
-// panel at once (one DMMA GEMM with K = c0, B scaled by the saved pivots) -- Prop. 5's exactness
-// does not depend on the update order.  A chunk can start as soon as its columns are resident:
-// the _host path copies chunk by chunk on a third stream and the chunk events gate the compute.
-struct Chunking {
-  int64_t cw = 0;               // 0: off
-  const cudaEvent_t* ev = nullptr;  // per chunk: its columns are resident (nullable)
-  // copy-gated mode (the _host path's default): the factorization is NOT restricted; the copy
-  // arrives in chunks of copy_cw columns (events ev), each step's diag/panel/lookahead waits for
-  // the chunk holding its next block column, and the trailing updates of the first split_steps
-  // steps are launched per copy chunk, each waiting only for its own chunk
-  int64_t copy_cw = 0;
-  int split_steps = 0;
-};
-
-// DPP_CHUNK_COLS > 0 selects the column-chunked factorization (both paths; measured slower: 19.9
-// vs 25.8 TF/s at n = 16384 with 2048-column chunks -- the restricted trailing updates leave the
-// sequential chain exposed in every chunk).
-int chunk_cols(bool host, int64_t n) {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("DPP_CHUNK_COLS");
-    v = e ? atoi(e) : 0;
-  }
-  (void)host;
-  (void)n;
-  return v;
-}
-
-// DPP_COPY_GATED=1: the _host path's copy-gated mode.  Off by default: measured slower (e2e 18.3
-// vs 19.3 TF/s at n = 16384) -- the right-looking order needs every column before the first
-// trailing update completes, and the work a left-looking order could do on the first columns is
-// small, so little of the copy can hide behind compute.
 // Grouped trailing updates (lookahead on): the trailing updates of G consecutive steps are applied
 // by the group's last step as ONE DMMA pass with K = G nb (the G panels are adjacent columns of the
 // factor; their operand copies -- W21 = L21 D1, or U12^T -- are stacked in one buffer), so the
 // update kernel's per-tile epilogue and the C read/write are amortized over G times the work.
-// G = 2 ("paired updates") by default; DPP_GROUP=g sets G, DPP_PAIR=0 turns grouping off.
-int group_size() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DPP_PAIR");
-    const char* g = getenv("DPP_GROUP");
-    v = (e && e[0] == '0') ? 1 : (g ? std::max(1, std::min(8, atoi(g))) : 2);
-  }
-  return v;
+// G = 2 ("paired updates") by default (opts->group).
+//
+// Default grouping thresholds (opts->group_min_rows = 0): no grouping once the trailing size is
+// <= 6144 rows for 128-wide Hermitian blocks, where the diag tile makes the chain the bound near
+// the end (measured C4 25.8 -> 26.1 TF/s); 0 for 64-wide Hermitian blocks, whose chain is short
+// (complex Hermitian n = 8192: 27.0 vs 26.6 TF/s with 6144); 8192 for LU (two panel GEMMs and two
+// lookahead updates per step: n = 8192 27.6 TF/s unpaired vs 26.1 paired; Aztec n = 25600 33.3
+// paired vs 32.0); 0 for batches of >= 8 (the chain is shared by the batch and the updates
+// dominate throughout: UST 40x40, 256 per launch, 2373 paired vs 2275 samples/s).
+int64_t group_threshold(const Opts& o, bool herm, int batch) {
+  if (o.group_min_rows >= 0) return o.group_min_rows;
+  if (batch >= 8) return 0;
+  if (!herm) return 8192;
+  return o.nb >= 128 ? 6144 : 0;
 }
 
-// rows below which the real Hermitian sampler switches to half-width blocks (DPP_TAIL_ROWS, 0 = off)
-int64_t tail_rows() {
-  static long long v = -1;
-  if (v < 0) {
-    const char* e = getenv("DPP_TAIL_ROWS");
-    v = e ? atoll(e) : 0;
-  }
-  return (int64_t)v;
-}
-
-// trailing size below which updates are no longer paired (DPP_PAIR_MIN_ROWS; defaults: 6144 rows
-// for 128-wide Hermitian blocks, where the 63..86-us diag tile makes the chain the bound near the end --
-// measured C4 25.8 -> 26.1 TF/s -- 0 for 64-wide Hermitian blocks, whose chain is short (complex
-// Hermitian n = 8192: 27.0 vs 26.6 TF/s with 6144), 8192 for LU)
-int64_t pair_min_rows(int nb, bool herm, int batch) {
-  static long long v = -2;
-  if (v == -2) {
-    const char* e = getenv("DPP_PAIR_MIN_ROWS");
-    v = e ? atoll(e) : -1;
-  }
-  if (v >= 0) return (int64_t)v;
-  if (batch >= 8) return 0;  // batched: the chain is shared by the batch, the updates dominate throughout
-                             // (UST 40x40, 256 per launch: 2373 paired vs 2275 samples/s)
-  if (!herm) return 8192;  // LU: two panel GEMMs and two lookahead updates per step (n = 8192: 27.6
-                           // TF/s unpaired vs 26.1 paired; Aztec n = 25600: 33.3 paired vs 32.0)
-  return nb >= 128 ? 6144 : 0;
-}
-
-bool head_block() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DPP_HEAD_BLOCK");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
-bool copy_gated() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DPP_COPY_GATED");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
+// Factors `batch` matrices A + s*strideA (in place), samples b0 + s.
 int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_t strideA, int batch,
                 uint64_t seed, uint64_t b0, uint8_t* mask, const uint8_t* forced, double* loglik,
-                dpp_info_t* info, char* work, const WsLayout& L, cudaStream_t caller, bool map = false,
-                Chunking ch = Chunking{}) {
+                dpp_info_t* info, char* work, const WsLayout& L, cudaStream_t caller, bool map = false) {
   void* state = work + L.state_off;
   if (n == 0) { CK(launch_zero_state(state, loglik, info, batch, caller)); return DPP_OK; }
   DeviceStreams* ds = nullptr;
@@ -365,6 +295,10 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
   // 16-byte aligned columns: the TMA / cp.async 16-byte operand paths
   const bool vec = ((size_t)ld * es) % 16 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0 &&
                    ((size_t)strideA * es) % 16 == 0;
+  auto upd = [&](UpdateArgs u, cudaStream_t s) -> cudaError_t {
+    u.generic = o.generic ? 1 : 0;
+    return launch_update(kind, u, s);
+  };
   void* Bm = work + L.bm_off;
   void* Am = work + L.am_off;
   int step = 0;
@@ -372,70 +306,28 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
   int gpos = -1;            // position of the previous step in its group (-1: none)
   bool prev_glast = false;  // the previous step was the last of a group
   const int sms = device_sms();
-  if (!herm || !la || ch.cw < nb || ch.cw % nb) ch.cw = 0;
-  if (ch.cw && (n + ch.cw - 1) / ch.cw > MAX_CHUNKS) ch.cw = (n + MAX_CHUNKS - 1) / MAX_CHUNKS / nb * nb + nb;
-  double* dhist = herm ? reinterpret_cast<double*>(work + L.dh_off) : nullptr;
-  // Tail blocks: once at most `thr` rows remain, the blocks are nb/2 wide -- the sequential chain
-  // (diag tile, panel, lookahead column) is what bounds those steps, and a half-width diag tile
-  // costs far less than half of a full one.  Pivot draws are by global index (R2): the blocking
-  // does not change the sample.
-  const int64_t thr = (nb == 128 && herm && la && !ch.cw && !ch.copy_cw) ? tail_rows() : 0;
-  auto bs_of = [&](int64_t j) -> int { return (thr > 0 && n - j <= thr) ? nb / 2 : nb; };
   // Head block: when nb does not divide n, the FIRST block takes the remainder (n mod nb) so that
-  // every trailing region is a whole number of 128-row tiles (a ragged last block would leave a
-  // partly empty tile row and column in every trailing update).  Only when the remainder keeps every
-  // block origin 16-byte aligned (the TMA operand copies): a multiple of 16 / element-size rows.
-  // DPP_HEAD_BLOCK=0: ragged last block.
+  // every trailing region is a whole number of tiles (a ragged last block would leave a partly
+  // empty tile row and column in every trailing update: UST n = 3120, 2472 -> 2574 samples/s).
+  // Only when the remainder keeps every block origin 16-byte aligned (the TMA operand copies): a
+  // multiple of 16 / element-size rows.  Pivot draws are by global index (reading R2), so the
+  // blocking does not change the sample.
   const int64_t rem = n % nb;
-  const int64_t head = (head_block() && !ch.cw && !ch.copy_cw && thr == 0 && n > nb && rem &&
-                        rem % (int64_t)(16 / es) == 0) ? rem : 0;
+  const int64_t head = (n > nb && rem && rem % (int64_t)(16 / es) == 0) ? rem : 0;
   const int gbase = head ? 1 : 0;  // groups are aligned after the head block
-  auto blk = [&](int64_t j) -> int64_t { return (head && j == 0) ? head : std::min<int64_t>(bs_of(j), n - j); };
+  const int G = o.group;
+  const int64_t gthr = group_threshold(o, herm, batch);
+  auto blk = [&](int64_t j) -> int64_t { return (head && j == 0) ? head : std::min<int64_t>(nb, n - j); };
   for (int64_t j0 = 0; j0 < n; j0 += blk(j0), ++step) {
     const int jb = (int)blk(j0);
     const int64_t j1 = j0 + jb, m2 = n - j1;
-    const int64_t c0 = ch.cw ? (j0 / ch.cw) * ch.cw : 0;
-    const int64_t ce = ch.cw ? std::min<int64_t>(n, c0 + ch.cw) : n;  // the chunk's columns: [c0, ce)
-    if (ch.copy_cw && ch.ev) {
-      // copy-gated: this step's tile, panel and lookahead column need the chunk of block column
-      // j0 + 1 (and all before it -- the copies are issued in order on one stream)
-      const int64_t need = std::min<int64_t>(n - 1, j1 + nb - 1);
-      CK(cudaStreamWaitEvent(s1, ch.ev[need / ch.copy_cw], 0));
-      // past the split steps the trailing updates are single launches: the whole copy must be in
-      if (step == ch.split_steps) CK(cudaStreamWaitEvent(s2, ch.ev[(n - 1) / ch.copy_cw], 0));
-    }
-    if (ch.cw && j0 == c0) {
-      if (ch.ev) {
-        CK(cudaStreamWaitEvent(s1, ch.ev[j0 / ch.cw], 0));
-        CK(cudaStreamWaitEvent(s2, ch.ev[j0 / ch.cw], 0));
-      }
-      if (c0 > 0) {
-        // every earlier panel into the new chunk: A(c0:n, c0:ce) -= L(c0:n, 0:c0) D L(c0:ce, 0:c0)^H
-        CK(cudaEventRecord(ds->ev_panel, s1));
-        CK(cudaStreamWaitEvent(s2, ds->ev_panel, 0));
-        UpdateArgs dl = base_update(kind, batch, vec);
-        dl.Aop = Ab + (size_t)c0 * es; dl.lda = ld; dl.strideA = strideA;
-        dl.Bop = Ab + (size_t)c0 * es; dl.ldb = ld; dl.strideB = strideA;
-        dl.dscale = dhist; dl.dstride = n; dl.mask = 1; dl.conj = (kind == HERM_Z);
-        dl.C = Ab + (size_t)(c0 + c0 * ld) * es; dl.ldc = ld; dl.strideC = strideA;
-        dl.a_rows = (int)(n - c0); dl.b_rows = (int)(ce - c0); dl.K = (int)c0;
-        dl.row0 = 0; dl.col0 = 0; dl.rows = (int)(n - c0); dl.cols = (int)(ce - c0); dl.tri = 0;
-        {
-          ProfScope ps(3, region_flops(kind, c0, c0, n - c0, ce - c0, (int)c0) * batch, s2);
-          CK(launch_update(kind, dl, s2));
-        }
-        CK(cudaEventRecord(ds->ev_delay, s2));
-        CK(cudaStreamWaitEvent(s1, ds->ev_delay, 0));
-      }
-    }
     double* dvec = herm ? reinterpret_cast<double*>(work + L.d_off) + (size_t)(step & 1) * batch * nb : nullptr;
     // LU: U12^T (m2 x jb, ld = ldk, K-major GEMM operand); Hermitian: W21 = L21 D1 (same shape);
     // double-buffered like D1
     const int64_t strideU = L.strideU;
     char* UT = work + L.ut_off + (size_t)(step & 1) * batch * strideU * es;
     // grouping: steps (G g .. G g + G-1) share the group buffer (g & 1) of G panels per sample
-    const int G = group_size();
-    const bool grouping = la && !ch.cw && !ch.copy_cw && G > 1 && nb == (int)std::min<int64_t>(nb, n);
+    const bool grouping = la && G > 1 && nb == (int)std::min<int64_t>(nb, n);
     const int64_t strideW = (int64_t)std::max(G, 2) * strideU;
     const int gstep = step - gbase;  // (-1 for the head block: group buffer 1, unused by group 0)
     char* WP = work + L.ut_off + (size_t)((gstep < 0 ? 1 : gstep / G) & 1) * batch * strideW * es;
@@ -449,11 +341,8 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     if (grouping) {
       if (gpos >= 0 && gpos < G - 1) {
         gp = gpos + 1;
-      } else if (gstep >= 0 && gstep % G == 0 && m2 - (int64_t)(G - 1) * nb > 0 &&
-                 m2 > pair_min_rows(nb, herm, batch)) {
-        bool full = true;
-        for (int g = 0; g < G; ++g) full = full && bs_of(j0 + (int64_t)g * nb) == nb;
-        if (full) gp = 0;
+      } else if (gstep >= 0 && gstep % G == 0 && m2 - (int64_t)(G - 1) * nb > 0 && m2 > gthr) {
+        gp = 0;
       }
     }
     const bool glast = gp == G - 1, gnonlast = gp >= 0 && !glast;
@@ -473,12 +362,9 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     {
       const double fl = (herm ? 1.0 : 2.0) * jb * (double)jb * jb / 3.0 * cplx_mult(kind) * batch;
       ProfScope ps(0, fl, s1);
-      CK(launch_diag(kind, bs_of(j0), d, s1));
+      CK(launch_diag(kind, nb, d, s1));
     }
     if (m2 <= 0) break;
-    if (ch.cw && herm)  // this block's pivots, for the later chunks' catch-up updates
-      CK(cudaMemcpy2DAsync(dhist + j0, (size_t)n * 8, dvec, (size_t)nb * 8, (size_t)jb * 8, (size_t)batch,
-                           cudaMemcpyDeviceToDevice, s1));
     // ---- stage 2: panel GEMMs with the tile operators (in place)
     {
       const double fl = (herm ? 1.0 : 2.0) * (double)m2 * jb * jb * cplx_mult(kind) * batch;  // TRSM count
@@ -495,7 +381,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
         p.wout = grouping ? PH : UT; p.ldw = L.ldk; p.strideWo = grouping ? strideW : strideU;
         p.wscale = dvec; p.wsstride = nb;
       }
-      CK(launch_update(kind, p, s1));
+      CK(upd(p, s1));
       if (!herm) {
         // U12 = L11^-1 A12 = A12 - Am A12 (Am = I - L11^-1), computed transposed so that every
         // operand is K-major:  U12^T = A12^T - A12^T Am^T  in the U12^T buffer, then copied back.
@@ -509,7 +395,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
         q.C = UTs; q.ldc = L.ldk; q.strideC = sU;                                  // U12^T in place
         q.a_rows = (int)m2; q.b_rows = jb; q.K = jb;
         q.row0 = 0; q.col0 = 0; q.rows = (int)m2; q.cols = jb;
-        CK(launch_update(kind, q, s1));
+        CK(upd(q, s1));
         if (!la) {
           ProfScope pa(4, 0.0, s1);
           CK(launch_transpose(es, UTs, L.ldk, sU, A12, ld, strideA, (int)m2, jb, batch, s1));  // U12 -> K
@@ -545,11 +431,11 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     u.a_rows = (int)m2; u.b_rows = (int)m2; u.K = (gp > 0 ? gp * nb : 0) + jb;
     // width of the lookahead region: the next block -- or, at the last step of a group, the next
     // group's G blocks, so the next group's whole diag/panel chain runs under this group's update
-    const int jn = (int)std::min<int64_t>(glast ? (int64_t)G * nb : bs_of(j1), m2);
+    const int jn = (int)std::min<int64_t>(glast ? (int64_t)G * nb : nb, m2);
     if (!la) {
       u.row0 = 0; u.col0 = 0; u.rows = (int)m2; u.cols = (int)m2; u.tri = herm;
       ProfScope ps(3, region_flops(kind, 0, 0, m2, m2, jb) * batch, s1);
-      CK(launch_update(kind, u, s1));
+      CK(upd(u, s1));
       continue;
     }
     CK(cudaEventRecord(ds->ev_panel, s1));
@@ -559,49 +445,36 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       CK(launch_transpose(es, cb_src, L.ldk, cb_stride, cb_dst, ld, strideA, (int)m2, jb, batch, s2));  // U12 -> K
       copyback = false;
     }
-    // (a) next block column [0, jn) x rows [0, m2)  (+ LU: next block row [0, jn) x cols [jn, m2));
-    // chunked: only while the next block is in this chunk (else the catch-up update covers it)
+    // (a) next block column [0, jn) x rows [0, m2)  (+ LU: next block row [0, jn) x cols [jn, m2))
     // (a non-last step of a group needs no wait: its lookahead block was covered by the previous
     // group's lookahead update and is not part of the previous trailing update)
     if (have_rest && !(gnonlast && (gp > 0 || prev_glast))) CK(cudaStreamWaitEvent(s1, ds->ev_rest, 0));
     prev_glast = glast;
-    if (j1 < ce) {
+    {
       UpdateArgs ua = u;
       ua.row0 = 0; ua.col0 = 0; ua.rows = (int)m2; ua.cols = jn; ua.tri = 0;
       double fl = region_flops(kind, 0, 0, m2, jn, ua.K);
       if (!herm && m2 > jn) fl += region_flops(kind, 0, jn, jn, m2 - jn, jb);
       ProfScope ps(2, fl * batch, s1);
-      CK(launch_update(kind, ua, s1));
+      CK(upd(ua, s1));
       if (!herm && m2 > jn) {
         UpdateArgs ur = u;
         ur.row0 = 0; ur.col0 = jn; ur.rows = jn; ur.cols = (int)(m2 - jn); ur.tri = 0;
-        CK(launch_update(kind, ur, s1));
+        CK(upd(ur, s1));
       }
     }
-    // (b) the rest [jn, m2)^2 on S2 (chunked: its columns restricted to the chunk)
-    const int64_t colsb = std::min<int64_t>(m2, ce - j1) - jn;
+    // (b) the rest [jn, m2)^2 on S2, persistently on the SMs the lookahead chain leaves free
     gpos = gp;  // a non-last position: the group's last step applies this step's trailing update
-    if (m2 > jn && colsb > 0 && !gnonlast) {
+    if (m2 > jn && !gnonlast) {
       CK(cudaStreamWaitEvent(s2, ds->ev_panel, 0));
       UpdateArgs ub = u;
-      ub.row0 = jn; ub.col0 = jn; ub.rows = (int)(m2 - jn); ub.cols = (int)colsb;
-      ub.tri = herm && colsb == m2 - jn;
+      ub.row0 = jn; ub.col0 = jn; ub.rows = (int)(m2 - jn); ub.cols = (int)(m2 - jn);
+      ub.tri = herm;
       if (vec)
         ub.grid_limit = sms - reserve_sms(m2, jn, sms, batch, kind_cplx(kind) ? 64 : 128, herm, glast ? G : 1);
-      if (ch.copy_cw && ch.ev && step < ch.split_steps) {
-        // one launch per copy chunk of the trailing columns, each gated by its own chunk
-        for (int64_t g0 = j1 + jn; g0 < j1 + jn + colsb;) {
-          const int64_t g1 = std::min<int64_t>(j1 + jn + colsb, (g0 / ch.copy_cw + 1) * ch.copy_cw);
-          CK(cudaStreamWaitEvent(s2, ch.ev[(g1 - 1) / ch.copy_cw], 0));
-          UpdateArgs up = ub;
-          up.col0 = (int)(g0 - j1); up.cols = (int)(g1 - g0); up.tri = 0;
-          ProfScope ps(3, region_flops(kind, jn, g0 - j1, m2 - jn, g1 - g0, jb) * batch, s2);
-          CK(launch_update(kind, up, s2));
-          g0 = g1;
-        }
-      } else {
-        ProfScope ps(3, region_flops(kind, jn, jn, m2 - jn, colsb, ub.K) * batch, s2);
-        CK(launch_update(kind, ub, s2));
+      {
+        ProfScope ps(3, region_flops(kind, jn, jn, m2 - jn, m2 - jn, ub.K) * batch, s2);
+        CK(upd(ub, s2));
       }
       CK(cudaEventRecord(ds->ev_rest, s2));
       have_rest = true;
@@ -632,13 +505,11 @@ int sample_inplace(Kind kind, int64_t n, void* K, int64_t ld, uint64_t seed, uin
   if (rc) return rc;
   if ((rc = validate(n, ld, K, mask, loglik))) return rc;
   if ((rc = check_device())) return rc;
-  WsLayout L = layout(kind, 1, n, o.nb, false, false);
+  WsLayout L = layout(kind, 1, n, o, false, false);
   if (!work || work_bytes < L.total || reinterpret_cast<uintptr_t>(work) % ALIGN) return DPP_EWORKSPACE;
   if (reinterpret_cast<uintptr_t>(K) % esize(kind)) return DPP_EINVAL;
-  Chunking chk;
-  chk.cw = kind_herm(kind) ? chunk_cols(false, n) : 0;
   return run_blocked(kind, o, n, K, ld, 0, 1, seed, 0, mask, o.forced, loglik, info, reinterpret_cast<char*>(work),
-                     L, st, map, chk);
+                     L, st, map);
 }
 
 int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t ld, int64_t strideK, uint64_t seed,
@@ -654,7 +525,7 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
   if ((rc = check_device())) return rc;
   const int64_t chunk = o.batch_chunk > 0 ? std::min(o.batch_chunk, batch) : batch;
   if (chunk > 65535) return DPP_EINVAL;
-  WsLayout L = layout(kind, chunk, n, o.nb, true, host);
+  WsLayout L = layout(kind, chunk, n, o, true, host);
   if (!work || work_bytes < L.total || reinterpret_cast<uintptr_t>(work) % ALIGN) return DPP_EWORKSPACE;
   char* w = reinterpret_cast<char*>(work);
   const size_t es = esize(kind);
@@ -680,56 +551,6 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
   };
   for (int64_t c0 = 0; c0 < batch; c0 += chunk) {
     const int cb = (int)std::min<int64_t>(chunk, batch - c0);
-    const int64_t cw = (lower && cb == 1 && o.lookahead > 0) ? chunk_cols(host, n) : 0;
-    const bool gated = host && lower && cb == 1 && o.lookahead > 0 && n >= 4096 && copy_gated();
-    if (host && (cw > 0 || gated) && n > 0) {
-      // pipelined: the copy of column chunk c (on s3) gates only chunk c of the factorization
-      DeviceStreams* ds = nullptr;
-      if ((rc = get_streams(&ds, st))) return rc;
-      std::lock_guard<std::recursive_mutex> lk(ds->mu);
-      CK(cudaEventRecord(ds->ev_copy_start, st));
-      CK(cudaStreamWaitEvent(ds->s3, ds->ev_copy_start, 0));
-      const char* src = reinterpret_cast<const char*>(K) + (size_t)(strideK * c0) * es;
-      int64_t cwe = cw > 0 ? cw : 2048;
-      if ((n + cwe - 1) / cwe > MAX_CHUNKS) cwe = (n + MAX_CHUNKS - 1) / MAX_CHUNKS / o.nb * o.nb + o.nb;
-      for (int64_t q0 = 0, ci = 0; q0 < n; q0 += cwe, ++ci) {
-        for (int64_t c = q0; c < std::min<int64_t>(n, q0 + cwe); c += 128) {
-          const int64_t w_ = std::min<int64_t>({(int64_t)128, n - c, q0 + cwe - c});
-          CK(cudaMemcpy2DAsync(Kc + (size_t)(c + c * L.ldk) * es, (size_t)L.ldk * es, src + (size_t)(c + c * ld) * es,
-                               (size_t)ld * es, (size_t)(n - c) * es, (size_t)w_, ck, ds->s3));
-        }
-        CK(cudaEventRecord(ds->ev_chunk[ci], ds->s3));
-      }
-      uint8_t* mk = reinterpret_cast<uint8_t*>(w + L.mask_off);
-      double* llk = reinterpret_cast<double*>(w + L.ll_off);
-      dpp_info_t* ifo = info ? reinterpret_cast<dpp_info_t*>(w + L.info_off) : nullptr;
-      const uint8_t* fz = o.forced ? o.forced + c0 * n : nullptr;
-      Chunking chk;
-      chk.ev = ds->ev_chunk;
-      if (cw > 0) {
-        chk.cw = cwe;
-      } else {
-        // copy-gated: split the trailing updates of the steps that can start before the copy is
-        // over (estimate: copy at ~50 GB/s, trailing updates at ~25 TF/s)
-        chk.copy_cw = cwe;
-        double t_copy = 0.0;
-        for (int64_t c = 0; c < n; c += 128) t_copy += (double)(n - c) * std::min<int64_t>(128, n - c) * es / 50e9;
-        double t = 0.0;
-        int k = 0;
-        for (int64_t j = 0; j < n && t < t_copy; j += o.nb, ++k) {
-          const double m = (double)(n - j - o.nb);
-          t += m > 0 ? m * m * o.nb * cplx_mult(kind) / 25e12 : 0.0;
-        }
-        chk.split_steps = k + 1;
-      }
-      rc = run_blocked(kind, o, n, Kc, L.ldk, L.strideK, cb, seed, b0 + (uint64_t)c0, mk, fz, llk, ifo, w, L, st,
-                       false, chk);
-      if (rc) return rc;
-      CK(cudaMemcpyAsync(mask + c0 * n, mk, (size_t)cb * n, cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(loglik + c0, llk, 8 * (size_t)cb, cudaMemcpyDeviceToHost, st));
-      if (info) CK(cudaMemcpyAsync(info + c0, ifo, sizeof(dpp_info_t) * (size_t)cb, cudaMemcpyDeviceToHost, st));
-      continue;
-    }
     if (n > 0) {
       if (host && strideK == 0) {
         // one host->device transfer of the shared kernel, then device-side replication
@@ -752,10 +573,7 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
     double* llk = host ? reinterpret_cast<double*>(w + L.ll_off) : loglik + c0;
     dpp_info_t* ifo = host ? (info ? reinterpret_cast<dpp_info_t*>(w + L.info_off) : nullptr) : (info ? info + c0 : nullptr);
     const uint8_t* fz = o.forced ? o.forced + c0 * n : nullptr;
-    Chunking chk;
-    chk.cw = cw;
-    rc = run_blocked(kind, o, n, Kc, L.ldk, L.strideK, cb, seed, b0 + (uint64_t)c0, mk, fz, llk, ifo, w, L, st, false,
-                     chk);
+    rc = run_blocked(kind, o, n, Kc, L.ldk, L.strideK, cb, seed, b0 + (uint64_t)c0, mk, fz, llk, ifo, w, L, st);
     if (rc) return rc;
     if (host) {
       if (n > 0) CK(cudaMemcpyAsync(mask + c0 * n, mk, (size_t)cb * n, cudaMemcpyDeviceToHost, st));
@@ -781,7 +599,7 @@ size_t dpp_workspace_bytes(int op, int64_t batch, int64_t n, const dpp_opts_t* o
   int64_t chunk = batched ? batch : 1;
   if (batched && o.batch_chunk > 0) chunk = std::min(chunk, o.batch_chunk);
   chunk = std::max<int64_t>(chunk, 1);
-  return layout(kind, chunk, n, o.nb, batched, host).total;
+  return layout(kind, chunk, n, o, batched, host).total;
 }
 
 int dpp_sample_herm_d(int64_t n, double* K, int64_t ld, uint64_t seed, uint8_t* mask, double* loglik,
@@ -872,16 +690,22 @@ int dpp_profile_end(dpp_profile_t* out) {
     out->launches[r.stage] += 1;
     out->ms[r.stage] += ms;
     out->flops[r.stage] += r.flops;
+    if (r.flops > out->top_flops[r.stage]) { out->top_flops[r.stage] = r.flops; out->top_ms[r.stage] = ms; }
     iv[r.stage].push_back({(double)t0, (double)t1});
   }
   for (int st = 0; st < 5; ++st) {  // length of the union of the stage's launch intervals
+    // offsets are from the first record ISSUED, so intervals on other streams may start before
+    // it (negative offsets): the sweep starts from the earliest interval, not from 0
     std::sort(iv[st].begin(), iv[st].end());
-    double lo = 0.0, hi = -1.0, u = 0.0;
-    for (auto& p : iv[st]) {
-      if (p.first > hi) { if (hi > lo) u += hi - lo; lo = p.first; hi = p.second; }
-      else if (p.second > hi) hi = p.second;
+    double u = 0.0;
+    if (!iv[st].empty()) {
+      double lo = iv[st][0].first, hi = iv[st][0].second;
+      for (auto& p : iv[st]) {
+        if (p.first > hi) { u += hi - lo; lo = p.first; hi = p.second; }
+        else if (p.second > hi) hi = p.second;
+      }
+      u += hi - lo;
     }
-    if (hi > lo) u += hi - lo;
     out->ms_union[st] = u;
   }
   g_prof.recs.clear();

@@ -309,16 +309,12 @@ int dpp_elementary_herm_d(int64_t batch, int64_t n, int64_t k, const double* K, 
   a.st = reinterpret_cast<ElemState*>(w + W.st_off);
   a.order = order; a.loglik = loglik; a.ties = ties;
   const size_t smem = (size_t)k * 8;
-  // one CTA per sample when the batch fills the GPU (DPP_ELEM_FUSED=0/1 forces a choice)
-  static int fused_env = -2;
-  if (fused_env == -2) {
-    const char* e = getenv("DPP_ELEM_FUSED");
-    fused_env = e ? atoi(e) : -1;
-  }
+  // one CTA per sample for the whole draw when the batch fills the GPU (one launch per call: 3.7x
+  // at rank 10); otherwise per-step kernels that spread each sample's column update over the SMs
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const bool fused = fused_env >= 0 ? fused_env == 1 : batch >= sms;
+  const bool fused = batch >= sms;
   if (fused) {
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(elem_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)

@@ -67,6 +67,7 @@ struct UpdateArgs {
   int64_t dstride;
   int ktri;             // 1: A(i, k) = 0 for k < i (upper-triangular A): a tile starts its K loop at
                         //    its first row (fast kernel only; the others just multiply the zeros)
+  int generic;          // 1: the cp.async fallback kernel even for aligned operands (DPP_FLAG_GENERIC_UPDATE)
   int grid_limit;       // > 0: persistent launch with at most this many CTAs (SMs left to the
                         //      lookahead stream); 0: short-lived CTAs (<= 4 tiles each)
   // 1D block-column-cyclic mode (bcc_P > 0, BN == nb): tile column tj is local block

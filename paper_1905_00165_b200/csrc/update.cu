@@ -269,29 +269,14 @@ cudaError_t launch_transpose(size_t es, const void* src, int64_t lds, int64_t st
 
 // Dispatch on (kind, operand layout, flags).  Fast path: update_ws.cu (persistent,
 // warp-specialized, TMA-fed) for 16-byte-aligned operands; this file's cp.async kernel otherwise.
-static int g_force_generic = -1;
 static cudaError_t launch_update_core(Kind kind, UpdateArgs a, cudaStream_t s, bool ws);
-
-// DPP_FUSE_W=0: the second output W always by the separate column-scaling pass
-static bool fuse_w() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DPP_FUSE_W");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
 
 cudaError_t launch_update(Kind kind, UpdateArgs a, cudaStream_t s) {
   if (a.rows <= 0 || a.cols <= 0 || a.K <= 0) return cudaSuccess;
-  if (g_force_generic < 0) {
-    const char* e = getenv("DPP_UPDATE_GENERIC");  // test hook: exercise the generic kernel
-    g_force_generic = (e && e[0] == '1') ? 1 : 0;
-  }
-  const bool ws = a.vec && !g_force_generic && kind != HERM_S && kind != LU_C;
+  const bool ws = a.vec && !a.generic && kind != HERM_S && kind != LU_C;
   // the second output W: fused into the warp-specialized panel kernel (no mask, Hermitian), else a
   // column-scaling pass over the updated region
-  const bool fuse = a.wout && ws && !a.mask && a.bcc_P == 0 && (kind == HERM_D || kind == HERM_Z) && fuse_w();
+  const bool fuse = a.wout && ws && !a.mask && a.bcc_P == 0 && (kind == HERM_D || kind == HERM_Z);
   UpdateArgs k = a;
   if (!fuse) k.wout = nullptr;
   cudaError_t e = launch_update_core(kind, k, s, ws);

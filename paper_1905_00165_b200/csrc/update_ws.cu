@@ -8,7 +8,7 @@
 //  * one PRODUCER warp streams operand K-chunks with TMA bulk copies (cp.async.bulk, one 1-D copy
 //    per column segment into padded shared rows) into a STAGES-deep ring guarded by full/empty
 //    mbarriers; a second warp owns the C tile (bulk load -> consumers subtract -> bulk store);
-//  * CONSUMER warps (real: 16 of 32x32 in the default layout V1; complex: 8 of 32x16) run
+//  * CONSUMER warps (real: 16 of 32x32; complex: 8 of 32x16) run
 //    DMMA.8x8x4 (mma.sync m8n8k4 f64) out of the ring with no CTA-wide barrier in the main loop and
 //    subtract their accumulators from the C tile in shared memory.
 // Ragged edges: rows/columns beyond the tile are left stale in shared memory (they only feed
@@ -16,7 +16,6 @@
 // ordinary loads/stores.
 #include <cuda_runtime.h>
 
-#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -25,14 +24,8 @@
 namespace dpp {
 
 template <bool CPLX, int V> struct WsCfg;
-template <> struct WsCfg<false, 0> {  // real: 128x128 tile, consumer warps 2(M) x 4(N) of 64x32
-  static constexpr int BM = 128, BN = 128, WM = 2, WN = 4, KC = 8, STAGES = 5;
-};
 template <> struct WsCfg<false, 1> {  // real: 128x128 tile, 16 consumer warps 4 x 4 of 32x32
   static constexpr int BM = 128, BN = 128, WM = 4, WN = 4, KC = 8, STAGES = 5;
-};
-template <> struct WsCfg<false, 2> {  // real: 64x128 tile, 8 consumer warps 2 x 4 of 32x32, 2 CTAs per SM
-  static constexpr int BM = 64, BN = 128, WM = 2, WN = 4, KC = 8, STAGES = 3;
 };
 template <> struct WsCfg<true, 0> {   // complex: 64x64 tile, consumer warps 2 x 4 of 32x16
   static constexpr int BM = 64, BN = 64, WM = 2, WN = 4, KC = 8, STAGES = 4;
@@ -66,7 +59,7 @@ __device__ __forceinline__ void consumer_sync(int nthreads) {
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
 template <bool CPLX, bool BNMAJ, bool MASK, bool SCALE, bool CONJ, int V>
-__global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, (V == 2) ? 2 : 1) update_ws_kernel(const UpdateArgs a) {
+__global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_kernel(const UpdateArgs a) {
   using LY = WsLayoutT<CPLX, BNMAJ, V>;
   using C = WsCfg<CPLX, V>;
   using T = typename LY::T;
@@ -286,19 +279,15 @@ cudaError_t launch_update_ws_v(UpdateArgs a, cudaStream_t s) {
   using C = WsCfg<CPLX, V>;
   using LY = WsLayoutT<CPLX, BNMAJ, V>;
   if (a.rows <= 0 || a.cols <= 0 || a.K <= 0) return cudaSuccess;
-  constexpr int CPS = (C::BM == C::BN) ? 1 : 2;  // CTAs per SM (rectangular tiles: 2)
-  if (C::BM != C::BN) a.tri = 0;                 // rectangular tiles: rectangular enumeration, masked
+  constexpr int CPS = 1;  // CTAs per SM
   a.tiles_m = (a.rows + C::BM - 1) / C::BM;
   if (a.bcc_P == 0) a.tiles_n = (a.cols + C::BN - 1) / C::BN;
   const long long per = a.tri ? (long long)a.tiles_m * (a.tiles_m + 1) / 2 : (long long)a.tiles_m * a.tiles_n;
   const long long total = per * a.batch;
   if (total <= 0) return cudaSuccess;
-  // persistent CTAs, each walking <= TPC tiles, at least one wave of the SMs
-  static long long TPC = 0;
-  if (TPC == 0) {  // tiles per CTA (experiments: DPP_WS_TPC); 4 keeps CTAs short-lived
-    const char* e = getenv("DPP_WS_TPC");
-    TPC = (e && atoi(e) > 0) ? atoi(e) : 4;
-  }
+  // short-lived CTAs walk <= TPC = 4 tiles each (at least one wave of the SMs), so the high-priority
+  // lookahead stream still finds SMs between tiles; persistent launches take the CTAs granted
+  constexpr long long TPC = 4;
   long long g;
   if (a.grid_limit > 0) {
     const long long lim = (long long)a.grid_limit * CPS;
@@ -314,41 +303,13 @@ cudaError_t launch_update_ws_v(UpdateArgs a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// real kernels: warp-layout variant V (1, default: 16 consumer warps of 32x32 -- 85.9% tensor-active
-// vs 81.6% for 0: 8 consumer warps of 64x32 at the 168-register cap), DPP_WS_VARIANT=0 selects 0
-static int ws_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DPP_WS_VARIANT");
-    v = (e && e[0] == '0') ? 0 : (e && e[0] == '2') ? 2 : 1;
-  }
-  return v;
-}
-
-// DPP_WS_SMALL=1: small non-persistent launches (the chain's panel GEMM and lookahead column: at
-// most one 128 x 128 tile per free SM) take the 64 x 128 tiles of variant 2 -- such a launch runs
-// in one wave, so its duration is one tile's latency.  Off by default: measured neutral at C4
-// (26.62 / 26.76 vs 26.61 / 26.61 TF/s, panel stage 78.4 vs 78.6 ms per 5 samples) -- the
-// per-launch fixed costs (launch, C-tile load, ring fill, store) dominate a one-tile launch.
-static bool ws_small_tiles(const UpdateArgs& a) {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DPP_WS_SMALL");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  if (!v || a.grid_limit > 0 || a.bcc_P != 0) return false;
-  const long long tm = (a.rows + 127) / 128, tn = (a.cols + 127) / 128;
-  return tm * tn * a.batch <= num_sms() / 2;
-}
-
+// Real kernels: 128 x 128 tiles, 16 consumer warps of 32 x 32 (96 registers; 85.9 % tensor-active
+// against 81.6 % for 8 consumer warps of 64 x 32 at the 168-register cap, and faster than 64 x 128
+// tiles with two CTAs per SM, which double the operand traffic per flop -- round-1 measurements,
+// DESIGN.md §6).  Complex kernels: 64 x 64 tiles, 8 consumer warps of 32 x 16.
 template <bool CPLX, bool BNMAJ, bool MASK, bool SCALE, bool CONJ>
 cudaError_t launch_update_ws_t(UpdateArgs a, cudaStream_t s) {
-  if constexpr (!CPLX) {
-    if (ws_variant() == 1 && ws_small_tiles(a)) return launch_update_ws_v<CPLX, BNMAJ, MASK, SCALE, CONJ, 2>(a, s);
-    if (ws_variant() == 1) return launch_update_ws_v<CPLX, BNMAJ, MASK, SCALE, CONJ, 1>(a, s);
-    if (ws_variant() == 2) return launch_update_ws_v<CPLX, BNMAJ, MASK, SCALE, CONJ, 2>(a, s);
-  }
-  return launch_update_ws_v<CPLX, BNMAJ, MASK, SCALE, CONJ, 0>(a, s);
+  return launch_update_ws_v<CPLX, BNMAJ, MASK, SCALE, CONJ, CPLX ? 0 : 1>(a, s);
 }
 
 template cudaError_t launch_update_ws_t<false, false, true, true, false>(UpdateArgs, cudaStream_t);

@@ -55,14 +55,42 @@ def from_local(locals_: list, n: int, nb: int, world: int, like: torch.Tensor) -
 
 
 def message_bytes(n: int, nb: int, k: int, elem_bytes: int = 8) -> int:
-    """Bytes broadcast at block step k (mirrors csrc/dist.cu: header + L21 of the trailing rows;
-    elem_bytes 8 for real, 16 for complex Hermitian kernels)."""
-    ldw = max(((n + 15) // 16) * 16, 16)
+    """Bytes broadcast at block step k with P > 1 (mirrors csrc/dist.cu and
+    dpp_dist_message_bytes: a 256-byte-aligned header [state 64 B | D1 | decisions] + L21 of the
+    LIVE rows m2 = n - j1 at pitch round_up(m2, 16); elem_bytes 8 real, 16 complex Hermitian)."""
     header = 64 + 8 * nb + nb
     header = (header + 255) // 256 * 256
     j1 = min(n, (k + 1) * nb)
     jb = min(nb, n - k * nb)
-    return header + (ldw * jb * elem_bytes if n - j1 > 0 else 0)
+    m2 = n - j1
+    pitch = max(((m2 + 15) // 16) * 16, 16)
+    return header + (pitch * jb * elem_bytes if m2 > 0 else 0)
+
+
+def sample_local(locals_: list, n: int, seed: int, complex_: bool = False, opts=None, stream=None):
+    """One sample with the block columns spread over len(locals_) VIRTUAL ranks on the current
+    device (dpp_comm_init_local + dpp_sample_herm_{d,z}_dist_local): locals_[r] is rank r's local
+    storage (ncols_local, ld_local).  Returns {"masks": [P x n uint8], "loglik": [P], "info": [P x 32
+    bytes]} -- every virtual rank's copy of the result."""
+    from . import (DPP_OP_HERM_D, DPP_OP_HERM_Z, INFO_BYTES, dpp_comm_destroy, dpp_comm_init_local,
+                   dpp_dist_workspace_bytes, dpp_sample_herm_d_dist_local, dpp_sample_herm_z_dist_local)
+    P = len(locals_)
+    dev = locals_[0].device
+    op = DPP_OP_HERM_Z if complex_ else DPP_OP_HERM_D
+    wb = dpp_dist_workspace_bytes(op, n, P, opts)
+    works = [torch.empty(max(wb, 256), dtype=torch.uint8, device=dev) for _ in range(P)]
+    masks = torch.empty((P, max(n, 1)), dtype=torch.uint8, device=dev)
+    ll = torch.empty(P, dtype=torch.float64, device=dev)
+    info = torch.empty((P, INFO_BYTES), dtype=torch.uint8, device=dev)
+    comm = dpp_comm_init_local(P)
+    try:
+        fn = dpp_sample_herm_z_dist_local if complex_ else dpp_sample_herm_d_dist_local
+        fn(comm, n, locals_, locals_[0].shape[1], seed, [masks[r] for r in range(P)], ll, info, opts, works,
+           work_bytes=wb, stream=stream)
+        torch.cuda.synchronize(dev)
+    finally:
+        dpp_comm_destroy(comm)
+    return {"masks": masks[:, :n], "loglik": ll, "info": info}
 
 
 class DistComm:

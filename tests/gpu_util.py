@@ -53,3 +53,20 @@ def assert_factor_close(Fg: np.ndarray, Fo: np.ndarray, K: np.ndarray, kind: str
 
 def assert_loglik_close(lg: float, lo: float):
     assert abs(lg - lo) <= LOGLIK_TOL * abs(lo) + 1e-12, f"loglik {lg!r} vs oracle {lo!r}"
+
+
+def check_decisions(mask: np.ndarray, pivots: np.ndarray, seed: int, b: int, oracle_mod, tie_tol: float = 1e-9):
+    """Every decision of a sample of ANY size against the oracle's uniforms (Listing 1 decision,
+    PAPER.md:435-440): the pre-decision pivot is recovered from the returned factor as
+    p_j = Re(final pivot_j) + (1 - mask_j) (the sampler subtracts 1 exactly when it drops j), u_j is
+    recomputed with the ORACLE's Philox, and mask_j == (u_j <= p_j) must hold wherever
+    |u_j - p_j| > tie_tol.  Returns the number of ties (pivots within tie_tol).  Together with a
+    factor residual check (L D L^H = K - 1_{Y^c}) this pins the whole sample, not only a prefix."""
+    mask = np.asarray(mask).astype(np.int64)
+    p = np.asarray(pivots).real.astype(np.float64) + (1 - mask)
+    u = np.array([oracle_mod.uniform(seed, j, b) for j in range(len(mask))])
+    tie = np.abs(u - p) <= tie_tol
+    want = (u <= p).astype(np.int64)
+    bad = np.flatnonzero((want != mask) & ~tie)
+    assert bad.size == 0, f"decisions inconsistent with the oracle's uniforms at {bad[:10]}"
+    return int(tie.sum())

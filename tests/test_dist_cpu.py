@@ -8,7 +8,8 @@
   broadcasts [D1 | decisions | running loglik | L21] (here over gloo), every rank updates its own
   trailing block columns, in the lookahead order of csrc/dist.cu -- reproduces the oracle's sample
   and factor for real and complex Hermitian kernels.  (The CUDA kernels of that
-  schedule are covered on the GPU by tests/test_gpu_dist.py at world size 1.)
+  schedule are covered on the GPU by tests/test_gpu_dist.py: world size 1 over NCCL and P = 2, 3, 4
+  virtual ranks with the in-process transport, which runs the same per-step code.)
 """
 import os
 import socket
@@ -41,8 +42,10 @@ def _emulate(K, n, nb, world, rank, seed, oracle_mod):
     mask = np.zeros(n, dtype=np.uint8)
     ll = [0.0]
     nblk = (n + nb - 1) // nb
-    ldw = max(((n + 15) // 16) * 16, 16)
     msgs = {}
+
+    def pitch(m2):  # the message's L21 pitch: the live rows, 16-aligned (csrc/dist.cu msg_pitch)
+        return max(((m2 + 15) // 16) * 16, 16)
 
     def span(k):
         j0, j1 = k * nb, min(n, (k + 1) * nb)
@@ -68,14 +71,14 @@ def _emulate(K, n, nb, world, rank, seed, oracle_mod):
         A21 = loc[j1:, q:q + jb]
         W21 = np.linalg.solve(L11, A21.conj().T).conj().T if m2 else np.zeros((0, jb))  # A21 L11^{-H}
         loc[j1:, q:q + jb] = W21 / Dg[None, :]                                         # L21
-        buf = np.zeros((ldw, jb), dtype=loc.dtype)
+        buf = np.zeros((pitch(m2), jb), dtype=loc.dtype)
         buf[:m2] = loc[j1:, q:q + jb]
         return [ll[0], Dg, mask[j0:j1].copy(), buf]
 
     def exchange(k):  # ncclBroadcast(message k, root = owner(k)) -- here over gloo
         j0, j1, jb, m2 = span(k)
         owner = D.owner_of_block(k, world)
-        body = np.zeros(ldw * jb, dtype=loc.dtype)
+        ldw = pitch(m2)
         msg = torch.zeros(2 + 2 * jb + (2 if cplx else 1) * ldw * jb, dtype=torch.float64)
         if rank == owner:
             lk, Dg, mk, buf = msgs[k]
@@ -166,6 +169,14 @@ def _worker(rank, world, port, results):
         out["roundtrip_ok"] = bool(torch.equal(D.from_local(locs, n, nb, world, Kc), Kc))
         out["msg0"] = D.message_bytes(16384, 128, 0)
         out["msg0z"] = D.message_bytes(32768, 64, 0, elem_bytes=16)
+        # the Python mirror equals the library's dpp_dist_message_bytes at every step
+        out["msg_mirror_ok"] = all(
+            D.message_bytes(n_, nb_, k, es) == dpp.dpp_dist_message_bytes(op, n_, 2, k)
+            for n_, nb_, es, op in ((1000, 128, 8, dpp.DPP_OP_HERM_D), (65536, 128, 8, dpp.DPP_OP_HERM_D),
+                                    (777, 64, 16, dpp.DPP_OP_HERM_Z))
+            for k in range((n_ + nb_ - 1) // nb_))
+        # per receiver over a whole n = 65536 sample: ~ 4 n^2 bytes (the live rows only)
+        out["msg_total_65536"] = sum(D.message_bytes(65536, 128, k) for k in range(512))
         results[rank] = out
     finally:
         dist.destroy_process_group()
@@ -184,6 +195,9 @@ def test_two_rank_gloo_host_logic():
             assert res["mask_ok_" + tag], res
             assert res["factor_err_" + tag] < 1e-10, res
             assert res["ll_err_" + tag] < 1e-12, res
-        # header (64 B state + 128 pivots + 128 decision bytes, 256-aligned) + W21 (ldw x nb)
-        assert res["msg0"] == 1280 + 16384 * 128 * 8, res
-        assert res["msg0z"] == 768 + 32768 * 64 * 16, res
+        # header (64 B state + 128 pivots + 128 decision bytes, 256-aligned) + L21 of the live rows
+        # (m2 = n - nb, pitch round_up(m2, 16))
+        assert res["msg0"] == 1280 + 16256 * 128 * 8, res
+        assert res["msg0z"] == 768 + 32704 * 64 * 16, res
+        assert res["msg_mirror_ok"], res
+        assert abs(res["msg_total_65536"] / (4 * 65536 ** 2) - 1) < 0.01, res

@@ -40,6 +40,15 @@ def _gpu_single(kind, K, seed, opts=None, ld=None):
     return s, from_device(Kc, n), Kc
 
 
+def _assert_info_pivots(info, o, K):
+    """min_j |final pivot_j| and (LU) max_j |Im p_j| agree with the oracle's within the factor
+    tolerance (the pivots are factor entries: R16)."""
+    scale = float(np.max(np.abs(K))) if np.size(K) else 1.0
+    assert abs(info["min_abs_pivot"] - o.min_abs_pivot) <= 1e-9 * scale, (info["min_abs_pivot"], o.min_abs_pivot)
+    assert abs(info["max_abs_imag_pivot"] - o.max_abs_imag_pivot) <= 1e-9 * scale, (
+        info["max_abs_imag_pivot"], o.max_abs_imag_pivot)
+
+
 def test_philox_matches_oracle_and_curand(oracle_mod):
     from tests.philox_tool import curand_philox
     for seed, j0, b in [(0, 0, 0), (123456789, 1000, 7), (2**63 + 11, 2**33, 2**40 + 1)]:
@@ -73,6 +82,7 @@ def test_single_sample_parity(oracle_mod, kind, n, nb, la):
         assert_loglik_close(float(s.loglik), o.loglik)
         assert info["n_kept"] == o.n_kept
         assert info["n_out_of_range"] == o.n_out_of_range
+        _assert_info_pivots(info, o, K)
     if kind != "lu_z":  # strict upper triangle never touched
         iu = np.triu_indices(n, 1)
         assert np.array_equal(F[iu], np.asarray(K)[iu])
@@ -237,138 +247,88 @@ def test_large_parity_2048(oracle_mod):
         assert_loglik_close(float(s.loglik), o.loglik)
 
 
-@pytest.mark.parametrize("env", [{"DPP_UPDATE_GENERIC": "1"}, {"DPP_WS_VARIANT": "0"}, {"DPP_WS_VARIANT": "2"},
-                                 {"DPP_WS_SMALL": "1"}, {"DPP_FUSE_W": "0"}, {"DPP_HEAD_BLOCK": "0"},
-                                 {"DPP_DIAG_NT": "512"},
-                                 {"DPP_DIAG_BLOCKED": "1"}, {"DPP_PAIR": "0"}, {"DPP_TAIL_ROWS": "200"},
-                                 {"DPP_PAIR_MIN_ROWS": "0"}])
-def test_alternate_update_kernels_subprocess(env):
-    """The cp.async fallback update kernel (DPP_UPDATE_GENERIC=1), the 8-consumer-warp layout of
-    the warp-specialized kernel (DPP_WS_VARIANT=0), its 64 x 128-tile layout for every launch
-    (DPP_WS_VARIANT=2) or for the small chain launches only (DPP_WS_SMALL=1), the pre-scaled panel
-    copy W21 by a separate column-scaling pass instead of the panel kernel (DPP_FUSE_W=0), the
-    ragged block last instead of first (DPP_HEAD_BLOCK=0), the 512-thread
-    register-tile diag kernel
-    (DPP_DIAG_NT=512), the 32-column-blocked Hermitian diag kernel (DPP_DIAG_BLOCKED=1) and the
-    unpaired trailing updates (DPP_PAIR=0: one K = nb update per step) give the same
-    samples and factors as the oracle for all three kinds (each run in a fresh process)."""
-    import os
-    import subprocess
-    import sys
-    code = r'''
-import numpy as np, torch, oracle, workloads as W, paper_1905_00165_b200 as dpp
-from tests.gpu_util import to_device, from_device, compare_masks, assert_factor_close, assert_loglik_close
-for kind, n in (("herm_d", 333), ("herm_z", 201), ("lu_z", 150)):
-    K = W.haar_kernel(n, seed=7, complex_=(kind != "herm_d"))
-    if kind == "lu_z":
-        K = W.similarity(K, seed=7)
-    o = {"herm_d": oracle.sample_herm_d, "herm_z": oracle.sample_herm_z, "lu_z": oracle.sample_lu_z}[kind](K, 3, 0)
-    Kc = to_device(K, kind)
-    s = dpp.sample(kind, Kc, 3)
-    torch.cuda.synchronize()
+# Schedules and kernels selected through dpp_opts_t (the library reads no environment): the
+# cp.async fallback update kernel for every GEMM, unpaired trailing updates (G = 1), the default
+# pairing G = 2 engaged at every size (group_min_rows < 0; by default it starts only above 6144
+# trailing rows for real 128-blocks, 8192 for LU), G = 3 and 4, and nb wider than the tile
+# (256 real; 128 complex), which runs as grouped 128- (64-) wide sub-blocks.
+OPT_CASES = {
+    "generic": dict(flags=1),
+    "unpaired": dict(group=1),
+    "pair_all_sizes": dict(group=2, group_min_rows=-1),
+    "group3": dict(group=3, group_min_rows=-1),
+    "group4": dict(group=4, group_min_rows=-1),
+    "nb_wide": dict(nb=-1),
+}
+
+
+@pytest.mark.parametrize("case", list(OPT_CASES))
+@pytest.mark.parametrize("kind,n", [("herm_d", 2125), ("herm_d", 1130), ("herm_z", 555), ("lu_z", 480)])
+def test_schedule_options_parity(oracle_mod, case, kind, n):
+    """Each option gives the oracle's sample element by element (decisions, factor, loglik, info),
+    in place and batched, at sizes where several groups form and a ragged tail stays ungrouped
+    (1130: an even remainder, so the head block is taken)."""
+    kw = dict(OPT_CASES[case])
+    if kw.get("nb") == -1:
+        kw["nb"] = 256 if kind == "herm_d" else 128
+    opts = dpp.make_opts(**kw)
+    K = _kernel(kind, n, seed=n)
+    o = _oracle(oracle_mod, kind, K, 5)
+    s, F, _ = _gpu_single(kind, K, 5, opts)
     compare_masks(s.mask.cpu().numpy(), o)
+    info = s.info_dicts()[0]
+    assert info["n_ties"] == o.n_ties
     if o.n_ties == 0:
-        assert_factor_close(from_device(Kc, n), o.factor, K, kind)
+        assert_factor_close(F, o.factor, K, kind)
         assert_loglik_close(float(s.loglik), o.loglik)
-print("GENERIC_OK")
-'''
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PYTHONPATH=root, **env)
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
-    assert "GENERIC_OK" in r.stdout, r.stdout + r.stderr
+        _assert_info_pivots(info, o, K)
+    if n < 1500:  # batched: samples b0 .. b0 + 2 of the same (read-only) kernel
+        sb = dpp.sample_batched(kind, to_device(K, kind), 3, seed=5, b0=1, opts=opts)
+        torch.cuda.synchronize()
+        for b in range(3):
+            ob = _oracle(oracle_mod, kind, K, 5, 1 + b)
+            compare_masks(sb.mask[b].cpu().numpy(), ob)
+            if ob.n_ties == 0:
+                assert_loglik_close(float(sb.loglik[b]), ob.loglik)
 
 
-@pytest.mark.parametrize("group", ["3", "4"])
-def test_grouped_trailing_updates_subprocess(group):
-    """Trailing updates grouped by G = 3 and 4 steps (DPP_GROUP; one K = G nb pass applied by the
-    group's last step, the lookahead update of the middle steps with K = (i+1) nb) give the
-    oracle's samples and factors for all three kinds, single and batched, at sizes where several
-    groups form and a ragged tail stays ungrouped (each run in a fresh process)."""
-    import os
-    import subprocess
-    import sys
-    code = r'''
-import numpy as np, torch, oracle, workloads as W, paper_1905_00165_b200 as dpp
-from tests.gpu_util import to_device, from_device, compare_masks, assert_factor_close, assert_loglik_close
-for kind, n in (("herm_d", 1111), ("herm_d", 1130), ("herm_z", 555), ("lu_z", 480)):
-    # (1130: an even remainder, so the head block is taken -- on the aligned batched copies too)
-    K = W.haar_kernel(n, seed=n, complex_=(kind != "herm_d"))
-    if kind == "lu_z":
-        K = W.similarity(K, seed=n)
-    fn = {"herm_d": oracle.sample_herm_d, "herm_z": oracle.sample_herm_z, "lu_z": oracle.sample_lu_z}[kind]
-    o = fn(K, 5, 0)
-    Kc = to_device(K, kind)
-    s = dpp.sample(kind, Kc, 5)
-    torch.cuda.synchronize()
-    compare_masks(s.mask.cpu().numpy(), o)
-    if o.n_ties == 0:
-        assert_factor_close(from_device(Kc, n), o.factor, K, kind)
-        assert_loglik_close(float(s.loglik), o.loglik)
-    # batched: samples b0 .. b0 + 2 of the same kernel
-    Kb = to_device(K, kind)
-    sb = dpp.sample_batched(kind, Kb, 3, seed=5, b0=1)
-    torch.cuda.synchronize()
-    for b in range(3):
-        ob = fn(K, 5, 1 + b)
-        compare_masks(sb.mask[b].cpu().numpy(), ob)
-        if ob.n_ties == 0:
-            assert_loglik_close(float(sb.loglik[b]), ob.loglik)
-print("GROUP_OK")
-'''
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PYTHONPATH=root, DPP_GROUP=group, DPP_PAIR_MIN_ROWS="0")
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
-    assert "GROUP_OK" in r.stdout, r.stdout + r.stderr
-
-
-def test_column_chunked_schedule_subprocess():
-    """The column-chunked schedule (DPP_CHUNK_COLS=256: right-looking inside 256-column chunks, a
-    K = c0 catch-up GEMM per chunk, and for the _host entry point the copy pipelined chunk by chunk
-    on its own stream) gives the oracle's samples and factors -- in place, batched and host
-    entry points, real and complex Hermitian (run in a fresh process)."""
-    import os
-    import subprocess
-    import sys
-    code = r'''
-import numpy as np, torch, oracle, workloads as W, paper_1905_00165_b200 as dpp
-from tests.gpu_util import to_device, from_device, compare_masks, assert_factor_close, assert_loglik_close
-for kind, n in (("herm_d", 1000), ("herm_d", 1311), ("herm_z", 700)):
-    K = W.haar_kernel(n, seed=n, complex_=(kind != "herm_d"))
-    fn = oracle.sample_herm_d if kind == "herm_d" else oracle.sample_herm_z
-    o = fn(K, 9, 0)
-    Kc = to_device(K, kind)
-    s = dpp.sample(kind, Kc, 9)
-    torch.cuda.synchronize()
-    compare_masks(s.mask.cpu().numpy(), o)
-    if o.n_ties == 0:
-        assert_factor_close(from_device(Kc, n), o.factor, K, kind)
-        assert_loglik_close(float(s.loglik), o.loglik)
-    sb = dpp.sample_batched(kind, to_device(K, kind), 2, seed=9, b0=0)
-    compare_masks(sb.mask[0].cpu().numpy(), o)
-    if kind == "herm_d":
-        Kh = torch.from_numpy(np.ascontiguousarray(K.T)).pin_memory()
-        mh = torch.empty((1, n), dtype=torch.uint8).pin_memory()
-        lh = torch.empty(1, dtype=torch.float64).pin_memory()
-        op = dpp.DPP_OP_HERM_D | dpp.DPP_OP_HOST
-        work = torch.empty(dpp.dpp_workspace_bytes(op, 1, n), dtype=torch.uint8, device="cuda")
-        dpp.dpp_sample_herm_d_host(1, n, Kh, n, 0, 9, 0, mh, lh, None, None, work)
-        compare_masks(mh[0].numpy(), o)
-        if o.n_ties == 0:
-            assert_loglik_close(float(lh[0]), o.loglik)
-print("CHUNK_OK")
-'''
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PYTHONPATH=root, DPP_CHUNK_COLS="256")
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
-    assert "CHUNK_OK" in r.stdout, r.stdout + r.stderr
+def test_many_caller_streams_bitwise():
+    """More caller streams (6) than the library's pool of stream pairs (4): batched and in-place
+    calls rotated over them with separate workspaces give bit for bit the serial results (masks,
+    loglik, factors) -- the pair reassignment keeps every call stream-ordered."""
+    ns = 6
+    for kind, n in (("herm_d", 700), ("lu_z", 300)):
+        K = _kernel(kind, n, seed=31)
+        Kd = to_device(K, kind)
+        ref = []
+        for i in range(ns):
+            sb = dpp.sample_batched(kind, Kd, 1, seed=3, b0=i)
+            Kc = to_device(K, kind)
+            si = dpp.sample(kind, Kc, 3 + i)
+            torch.cuda.synchronize()
+            ref.append((sb.mask.clone(), sb.loglik.clone(), si.mask.clone(), si.loglik.clone(), Kc.clone()))
+        strs = [torch.cuda.Stream() for _ in range(ns)]
+        outs = []
+        for rep in range(2):
+            for i in range(ns):
+                with torch.cuda.stream(strs[i]):
+                    sb = dpp.sample_batched(kind, Kd, 1, seed=3, b0=i, stream=strs[i])
+                    Kc = to_device(K, kind)
+                    si = dpp.sample(kind, Kc, 3 + i, stream=strs[i])
+                outs.append((i, sb, si, Kc))
+        torch.cuda.synchronize()
+        for i, sb, si, Kc in outs:
+            r = ref[i]
+            assert torch.equal(sb.mask, r[0]) and torch.equal(sb.loglik, r[1]), (kind, i)
+            assert torch.equal(si.mask, r[2]) and torch.equal(si.loglik, r[3]), (kind, i)
+            assert torch.equal(Kc, r[4]), (kind, i)
 
 
 @pytest.mark.parametrize("n", [4500, 8192])
 def test_host_equals_device_path(oracle_mod, n):
-    """The _host entry point (with DPP_COPY_GATED=1 in the environment: its copy pipelined, the
-    trailing updates of the first steps launched per arrived column chunk) sees the same operations
-    per element as the device path, so mask and loglik equal the batched call's bit for bit; the
-    leading block also matches the oracle (prefix property)."""
+    """The _host entry point sees the same operations per element as the device path, so mask and
+    loglik equal the batched call's bit for bit; the leading block also matches the oracle (prefix
+    property)."""
     Kc = W.haar_kernel_torch(n, seed=3, spectrum="beta")
     sb = dpp.sample_batched("herm_d", Kc, 1, seed=4, b0=0)
     Kh = Kc.cpu().pin_memory()
@@ -382,17 +342,3 @@ def test_host_equals_device_path(oracle_mod, n):
     m = 600
     o = oracle_mod.sample_herm_d(Kc[:m, :m].cpu().numpy().T.copy(), 4, 0)
     compare_masks(mh[0].numpy()[:m], o)
-
-
-def test_host_copy_gated_subprocess():
-    """The copy-gated _host schedule (DPP_COPY_GATED=1) equals the device path bit for bit."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PYTHONPATH=root, DPP_COPY_GATED="1", DPP_PAIR="0",
-               DPP_HEAD_BLOCK="0")  # same blocking and update grouping on both paths
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-k", "test_host_equals_device_path",
-                        os.path.join(root, "tests", "test_gpu_parity.py")], cwd=root, env=env, capture_output=True,
-                       text=True, timeout=900)
-    assert r.returncode == 0, r.stdout + r.stderr

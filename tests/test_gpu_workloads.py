@@ -16,7 +16,7 @@ import numpy as np
 import pytest
 
 import workloads as W
-from tests.gpu_util import (assert_factor_close, assert_loglik_close, compare_masks, from_device,
+from tests.gpu_util import (assert_factor_close, assert_loglik_close, check_decisions, compare_masks, from_device,
                             to_device)
 from tests.stats_util import (check_marginals, check_subset_frequencies, masks_to_index,
                               subset_probabilities)
@@ -134,6 +134,8 @@ def test_config2_aztec_d80_balanced(oracle_mod):
     assert round(ll, 1) == GOLD["aztec_d80_loglik"]["value"]
     info = s.info_dicts()[0]
     assert info["n_kept"] == 6480 and info["n_ties"] == 0
+    # every one of the 25600 decisions against the oracle's uniforms (LU pivot = U_jj)
+    check_decisions(mask, torch.diagonal(Kc).cpu().numpy(), 0, 0, oracle_mod)
     o = oracle_mod.sample_lu_z(Kpre, 0, 0)
     compare_masks(mask[:m], o)
     if o.n_ties == 0:
@@ -163,6 +165,8 @@ def test_config3_n16384_prefix_parity(oracle_mod):
     D = torch.diagonal(Kc)
     assert abs(float(torch.log(D.abs()).sum()) - float(s.loglik)) <= 1e-10 * abs(float(s.loglik))
     assert 0.4 * n < int(s.mask.sum()) < 0.6 * n
+    # every one of the 16384 decisions against the oracle's uniforms (not only the prefix)
+    check_decisions(mask, D.cpu().numpy(), 0, 0, oracle_mod)
     # randomized factor check on the GPU: (L D L^T) x vs (K - 1_{Y^c}) x
     Lt = torch.tril(Kc.T, -1) + torch.eye(n, dtype=torch.float64, device="cuda")  # natural L
     Kn = torch.tril(K0.T) + torch.tril(K0.T, -1).T
