@@ -145,7 +145,8 @@ def main():
                     help="c4: caller streams the consecutive steps alternate between")
     ap.add_argument("--prof", choices=["trailing", "all"], default="trailing",
                     help="c4: stages bracketed by events inside the timed region")
-    ap.add_argument("--workload", default="c4", choices=["c4", "ust", "dist", "dist_z", "herm_z", "lu_z", "aztec", "herm_s", "aztec_c", "elementary", "lensemble"],
+    ap.add_argument("--workload", default="c4", choices=["c4", "ust", "dist", "dist_z", "herm_z", "lu_z", "aztec", "herm_s", "aztec_c", "elementary", "lensemble",
+                             "crossover"],
                     help="c4 (default, BASELINE configs[3]); ust: configs[1] batch of UST samples per GPU; "
                          "dist / dist_z: configs[4] 1D block-column-cyclic single sample over all ranks (real n=65536 / "
                          "complex n=32768); "
@@ -153,7 +154,8 @@ def main():
                          "complex paths); aztec: configs[2], order-80 Aztec diamond LU sampler; herm_s / aztec_c: the "
                          "single-precision samplers (n=16384 real; order-80 Aztec consistency, PAPER.md:1164-1169); "
                          "elementary: Listing 2 on a rank-k projection, n=5000 (the paper's Fig. setting); lensemble: "
-                         "K = I - (L+I)^{-1} at n=16384")
+                         "K = I - (L+I)^{-1} at n=16384; crossover: elementary (Listing 2) vs generic sampler on "
+                         "the same n=5000 rank-k projections, k = 10..4000 (PAPER.md:1490-1493)")
     ap.add_argument("--batch", type=int, default=1024, help="ust: samples per GPU per step")
     ap.add_argument("--batch-chunk", type=int, default=1024, help="ust: samples factored concurrently")
     ap.add_argument("--aztec-d", type=int, default=80, help="aztec_c: diamond order")
@@ -161,6 +163,7 @@ def main():
     ap.add_argument("--rank", type=int, default=500, help="elementary: projection rank k")
     ap.add_argument("--lookahead", type=int, default=1, help="ust: 0 = single stream")
     ap.add_argument("--nb", type=int, default=128, help="ust: block size")
+    ap.add_argument("--group", type=int, default=0, help="ust: dpp_opts_t.group (0 = library default)")
     ap.add_argument("--no-dist", action="store_true", help="c4: skip the configs[4] block-cyclic sub-record")
     ap.add_argument("--dist-n", type=int, default=65536, help="c4: n of the block-cyclic sub-record")
     ap.add_argument("--dist-steps", type=int, default=2, help="c4: timed samples of the block-cyclic sub-record")
@@ -554,14 +557,15 @@ def dist_record(args, world, rank, dist):
 
 
 def _traffic():
-    """DRAM bytes per launch of the trailing-update kernel from the committed ncu capture
-    (profiles/r01h_update_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum averaged over
-    the trailing-update launches of one n=16384 sample); None if absent."""
+    """DRAM bytes of the roofline's probe launch (the largest trailing-update launch of one C4
+    sample) from the committed ncu capture (profiles/r02/probe_traffic.json: dram__bytes_read.sum +
+    dram__bytes_write.sum of that launch); None if absent."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r01h_update_traffic.json")))
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02", "probe_traffic.json")))
         return {"bytes_per_launch": int(d["measured_bytes_per_launch"]),
+                "algorithmic_bytes_per_launch": int(d["algorithmic_bytes_per_launch"]),
                 "measured_over_algorithmic": d["ratio_measured_over_algorithmic"],
-                "source": "profiles/r01h_update_traffic.json (ncu)"}
+                "source": "profiles/r02/probe_traffic.json (ncu)"}
     except Exception:
         return None
 
@@ -639,7 +643,8 @@ def extra_workload(args):
         K = W.ust_kernel(40, 40)
         Kc = torch.from_numpy(np.ascontiguousarray(K.T)).cuda()
         B = args.batch
-        opts = dpp.make_opts(nb=args.nb, lookahead=args.lookahead, batch_chunk=min(B, args.batch_chunk))
+        opts = dpp.make_opts(nb=args.nb, lookahead=args.lookahead, batch_chunk=min(B, args.batch_chunk),
+                             group=args.group)
         op = dpp.DPP_OP_HERM_D | dpp.DPP_OP_BATCHED
         NSU = args.ust_streams  # consecutive steps rotate over this many streams (batches in flight)
         works = [torch.empty(dpp.dpp_workspace_bytes(op, B, n, opts), dtype=torch.uint8, device="cuda")
@@ -653,7 +658,10 @@ def extra_workload(args):
             k = i % NSU
             dpp.dpp_sample_herm_d_batched(B, n, Kc, n, 0, SEED, b0, masks[k], lls[k], None, opts, works[k],
                                           stream=ustreams[k])
-        ms, clocks = _timed(step, args.steps, args.warmup, world, dist, streams=ustreams[1:])
+        ms, clocks = _timed(step, args.steps, args.warmup, world, dist,
+                            0x1F if args.prof == "all" else 1 << dpp.STAGES.index("update_trailing"),
+                            streams=ustreams[1:])
+        prof = _fill_stages(dpp.dpp_profile_end(), step, args)
         mask = torch.cat(masks)
         ok = bool((mask.sum(dim=1) == 1599).all())
         flops = model_flops(n) * B * args.steps * world
@@ -661,9 +669,12 @@ def extra_workload(args):
                     dtype="f64", samples_per_s=round(B * args.steps * world / (ms / 1e3), 2),
                     config={"workload": f"BASELINE configs[1]: UST of the 40x40 grid (n=3120, rank 1599), {B} "
                                         f"independent samples per GPU per step", "n": n, "global_batch": B * world,
-                            "nb": args.nb, "batch_chunk": min(B, args.batch_chunk), "lookahead": args.lookahead, "seq_len": None,
+                            "nb": args.nb, "group": args.group or 2, "batch_chunk": min(B, args.batch_chunk),
+                            "lookahead": args.lookahead, "seq_len": None,
                             "parallelism": f"dp{world} (independent samples)"},
                     all_samples_are_spanning_trees_with_1599_edges=ok,
+                    stages={k: {"launches": v["launches"], "ms": round(v["ms"], 3), "ms_union": round(v["ms_union"], 3),
+                                "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3)} for k, v in prof.items()},
                     pct_fp64_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), 2), clocks=clocks)
     elif args.workload == "aztec":
         d = 80
@@ -820,6 +831,59 @@ def extra_workload(args):
                               "note": "the per-sample factor (n x k x 8 B) is L2-resident for small k"},
                     gpu_launches=int(args.steps),  # one fused launch per step (batch >= SMs)
                     clocks=clocks)
+    elif args.workload == "crossover":
+        # PAPER.md:1490-1493 (future work there): "at which rank it becomes beneficial to use our
+        # generic sampling approach ... on GPU-accelerated architectures" -- the elementary sampler
+        # (Listing 2, O(n k^2)) against the generic blocked sampler (O(n^3), independent of k) on the
+        # same rank-k projections of order n = 5000 (the paper's Fig. 10 setting)
+        n = args.n if args.n != N else 5000
+        rows = []
+        g = torch.Generator(device="cuda"); g.manual_seed(KSEED)
+        Gm = torch.randn(n, 4000, generator=g, device="cuda", dtype=torch.float64)
+        for k in (10, 50, 100, 250, 500, 1000, 2000, 4000):
+            Q, _ = torch.linalg.qr(Gm[:, :k])
+            Kc = (Q @ Q.T).contiguous()
+            del Q
+            Be = int(min(592, max(148, 592 * (500.0 / k) ** 2)))
+            order = torch.empty((Be, k), dtype=torch.int64, device="cuda")
+            lle = torch.empty(Be, dtype=torch.float64, device="cuda")
+            we = torch.empty(dpp.dpp_elementary_workspace_bytes(Be, n, k), dtype=torch.uint8, device="cuda")
+
+            def estep(i):
+                dpp.dpp_elementary_herm_d(Be, n, k, Kc, n, SEED, i * Be, order, lle, None, we)
+            ms_e, _ = _timed(estep, 2, 1, 1, dist)
+            Bg = 64
+            optg = dpp.make_opts(nb=128, lookahead=1)
+            opg = dpp.DPP_OP_HERM_D | dpp.DPP_OP_BATCHED
+            wg = torch.empty(dpp.dpp_workspace_bytes(opg, Bg, n, optg), dtype=torch.uint8, device="cuda")
+            mg = torch.empty((Bg, n), dtype=torch.uint8, device="cuda")
+            lg_ = torch.empty(Bg, dtype=torch.float64, device="cuda")
+
+            def gstep(i):
+                dpp.dpp_sample_herm_d_batched(Bg, n, Kc, n, 0, SEED, i * Bg, mg, lg_, None, optg, wg)
+            ms_g, _ = _timed(gstep, 2, 1, 1, dist)
+            ok = bool((mg.sum(dim=1) == k).all())  # projection: every sample has exactly k items
+            rows.append({"rank": k, "elementary_samples_per_s": round(2 * Be / (ms_e / 1e3), 2),
+                         "elementary_batch": Be, "generic_samples_per_s": round(2 * Bg / (ms_g / 1e3), 2),
+                         "generic_batch": Bg, "generic_cardinality_ok": ok})
+            del Kc, we, wg, order
+            torch.cuda.empty_cache()
+        cross = None
+        for a_, b_ in zip(rows, rows[1:]):
+            ra = a_["elementary_samples_per_s"] / a_["generic_samples_per_s"]
+            rb = b_["elementary_samples_per_s"] / b_["generic_samples_per_s"]
+            if ra >= 1.0 > rb:  # log-log interpolation of the ratio
+                t = np.log(ra) / (np.log(ra) - np.log(rb))
+                cross = round(float(np.exp(np.log(a_["rank"]) + t * (np.log(b_["rank"]) - np.log(a_["rank"])))), 0)
+        line.update(value=cross, unit="rank", ms_per_step=None, scaling="weak", dtype="f64", higher_is_better=None,
+                    metric="crossover rank: elementary (Listing 2) vs generic sampler, samples/s on the same "
+                           "n=5000 rank-k projections",
+                    config={"workload": f"rank-k projections K = Q Q^T (QR of an n x k Gaussian), n={n}", "n": n,
+                            "seq_len": None, "global_batch": None, "parallelism": "single GPU"},
+                    rows=rows, crossover_rank=cross,
+                    note="above the crossover rank the generic O(n^3) sampler draws more samples/s than the "
+                         "O(n k^2) elementary sampler (PAPER.md:1490-1493); paper, 1 CPU core: elementary "
+                         "3.8k / 115 / 5 samples/s at ranks 10 / 100 / 500 vs generic 1.2 samples/s (Fig. 10)")
     elif args.workload == "lensemble":
         # L-ensemble -> marginal conversion, "3 samples worth of time"
         n = args.n

@@ -283,6 +283,7 @@ int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* const* K_local, int64_
       p.Bop = c.w + W.bm_off; p.ldb = nb;
       p.C = c.K + (size_t)(j1 + tcol * ld_local) * es; p.ldc = ld_local;
       p.a_rows = (int)m2; p.b_rows = jb; p.K = jb; p.rows = (int)m2; p.cols = jb; p.batch = 1; p.vec = vec ? 1 : 0;
+      p.btri = 1;
       CK(launch_update(kind, p, s));
       if (!self_only)
         CK(cudaMemcpy2DAsync(msg + M.w_off, (size_t)msg_pitch(m2) * es, c.K + (size_t)(j1 + tcol * ld_local) * es,

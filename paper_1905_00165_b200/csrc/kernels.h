@@ -67,6 +67,9 @@ struct UpdateArgs {
   int64_t dstride;
   int ktri;             // 1: A(i, k) = 0 for k < i (upper-triangular A): a tile starts its K loop at
                         //    its first row (fast kernel only; the others just multiply the zeros)
+  int btri;             // 1: op(B)(j, k) = 0 for k > j (the stage-2 operators are triangular): a
+                        //    warp's K loop stops at its last column (fast kernel only; the others
+                        //    just multiply the zeros)
   int generic;          // 1: the cp.async fallback kernel even for aligned operands (DPP_FLAG_GENERIC_UPDATE)
   int grid_limit;       // > 0: persistent launch with at most this many CTAs (SMs left to the
                         //      lookahead stream); 0: short-lived CTAs (<= 4 tiles each)

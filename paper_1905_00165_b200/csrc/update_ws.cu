@@ -213,6 +213,9 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
     // keeps pace with the ring (waits and releases every stage) and leaves the DMMA pipe to the others
     const bool idle = MASK && ti.diag && ti.gcol0 + wn * TN > ti.grow0 + wm * TM + TM - 1;
     const int kc0 = a.ktri ? ti.grow0 / C::KC : 0;
+    // triangular B (stage-2 operators): the warp's columns need k <= its last column only; the
+    // chunks past it are waited for and released without DMMA (the ring is shared by all warps)
+    const int kcend = a.btri ? min(nchunks, (ti.gcol0 + wn * TN + TN + C::KC - 1) / C::KC) : nchunks;
     if (idle) {
       for (int kc = kc0; kc < nchunks; ++kc) {
         mbar_wait(&full[stage], phase);
@@ -223,6 +226,12 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
     } else {
       for (int kc = kc0; kc < nchunks; ++kc) {
         mbar_wait(&full[stage], phase);
+        if (kc >= kcend) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          continue;
+        }
         const T* As = ring + stage * LY::STAGE_ELEMS;
         mma_chunk<CPLX, BNMAJ, SCALE, CONJ, C::KC, MI, NI, LY::LDA, LY::LDBK, LY::LDBN>(
             acc, As, As + LY::A_ELEMS, reinterpret_cast<const double*>(As + LY::A_ELEMS + LY::B_ELEMS), wm * TM,
