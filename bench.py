@@ -543,7 +543,8 @@ def dist_record(args, world, rank, dist):
         flops = n ** 3 / 3.0
         msg = sum(D.message_bytes(n, nb, k) for k in range((n + nb - 1) // nb)) if world > 1 else 0
         rec = {"workload": f"BASELINE configs[4]: real K n={n}, lam~U(0,1), ONE sample factored 1D block-column-"
-                           f"cyclic over {world} GPU(s), nb={nb}, depth-1 lookahead, NCCL broadcast per block step",
+                           f"cyclic over {world} GPU(s), nb={nb}, depth-1 lookahead, NCCL broadcast per block step "
+                           f"({'none at one rank' if world == 1 else 'live rows only'})",
                "n": n, "ranks": world, "scaling": "strong", "ms_per_sample": round(ms, 2),
                "value": round(flops / (ms / 1e3) / 1e9, 2), "unit": UNIT,
                "pct_fp64_peak": round(100 * flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), 2),
