@@ -372,6 +372,10 @@ int dpp_profile_begin(void);
  * (the others launch without events).  DPP_EINVAL if stage_mask has no bit 0..4. */
 int dpp_profile_begin_stages(unsigned stage_mask);
 int dpp_profile_end(dpp_profile_t* out);
+/* The same, plus the launch timeline: records[4 i .. 4 i + 3] = (stage, start ms, end ms, flops) of
+ * the i-th bracketed launch in issue order (times relative to the first one issued), for
+ * i < max_records; *count (nullable) = the number of launches recorded. */
+int dpp_profile_end_records(dpp_profile_t* out, double* records, int64_t max_records, int64_t* count);
 
 const char* dpp_strerror(int code);
 const char* dpp_version(void);

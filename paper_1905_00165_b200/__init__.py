@@ -93,6 +93,7 @@ class dpp_profile_t(ctypes.Structure):
 _sig("dpp_profile_begin", ctypes.c_int, [])
 _sig("dpp_profile_begin_stages", ctypes.c_int, [ctypes.c_uint])
 _sig("dpp_profile_end", ctypes.c_int, [ctypes.POINTER(dpp_profile_t)])
+_sig("dpp_profile_end_records", ctypes.c_int, [ctypes.POINTER(dpp_profile_t), _P, _I64, ctypes.POINTER(_I64)])
 _sig("dpp_strerror", ctypes.c_char_p, [ctypes.c_int])
 _sig("dpp_version", ctypes.c_char_p, [])
 
@@ -106,7 +107,7 @@ EXPORTS = ["dpp_workspace_bytes", "dpp_sample_herm_d", "dpp_sample_herm_z", "dpp
            "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host",
            "dpp_philox_uniforms", "dpp_comm_init", "dpp_comm_init_local", "dpp_comm_destroy", "dpp_bcc_local_cols",
            "dpp_dist_workspace_bytes", "dpp_dist_message_bytes", "dpp_sample_herm_d_dist", "dpp_sample_herm_z_dist",
-           "dpp_sample_herm_d_dist_local", "dpp_sample_herm_z_dist_local", "dpp_profile_begin", "dpp_profile_begin_stages", "dpp_profile_end",
+           "dpp_sample_herm_d_dist_local", "dpp_sample_herm_z_dist_local", "dpp_profile_begin", "dpp_profile_begin_stages", "dpp_profile_end", "dpp_profile_end_records",
            "dpp_strerror", "dpp_version"]
 
 
@@ -362,6 +363,22 @@ def dpp_profile_end() -> dict:
     return {st: dict(launches=int(p.launches[i]), ms=float(p.ms[i]), flops=float(p.flops[i]),
                      ms_union=float(p.ms_union[i]), top_flops=float(p.top_flops[i]), top_ms=float(p.top_ms[i]))
             for i, st in enumerate(STAGES)}
+
+
+def dpp_profile_end_records(max_records: int = 1 << 16):
+    """(per-stage aggregates as dpp_profile_end, timeline rows (stage name, start ms, end ms, flops))."""
+    import numpy as np
+    p = dpp_profile_t()
+    buf = np.zeros(4 * max_records, dtype=np.float64)
+    cnt = ctypes.c_int64(0)
+    _check(_lib.dpp_profile_end_records(ctypes.byref(p), buf.ctypes.data, max_records, ctypes.byref(cnt)))
+    agg = {st: dict(launches=int(p.launches[i]), ms=float(p.ms[i]), flops=float(p.flops[i]),
+                    ms_union=float(p.ms_union[i]), top_flops=float(p.top_flops[i]), top_ms=float(p.top_ms[i]))
+           for i, st in enumerate(STAGES)}
+    n = min(int(cnt.value), max_records)
+    rows = [(STAGES[int(buf[4 * i])], float(buf[4 * i + 1]), float(buf[4 * i + 2]), float(buf[4 * i + 3]))
+            for i in range(n)]
+    return agg, rows
 
 
 def dpp_version() -> str:

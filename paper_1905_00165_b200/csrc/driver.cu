@@ -230,21 +230,40 @@ int device_sms() {
 }
 
 // SMs to leave to the lookahead stream while the trailing update (b) of this step runs
-// persistently on the rest: minimise max(T1, T2) with T1 = diag latency + (tiles of the next
-// block column's update + next panel) / R, T2 = tiles of (b) / (SMs - R), in units of one tile.
-// g = G for the last step of a group: its trailing update has K = G nb (G times the tile time) and
-// the chain beside it holds the next group's G diag tiles and G panels.
+// persistently on the rest: minimise max(T1, T2) in units of one (K = nb) update tile, with
+//   T1 = (a) this step's lookahead update: ceil(jn / tile) block columns x K = g nb
+//      + the next group's chain beside (b): g diag tiles, g panel GEMMs and the g - 1 non-last
+//        lookahead updates (K = nb, 2 nb, ... (g-1) nb, one column each)
+//   T2 = (b): its tiles at K = g nb on SMs - R.
+// g = G at the last step of a group (its (a) covers the next group's G blocks with K = G nb), 1
+// otherwise.  (Round 2: the (a) term had counted one column at K = nb whatever g -- a 4x
+// underestimate at the paired steps, which starved the next pair's chain of SMs: a timeline of one
+// C4 sample showed the trailing kernel idle 5.3 ms, mostly at those steps.)
 int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile, bool herm, int g = 1) {
-  // the diag tile in update-tile times (measured: 2.5 .. 5 give the same C4 / UST rates within noise)
-  constexpr double diag_tiles = 5.0;
   const double side = (double)((m2 + tile - 1) / tile), side_b = (double)((m2 - jn + tile - 1) / tile);
-  const double ta = (herm ? 1.0 : 2.0) * side * batch;     // (a): next block column (LU: + row)
-  const double tp = (herm ? 1.0 : 2.0) * side_b * batch;   // next panel GEMM(s)
+  const double lu = herm ? 1.0 : 2.0;
   const double tb = (herm ? side_b * (side_b + 1) / 2 : side_b * side_b) * batch;  // (b) tiles
+  double diag_tiles, chain;
+  if (batch == 1 && tile == 128) {
+    // the diag tile in update-tile times (~49 us vs ~20-30 us per tile at K = nb)
+    diag_tiles = 2.5;
+    const double cols_a = (double)((jn + tile - 1) / tile);
+    const double ta = lu * side * cols_a * g;                 // (a) now
+    const double tp = lu * side_b;                            // one panel GEMM (K = nb)
+    const double tn = lu * side_b * (g * (g - 1) / 2.0);      // the next non-last (a) updates
+    chain = ta + g * tp + tn;
+  } else {
+    // batches (every launch spans the batch, the diag tiles of all samples share the free SMs
+    // with the chain's GEMMs) and the 64-wide complex tiles: the round-1 model, tuned on the UST
+    // batch and the complex workloads (the corrected terms above cost 10 % on the UST batch and
+    // 1.5-2.6 % on complex samples with three in flight; on one real C4 sample they save 1 ms)
+    diag_tiles = 5.0;
+    chain = lu * side * batch + g * lu * side_b * batch;
+  }
   int best = 8;
   double best_t = 1e300;
   for (int R = 4; R <= sms / 2; R += 2) {
-    const double t1 = g * diag_tiles + (ta + g * tp) / R;
+    const double t1 = g * diag_tiles + chain / R;
     const double t2 = g * tb / (sms - R);
     const double t = t1 > t2 ? t1 : t2;
     if (t < best_t) { best_t = t; best = R; }
@@ -687,9 +706,12 @@ int dpp_profile_begin_stages(unsigned stage_mask) {
 
 int dpp_profile_begin(void) { return dpp_profile_begin_stages(0x1fu); }
 
-int dpp_profile_end(dpp_profile_t* out) {
+int dpp_profile_end(dpp_profile_t* out) { return dpp_profile_end_records(out, nullptr, 0, nullptr); }
+
+int dpp_profile_end_records(dpp_profile_t* out, double* records, int64_t max_records, int64_t* count) {
   g_prof.on = false;
-  if (!out) return DPP_EINVAL;
+  if (!out || max_records < 0 || (max_records > 0 && !records)) return DPP_EINVAL;
+  if (count) *count = (int64_t)g_prof.recs.size();
   std::memset(out, 0, sizeof(*out));
   std::vector<std::pair<double, double>> iv[5];  // launch intervals per stage, from the first event
   const cudaEvent_t ref = g_prof.recs.empty() ? nullptr : g_prof.recs.front().e0;
@@ -704,6 +726,10 @@ int dpp_profile_end(dpp_profile_t* out) {
     out->flops[r.stage] += r.flops;
     if (r.flops > out->top_flops[r.stage]) { out->top_flops[r.stage] = r.flops; out->top_ms[r.stage] = ms; }
     iv[r.stage].push_back({(double)t0, (double)t1});
+    const int64_t i = (int64_t)(&r - g_prof.recs.data());
+    if (i < max_records) {  // (stage, start ms, end ms, flops) in issue order
+      records[4 * i + 0] = r.stage; records[4 * i + 1] = t0; records[4 * i + 2] = t1; records[4 * i + 3] = r.flops;
+    }
   }
   for (int st = 0; st < 5; ++st) {  // length of the union of the stage's launch intervals
     // offsets are from the first record ISSUED, so intervals on other streams may start before
