@@ -163,7 +163,7 @@ def main():
     ap.add_argument("--rank", type=int, default=500, help="elementary: projection rank k")
     ap.add_argument("--lookahead", type=int, default=1, help="ust: 0 = single stream")
     ap.add_argument("--nb", type=int, default=128, help="ust: block size")
-    ap.add_argument("--group", type=int, default=0, help="ust: dpp_opts_t.group (0 = library default)")
+    ap.add_argument("--group", type=int, default=0, help="c4 / ust: dpp_opts_t.group (0 = library default)")
     ap.add_argument("--no-dist", action="store_true", help="c4: skip the configs[4] block-cyclic sub-record")
     ap.add_argument("--dist-n", type=int, default=65536, help="c4: n of the block-cyclic sub-record")
     ap.add_argument("--dist-steps", type=int, default=2, help="c4: timed samples of the block-cyclic sub-record")
@@ -207,7 +207,7 @@ def main():
 
     Kc = W.haar_kernel_torch(n, seed=KSEED, spectrum="beta")  # column-major storage (symmetric)
     torch.cuda.synchronize()
-    opts = dpp.make_opts(nb=NB, lookahead=1)
+    opts = dpp.make_opts(nb=NB, lookahead=1, group=args.group)
     op = dpp.DPP_OP_HERM_D | dpp.DPP_OP_BATCHED
     # consecutive steps rotate over three caller streams with three workspaces (--streams 3): the
     # library gives each caller stream its own internal stream pair, so one sample's copy and first
@@ -682,7 +682,7 @@ def extra_workload(args):
         n = 4 * d * d
         Kc = W.aztec_kernel_balanced(d, device="cuda")  # balanced-gauge Kenyon kernel (reading R13)
         torch.cuda.synchronize()
-        opts = dpp.make_opts(nb=64, lookahead=1)
+        opts = dpp.make_opts(nb=64, lookahead=1, group=args.group)
         op = dpp.DPP_OP_LU_Z | dpp.DPP_OP_BATCHED
         NSA = args.aztec_streams  # consecutive samples rotate over this many streams
         works = [torch.empty(dpp.dpp_workspace_bytes(op, 1, n, opts), dtype=torch.uint8, device="cuda")
@@ -922,7 +922,7 @@ def extra_workload(args):
             g = torch.Generator(device="cuda"); g.manual_seed(7)
             dv = torch.exp(torch.rand(n, generator=g, device="cuda", dtype=torch.float64) - 0.5).to(torch.complex128)
             Kc = (Kc * dv[None, :]) / dv[:, None]  # storage (l, i) = K(i, l): K' = D^-1 K D
-        opts = dpp.make_opts(nb=64, lookahead=1)
+        opts = dpp.make_opts(nb=64, lookahead=1, group=args.group)
         op = (dpp.DPP_OP_HERM_Z if args.workload == "herm_z" else dpp.DPP_OP_LU_Z) | dpp.DPP_OP_BATCHED
         NSZ = args.streams  # consecutive samples rotate over this many streams (as the default workload)
         works = [torch.empty(dpp.dpp_workspace_bytes(op, 1, n, opts), dtype=torch.uint8, device="cuda")

@@ -90,8 +90,7 @@ typedef struct {
                             forced + b*n; decision j is forced[j] != 0 */
   int64_t batch_chunk;   /* batched: samples factored concurrently (0 = whole batch) */
   int32_t group;         /* G: the trailing updates of G consecutive block steps are applied as
-                            one K = G nb pass (lookahead on).  0 = default (2; 3 for batched calls
-                            that factor >= 8 samples together), 1 = off, <= 8 */
+                            one K = G nb pass (lookahead on).  0 = default (3), 1 = off, <= 8 */
   uint32_t flags;        /* DPP_FLAG_* */
   int64_t group_min_rows;/* grouping only while more than this many trailing rows remain;
                             0 = the library's defaults (6144 real nb = 128, 8192 LU, 0 otherwise

@@ -39,7 +39,6 @@ struct Opts {
   const uint8_t* forced;
   int64_t batch_chunk;
   int group;             // G: trailing updates of G consecutive steps applied as one K = G nb pass
-  bool group_fixed;      // G given by opts->group or by nb wider than the tile
   int64_t group_min_rows;  // -1: defaults; else group only while more than this many rows remain
   bool generic;          // DPP_FLAG_GENERIC_UPDATE
 };
@@ -59,8 +58,9 @@ int resolve_opts(Kind kind, const dpp_opts_t* o, Opts* r) {
   r->generic = o && (o->flags & DPP_FLAG_GENERIC_UPDATE);
   if (nb != 32 && nb != 64 && nb != 128 && nb != 256) return DPP_EINVAL;
   if (o && (o->group < 0 || o->group > 8)) return DPP_EINVAL;
-  r->group = (o && o->group) ? o->group : 2;
-  r->group_fixed = o && o->group;
+  // G = 3 by default (round 2: C4 31.2 vs 30.8 TF/s with G = 2, UST 2675 vs 2643 samples/s,
+  // complex samples within noise; round 1, with the slower diag kernel, had measured G = 2 best)
+  r->group = (o && o->group) ? o->group : 3;
   // internal: -1 = the library's default thresholds (group_threshold below), else group only while
   // more than this many trailing rows remain (0: at every size)
   const int64_t gm = o ? o->group_min_rows : 0;
@@ -68,7 +68,6 @@ int resolve_opts(Kind kind, const dpp_opts_t* o, Opts* r) {
   if (nb > tile_max) {
     r->group = nb / tile_max;
     r->group_min_rows = 0;
-    r->group_fixed = true;
     nb = tile_max;
   }
   r->nb = nb;
@@ -79,12 +78,6 @@ int resolve_opts(Kind kind, const dpp_opts_t* o, Opts* r) {
 
 size_t esize(Kind k) { return kind_esize(k); }
 
-// Default group for batches of >= 8 samples factored together: G = 3 (UST 40x40, 1024 samples:
-// 2675 vs 2643 samples/s with G = 2; round 1: 2404 vs 2366) -- the batch keeps every SM busy, and a
-// longer group amortizes more per-tile epilogue and C traffic.  Single samples keep G = 2.
-void batch_group_default(int64_t chunk, Opts* o) {
-  if (chunk >= 8 && !o->group_fixed) o->group = 3;
-}
 
 // Workspace layout (all regions 256-byte aligned):
 //   [SampleState x chunk]
@@ -284,7 +277,7 @@ UpdateArgs base_update(Kind kind, int batch, bool vec) {
 // by the group's last step as ONE DMMA pass with K = G nb (the G panels are adjacent columns of the
 // factor; their operand copies -- W21 = L21 D1, or U12^T -- are stacked in one buffer), so the
 // update kernel's per-tile epilogue and the C read/write are amortized over G times the work.
-// G = 2 ("paired updates") by default (opts->group).
+// G = 3 by default (opts->group; G = 2 is "paired updates").
 //
 // Default grouping thresholds (opts->group_min_rows = 0): no grouping once the trailing size is
 // <= 6144 rows for 128-wide Hermitian blocks, where the diag tile makes the chain the bound near
@@ -554,7 +547,6 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
   if ((rc = check_device())) return rc;
   const int64_t chunk = o.batch_chunk > 0 ? std::min(o.batch_chunk, batch) : batch;
   if (chunk > 65535) return DPP_EINVAL;
-  batch_group_default(chunk, &o);
   WsLayout L = layout(kind, chunk, n, o, true, host);
   if (!work || work_bytes < L.total || reinterpret_cast<uintptr_t>(work) % ALIGN) return DPP_EWORKSPACE;
   char* w = reinterpret_cast<char*>(work);
@@ -629,7 +621,6 @@ size_t dpp_workspace_bytes(int op, int64_t batch, int64_t n, const dpp_opts_t* o
   int64_t chunk = batched ? batch : 1;
   if (batched && o.batch_chunk > 0) chunk = std::min(chunk, o.batch_chunk);
   chunk = std::max<int64_t>(chunk, 1);
-  batch_group_default(chunk, &o);
   return layout(kind, chunk, n, o, batched, host).total;
 }
 
