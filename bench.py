@@ -500,6 +500,38 @@ def _factor_check(dpp, Kc, n, opts, seed, b):
         return {"error": str(e)[:200]}
 
 
+def _lu_factor_check(dpp, Kc, n, opts, seed, b):
+    """The complex LU sampler's factor at full size (untimed, one more sample in place on a copy):
+    max|L|, max|U| and the randomized residual max|(L U - (K - 1_{Y^c})) x| / (max|K| max|x|)
+    (reading R17: the panel solves use explicit tile inverses; Aztec kernels have |L| >> 1)."""
+    import torch
+    try:
+        Kf = Kc.clone()
+        work = dpp.workspace("lu_z", n, opts=opts)
+        s = dpp.sample("lu_z", Kf, seed, opts=opts, work=work)
+        torch.cuda.synchronize()
+        del work
+        F = Kf.T  # natural indexing of the column-major storage
+        g = torch.Generator(device="cuda"); g.manual_seed(1234)
+        x = torch.randn(n, 2, dtype=torch.float64, device="cuda", generator=g).to(torch.complex128)
+        U = torch.triu(F)
+        y = U @ x
+        max_u = float(U.abs().max())
+        del U
+        L = torch.tril(F, -1)
+        max_l = float(L.abs().max())
+        L.diagonal().fill_(1.0)
+        lhs = L @ y
+        del L, F, Kf
+        Kn = Kc.T
+        rhs = Kn @ x - (1.0 - s.mask.double()).to(torch.complex128)[:, None] * x
+        res = float((lhs - rhs).abs().max() / (Kn.abs().max() * x.abs().max()))
+        torch.cuda.empty_cache()
+        return {"max_abs_L": round(max_l, 3), "max_abs_U": round(max_u, 3), "residual": res, "sample_b": int(b)}
+    except Exception as e:  # diagnostics only
+        return {"error": str(e)[:200]}
+
+
 def dist_record(args, world, rank, dist):
     """BASELINE configs[4]: one sample of the n = 65536 real kernel (K = Q diag(lam) Q^T, lam ~
     U(0,1)) factored 1D block-column-cyclic over all `world` ranks with the NCCL panel broadcast
@@ -702,6 +734,7 @@ def extra_workload(args):
         last = (args.warmup + args.steps - 1) % NSA
         mask, ll = masks[last], lls[last]
         ok = W.is_aztec_tiling(d, mask[0].cpu().numpy())
+        lu_check = _lu_factor_check(dpp, Kc, n, opts, SEED, 99)
         flops = 8.0 * n ** 3 / 3.0 * args.steps * world  # complex LU, paper convention (R11)
         up = prof["update_trailing"]
         ach = up["flops"] / max(up.get("ms_union") or up["ms"], 1e-9) / 1e9  # union of its launch intervals
@@ -711,7 +744,7 @@ def extra_workload(args):
                                         f"LU sampler on the balanced-gauge Kenyon kernel, one sample per GPU per step",
                             "n": n, "nb": 64, "global_batch": world, "seq_len": None, "parallelism": f"dp{world}",
                             "api": "dpp_sample_lu_z_batched(batch=1): K copied into the workspace each step"},
-                    last_sample_is_perfect_tiling=ok, last_loglik=float(ll[0]),
+                    last_sample_is_perfect_tiling=ok, last_loglik=float(ll[0]), factor_check=lu_check,
                     loglik_closed_form=-d * (d + 1) / 2 * float(np.log(2.0)),
                     roofline={"bound": "tensor", "kernel": "update_ws_kernel<cplx> trailing update (b)",
                               "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
@@ -746,13 +779,21 @@ def extra_workload(args):
         line.update(value=round(flops / (ms / 1e3) / 1e9, 2), ms_per_step=round(ms / args.steps, 3), scaling="weak",
                     dtype="f32", samples_per_s=round(args.steps * world / (ms / 1e3), 3),
                     config={"workload": f"single-precision real symmetric sampler on the configs[3] kernel (n={n}, "
-                                        f"Beta(1/2,1/2), rounded to fp32), one sample per GPU per step",
+                                        f"Beta(1/2,1/2), rounded to fp32), one sample per GPU per step; updates "
+                                        f"on tcgen05 tensor cores (3xTF32)",
                             "n": n, "nb": 128, "global_batch": world, "seq_len": None, "parallelism": f"dp{world}"},
                     kept_last_sample=int(masks[0].sum()),
-                    roofline={"bound": "alu", "kernel": "update_simt_kernel<float> trailing update (b)",
-                              "achieved": round(ach, 3), "peak": FP32_SIMT_PEAK_TFLOPS, "unit": "TFLOP/s",
-                              "frac": round(ach / FP32_SIMT_PEAK_TFLOPS, 4), "traffic": None,
-                              "peak_source": "148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz (no exact-fp32 tensor MMA)"},
+                    roofline={"bound": "tensor", "kernel": "update_tc32_kernel (3xTF32 tcgen05) trailing update (b)",
+                              "achieved": round(3 * ach, 3), "peak": round(_tf32_peak(), 1), "unit": "TFLOP/s",
+                              "frac": round(3 * ach / _tf32_peak(), 4), "traffic": None,
+                              "model_tflops": round(ach, 3),
+                              "achieved_definition": "tensor-core flops (3 tf32 MMAs per fp32 product: 3 x the "
+                                                     "model flops) of the trailing-update launches / the union of "
+                                                     "their launch intervals",
+                              "peak_source": "MEASURED_PEAKS.json bf16_tflops x the guide's nominal tf32/bf16 ratio "
+                                             "(1.1 / 2.25 PFLOP/s dense)",
+                              "fp32_simt_peak": FP32_SIMT_PEAK_TFLOPS,
+                              "model_over_fp32_simt_peak": round(ach / FP32_SIMT_PEAK_TFLOPS, 4)},
                     stages={k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                                 "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3)} for k, v in prof.items()},
                     gpu_launches=int(sum(v["launches"] for v in prof.values())),
@@ -991,6 +1032,15 @@ def extra_workload(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _tf32_peak():
+    """Dense tf32 tensor-core peak: the measured bf16 peak x the nominal tf32/bf16 ratio."""
+    try:
+        bf16 = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+    except Exception:
+        bf16 = 2250.0  # the guide's nominal dense bf16 (no measurement available)
+    return bf16 * 1.1 / 2.25
 
 
 def _hbm_peak():

@@ -76,6 +76,10 @@ typedef struct CUstream_st* dpp_stream_t; /* == cudaStream_t */
 #define DPP_FLAG_GENERIC_UPDATE 1u /* every update / panel GEMM on the cp.async fallback kernel
                                       (diagnostics: it is otherwise used only for operands that are
                                       not 16-byte aligned); same results up to rounding */
+#define DPP_FLAG_FP32_SIMT 2u      /* dpp_sample_herm_s*: the updates on the FP32 SIMT pipe (every
+                                      product and sum an fp32 operation) instead of the default
+                                      3xTF32 split on the tcgen05 tensor cores (each product to
+                                      ~2^-21 relative, fp32 accumulation) */
 typedef struct {
   int32_t nb;            /* block size: 32, 64, 128 or 256 (0 = default: 128 real, 64 complex).
                             Blocks wider than the kind's tile (128 real, 64 complex) are factored

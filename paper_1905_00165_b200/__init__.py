@@ -37,6 +37,7 @@ class dpp_opts_t(ctypes.Structure):
 
 
 DPP_FLAG_GENERIC_UPDATE = 1
+DPP_FLAG_FP32_SIMT = 2
 
 
 class dpp_info_t(ctypes.Structure):

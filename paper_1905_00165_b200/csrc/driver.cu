@@ -41,6 +41,7 @@ struct Opts {
   int group;             // G: trailing updates of G consecutive steps applied as one K = G nb pass
   int64_t group_min_rows;  // -1: defaults; else group only while more than this many rows remain
   bool generic;          // DPP_FLAG_GENERIC_UPDATE
+  bool fp32_simt;        // DPP_FLAG_FP32_SIMT
 };
 
 // opts->nb larger than the kind's tile (256 real; 128 or 256 complex) is the blocked algorithm with
@@ -56,6 +57,7 @@ int resolve_opts(Kind kind, const dpp_opts_t* o, Opts* r) {
   r->forced = o ? o->forced : nullptr;
   r->batch_chunk = o ? o->batch_chunk : 0;
   r->generic = o && (o->flags & DPP_FLAG_GENERIC_UPDATE);
+  r->fp32_simt = o && (o->flags & DPP_FLAG_FP32_SIMT);
   if (nb != 32 && nb != 64 && nb != 128 && nb != 256) return DPP_EINVAL;
   if (o && (o->group < 0 || o->group > 8)) return DPP_EINVAL;
   // G = 3 by default (round 2: C4 31.2 vs 30.8 TF/s with G = 2, UST 2675 vs 2643 samples/s,
@@ -87,7 +89,8 @@ size_t esize(Kind k) { return kind_esize(k); }
 //    (Hermitian, the pre-scaled trailing-update operand) or U12^T (LU, the row panel K-major)]
 //   [K copies: chunk x ldk x n (batched / host)][host staging: mask, loglik, info (host)]
 struct WsLayout {
-  size_t state_off, bm_off, am_off, d_off, ut_off, k_off, mask_off, ll_off, info_off, total;
+  size_t state_off, bm_off, am_off, d_off, ut_off, tcs_off, k_off, mask_off, ll_off, info_off, total;
+  size_t tcs_bytes;  // per stream region (two regions: the chain's stream and the trailing stream)
   int64_t ldk, strideK, strideM, strideU;
 };
 
@@ -108,6 +111,15 @@ WsLayout layout(Kind kind, int64_t chunk, int64_t n, const Opts& o, bool copies,
   if (kind_herm(kind)) off = align_up(off + 2 * (size_t)chunk * nb * 8);
   L.ut_off = off;
   off = align_up(off + 2 * (size_t)std::max(o.group, 2) * chunk * (size_t)L.strideU * es);
+  // real single precision, one sample: the 3xTF32 tensor-core updates' packed operands, one region
+  // per stream (the lookahead and the trailing updates run concurrently)
+  L.tcs_off = off;
+  L.tcs_bytes = 0;
+  if (kind == HERM_S && chunk == 1 && !o.fp32_simt && n > 0) {
+    const int kmax = std::max(o.group, 1) * nb;
+    L.tcs_bytes = align_up(tc32_scratch_bytes((int)n, (int)n, kmax));
+    off = align_up(off + 2 * L.tcs_bytes);
+  }
   L.k_off = off;
   if (copies) off = align_up(off + (size_t)chunk * (size_t)L.strideK * es);
   L.mask_off = off;
@@ -319,6 +331,11 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
                    ((size_t)strideA * es) % 16 == 0;
   auto upd = [&](UpdateArgs u, cudaStream_t s) -> cudaError_t {
     u.generic = o.generic ? 1 : 0;
+    u.fp32_simt = o.fp32_simt ? 1 : 0;
+    if (L.tcs_bytes) {
+      u.tcs = work + L.tcs_off + ((la && s == s2) ? L.tcs_bytes : 0);
+      u.tcs_bytes = (int64_t)L.tcs_bytes;
+    }
     return launch_update(kind, u, s);
   };
   void* Bm = work + L.bm_off;

@@ -70,6 +70,9 @@ struct UpdateArgs {
   int btri;             // 1: op(B)(j, k) = 0 for k > j (the stage-2 operators are triangular): a
                         //    warp's K loop stops at its last column (fast kernel only; the others
                         //    just multiply the zeros)
+  int fp32_simt;        // single precision: the FP32 SIMT kernel instead of 3xTF32 tensor cores
+  void* tcs;            // real single precision: scratch for the 3xTF32 packed operands (or null)
+  int64_t tcs_bytes;
   int generic;          // 1: the cp.async fallback kernel even for aligned operands (DPP_FLAG_GENERIC_UPDATE)
   int grid_limit;       // > 0: persistent launch with at most this many CTAs (SMs left to the
                         //      lookahead stream); 0: short-lived CTAs (<= 4 tiles each)
@@ -91,6 +94,8 @@ struct UpdateArgs {
 cudaError_t launch_diag(Kind kind, int nb, const DiagArgs& a, cudaStream_t s);
 cudaError_t launch_update(Kind kind, UpdateArgs a, cudaStream_t s);
 cudaError_t launch_update_simt(Kind kind, UpdateArgs a, cudaStream_t s);  // single precision
+cudaError_t launch_update_tc32(UpdateArgs a, cudaStream_t s);  // real single precision, 3xTF32 tcgen05
+size_t tc32_scratch_bytes(int rows, int cols, int K);
 // dst(j, k) = src(k, j) for k < rows, j < cols (elements of es = 8 or 16 bytes), `batch` matrices at
 // the given strides: the LU row panel A12 / U12 (jb x m2, N-major as a GEMM operand) <-> its K-major
 // transpose.

@@ -29,15 +29,18 @@ def _kernel(kind, n, seed):
     return W.similarity(W.haar_kernel(n, seed=seed, complex_=True), seed=seed).astype(np.complex64)
 
 
-@pytest.mark.parametrize("kind,n,nb,la", [("herm_s", 1, 0, 1), ("herm_s", 100, 0, 1), ("herm_s", 300, 0, 1),
-                                           ("herm_s", 1000, 0, 0), ("herm_s", 1000, 64, 1), ("herm_s", 2125, 0, 1),
-                                           ("lu_c", 130, 0, 1), ("lu_c", 600, 0, 1), ("lu_c", 600, 32, 0)])
-def test_fp32_matches_fp32_oracle(oracle_mod, kind, n, nb, la):
+@pytest.mark.parametrize("kind,n,nb,la,flags", [
+    ("herm_s", 1, 0, 1, 0), ("herm_s", 100, 0, 1, 0), ("herm_s", 300, 0, 1, 0), ("herm_s", 1000, 0, 0, 0),
+    ("herm_s", 1000, 64, 1, 0), ("herm_s", 2125, 0, 1, 0), ("herm_s", 2125, 256, 1, 0),
+    # the FP32 SIMT updates (DPP_FLAG_FP32_SIMT) instead of the default 3xTF32 tensor-core updates
+    ("herm_s", 300, 0, 1, 2), ("herm_s", 2125, 0, 1, 2), ("herm_s", 1000, 64, 0, 2),
+    ("lu_c", 130, 0, 1, 0), ("lu_c", 600, 0, 1, 0), ("lu_c", 600, 32, 0, 0)])
+def test_fp32_matches_fp32_oracle(oracle_mod, kind, n, nb, la, flags):
     K = _kernel(kind, n, n + 3)
     fn = oracle_mod.sample_herm_s if kind == "herm_s" else oracle_mod.sample_lu_c
     o = fn(K, 7, 0, tie_tol=TIE32)
     Kc = to_device(K, kind)
-    s = dpp.sample(kind, Kc, 7, opts=dpp.make_opts(nb=nb, lookahead=la))
+    s = dpp.sample(kind, Kc, 7, opts=dpp.make_opts(nb=nb, lookahead=la, flags=flags))
     torch.cuda.synchronize()
     mask = s.mask.cpu().numpy()
     k = o.first_tie if o.n_ties else n
