@@ -162,7 +162,7 @@ def main():
     ap.add_argument("--tally", type=int, default=0, help="aztec_c: untimed extra batches whose tilings are all checked")
     ap.add_argument("--rank", type=int, default=500, help="elementary: projection rank k")
     ap.add_argument("--lookahead", type=int, default=1, help="ust: 0 = single stream")
-    ap.add_argument("--nb", type=int, default=128, help="ust: block size")
+    ap.add_argument("--nb", type=int, default=128, help="ust / herm_s: block size")
     ap.add_argument("--group", type=int, default=0, help="c4 / ust: dpp_opts_t.group (0 = library default)")
     ap.add_argument("--no-dist", action="store_true", help="c4: skip the configs[4] block-cyclic sub-record")
     ap.add_argument("--dist-n", type=int, default=65536, help="c4: n of the block-cyclic sub-record")
@@ -755,7 +755,7 @@ def extra_workload(args):
     elif args.workload == "herm_s":
         n = args.n
         Kc = W.haar_kernel_torch(n, seed=KSEED, spectrum="beta").to(torch.float32)
-        opts = dpp.make_opts(nb=128, lookahead=1)
+        opts = dpp.make_opts(nb=args.nb, lookahead=1, group=args.group)
         op = dpp.DPP_OP_HERM_S | dpp.DPP_OP_BATCHED
         NSS = args.streams  # consecutive samples rotate over this many streams (as the default workload)
         works = [torch.empty(dpp.dpp_workspace_bytes(op, 1, n, opts), dtype=torch.uint8, device="cuda")
@@ -781,7 +781,7 @@ def extra_workload(args):
                     config={"workload": f"single-precision real symmetric sampler on the configs[3] kernel (n={n}, "
                                         f"Beta(1/2,1/2), rounded to fp32), one sample per GPU per step; updates "
                                         f"on tcgen05 tensor cores (3xTF32)",
-                            "n": n, "nb": 128, "global_batch": world, "seq_len": None, "parallelism": f"dp{world}"},
+                            "n": n, "nb": args.nb, "global_batch": world, "seq_len": None, "parallelism": f"dp{world}"},
                     kept_last_sample=int(masks[0].sum()),
                     roofline={"bound": "tensor", "kernel": "update_tc32_kernel (3xTF32 tcgen05) trailing update (b)",
                               "achieved": round(3 * ach, 3), "peak": round(_tf32_peak(), 1), "unit": "TFLOP/s",

@@ -13,16 +13,17 @@
 //           is split once into hi/lo tf32 parts and written as 16 KB images of the canonical
 //           K-major no-swizzle UMMA layout, one per (128-row tile, 32-k chunk, part) -- so the
 //           GEMM's producer moves each stage with two contiguous bulk copies;
-//   GEMM:   one CTA per SM, persistent over 128 x 128 tiles of C, 192 threads:
+//   GEMM:   one CTA per SM, persistent over 128 x 128 tiles of C:
 //           warp 0     PRODUCER (one lane): TMA bulk copies (cp.async.bulk) of the four 16 KB
-//                      images of a k-chunk into a 3-stage ring, full/empty mbarriers;
+//                      images of a k-chunk into a 3-stage ring, full/empty mbarriers (320 threads);
 //           warp 1     MMA ISSUER (one lane): per k-group of 8, three tcgen05.mma (M = N = 128,
 //                      K = 8) into one of two TMEM accumulators (2 x 128 columns); tcgen05.commit
 //                      releases the ring stage and, at the end of a tile, the accumulator;
-//           warps 2-5  EPILOGUE: tcgen05.ld of their 32 TMEM lanes (= 32 rows of the tile), C -= acc
-//                      in global memory (coalesced column segments; Hermitian diagonal tiles
-//                      masked), then release the accumulator -- the epilogue of tile t overlaps the
-//                      MMAs of tile t+1.
+//           warps 2-9  EPILOGUE: each loads its C values (32 rows x 64 columns) while the tile's
+//                      MMAs run, then tcgen05.ld of its 32 TMEM lanes (= rows), C -= acc in global
+//                      memory (coalesced column segments; Hermitian diagonal tiles masked), and
+//                      releases the accumulator -- the epilogue of tile t overlaps the MMAs of
+//                      tile t+1.
 // The canonical layout (CuTe's Layout_K_INTER_Atom; make_umma_desc<Major::K> with SWIZZLE_NONE):
 // core matrices of 8 rows x 16 bytes (4 k); the two 4-k halves of one MMA's K = 8 slice are LBO
 // apart, consecutive 8-row groups SBO apart.  (The MN-major no-swizzle form, which would have
@@ -38,7 +39,7 @@ namespace dpp {
 namespace {
 
 constexpr int TC_BM = 128, TC_BN = 128, TC_KC = 32, TC_STAGES = 3;
-constexpr int TC_NT = 192;
+constexpr int TC_NT = 320;  // producer warp, MMA warp, 8 epilogue warps
 constexpr uint32_t TC_PART = TC_BM * TC_KC * 4;  // 16 KB: one (tile, chunk) image of one part
 constexpr uint32_t TC_STAGE = 4 * TC_PART;       // A hi, A lo, B hi, B lo
 constexpr uint32_t TC_KLBO = 128, TC_KSBO = 256, TC_KSLICE = (TC_BM / 8) * TC_KSBO;  // 4 KB per K = 8
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(TC_NT, 1) update_tc32_kernel(const UpdateArgs 
 
   if (tid == 0) {
     for (int i = 0; i < TC_STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 256); }
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -206,29 +207,37 @@ __global__ void __launch_bounds__(TC_NT, 1) update_tc32_kernel(const UpdateArgs 
     }
   } else {
     // ============================ epilogue ============================
-    const int q = warp & 3;  // TMEM lanes 32 q .. 32 q + 31 = tile rows
+    // 8 warps: warp w serves TMEM lanes 32 (w % 4) .. + 31 (= tile rows) and columns 64 h .. 64 h + 63,
+    // h = (w - 2) / 4; its C values are loaded BEFORE the accumulator is ready, so the global
+    // round trip overlaps the tile's MMAs
+    const int q = warp & 3, h = (warp - 2) >> 2;
     int ab = 0;
     uint32_t aphase = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const TileInfo ti = tile_info<TC_BM, TC_BN>(a, t, tiles_per_sample, MASK);
       if (!ti.valid) continue;
-      mbar_wait(&tfull[ab], aphase);
-      tc_fence_after();
       float* Cg = reinterpret_cast<float*>(a.C) + (int64_t)ti.s * a.strideC;
       const int r = 32 * q + lane;
       const int grow = ti.grow0 + r;
-      for (int c0 = 0; c0 < TC_BN; c0 += 32) {
+      const int cb = 64 * h;
+      float* p0 = Cg + grow + (int64_t)(ti.gcol0 + cb - ti.cshift) * a.ldc;
+      const bool row_in = r < ti.nrows;
+      float cv[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j)
+        cv[j] = (row_in && cb + j < ti.ncols && (!MASK || grow >= ti.gcol0 + cb + j)) ? p0[(int64_t)j * a.ldc] : 0.f;
+      mbar_wait(&tfull[ab], aphase);
+      tc_fence_after();
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
         float v[32];
-        tc_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(ab * TC_BN + c0), v);
-        if (r < ti.nrows) {
-          float* p0 = Cg + grow + (int64_t)(ti.gcol0 + c0 - ti.cshift) * a.ldc;
-          float cv[32];
+        tc_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(ab * TC_BN + cb + 32 * half), v);
+        if (row_in) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)  // all loads first: one global round trip per 32 columns
-            cv[j] = (c0 + j < ti.ncols && (!MASK || grow >= ti.gcol0 + c0 + j)) ? p0[(int64_t)j * a.ldc] : 0.f;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c0 + j < ti.ncols && (!MASK || grow >= ti.gcol0 + c0 + j)) p0[(int64_t)j * a.ldc] = cv[j] - v[j];
+          for (int j = 0; j < 32; ++j) {
+            const int c = cb + 32 * half + j;
+            if (c < ti.ncols && (!MASK || grow >= ti.gcol0 + c)) p0[(int64_t)(32 * half + j) * a.ldc] = cv[32 * half + j] - v[j];
+          }
         }
       }
       tc_fence_before();
