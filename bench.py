@@ -307,7 +307,21 @@ def main():
                "pct_fp64_peak": round(100 * model_flops(n) / (lat_ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS, 2),
                "trailing_update_tflops": round(one_tf, 3),
                "what": "one caller stream: each sample starts after the previous one ends (no samples in flight)"}
-    achieved_tf = probe_tf
+    # ---- the roofline probe proper: one launch of the same trailing-update kernel, alone and
+    #      persistent on every SM (dpp_probe_update_d), with the shape of the sample's largest
+    #      trailing update: m = n - 4 nb rows, K = G nb = 384 (the default group of 3 block steps)
+    pm, pK = n - 4 * NB, 3 * NB
+    gW = torch.Generator(device="cuda"); gW.manual_seed(5)
+    Wp = torch.randn(pK, pm, dtype=torch.float64, device="cuda", generator=gW)
+    Lp = torch.randn(pK, pm, dtype=torch.float64, device="cuda", generator=gW)
+    Cp = torch.zeros(pm, pm, dtype=torch.float64, device="cuda")
+    pms = sorted(dpp.dpp_probe_update_d(pm, pK, Wp, Lp, pm, Cp, pm) for _ in range(4))[1:3]
+    probe_ms = sum(pms) / len(pms)
+    probe_flops = pm * (pm + 1) / 2 * 2.0 * pK
+    iso_tf = probe_flops / (probe_ms / 1e3) / 1e12
+    del Wp, Lp, Cp
+    torch.cuda.empty_cache()
+    achieved_tf = iso_tf
 
     # ---- end-to-end through the host-buffer C-ABI calls (H2D of K + D2H of mask/loglik inside every
     #      step).  Headline: the stream-ordered entry point, consecutive steps on two streams with two
@@ -442,11 +456,17 @@ def main():
                          "frac": round(achieved_tf / FP64_PEAK_TFLOPS, 4),
                          "traffic": (_traffic() or {}).get("bytes_per_launch"), "traffic_detail": _traffic(),
                          "peak_source": PEAK_SOURCE,
-                         "achieved_definition": "isolated probe: the largest trailing-update launch of a sample "
-                                                "run alone (one caller stream), its algorithmic flops / its CUDA-"
-                                                "event duration on the launching stream (it runs on the SMs the "
-                                                "lookahead chain leaves it)",
-                         "probe_launch_flops": round(prof1["top_flops"]), "probe_launch_ms": round(prof1["top_ms"], 4),
+                         "achieved_definition": "isolated probe: one launch of the trailing-update kernel "
+                                                "(dpp_probe_update_d) alone and persistent on every SM, with the "
+                                                "shape of the sample's largest trailing update (m = n - 4 nb, K = "
+                                                "3 nb): algorithmic flops m(m+1)/2 x 2K / its CUDA-event duration "
+                                                "(median of the middle two of four launches)",
+                         "probe_m": pm, "probe_K": pK, "probe_launch_ms": round(probe_ms, 4),
+                         "probe_launch_flops": round(probe_flops),
+                         "in_situ_largest_launch_tflops": round(probe_tf, 3),
+                         "in_situ_definition": "the largest trailing-update launch inside a one-stream sample: its "
+                                               "flops / its event duration, on the SMs the lookahead chain leaves it",
+                         "in_situ_launch_flops": round(prof1["top_flops"]), "in_situ_launch_ms": round(prof1["top_ms"], 4),
                          "union_achieved": round(union_tf, 3),
                          "union_definition": "all trailing-update launches of the timed region (samples in "
                                              "flight): their flops / the union of their launch intervals",
@@ -807,38 +827,52 @@ def extra_workload(args):
         Kc = W.aztec_kernel_balanced(d, device="cuda").to(torch.complex64)
         torch.cuda.synchronize()
         B = args.batch if args.batch != 1024 else 8
-        opts = dpp.make_opts(nb=64, lookahead=1, batch_chunk=1)
+        want = -d * (d + 1) / 2 * float(np.log(2.0))
         op = dpp.DPP_OP_LU_C | dpp.DPP_OP_BATCHED
-        work = torch.empty(dpp.dpp_workspace_bytes(op, B, n, opts), dtype=torch.uint8, device="cuda")
         mask = torch.empty((B, n), dtype=torch.uint8, device="cuda")
         ll = torch.empty(B, dtype=torch.float64, device="cuda")
-
-        def step(i):
-            dpp.dpp_sample_lu_c_batched(B, n, Kc, n, 0, SEED, (rank * 1000 + i) * B, mask, ll, None, opts, work)
-        ms, clocks = _timed(step, args.steps, args.warmup, world, dist)
-        masks = mask.cpu().numpy()
-        good = sum(W.is_aztec_tiling(d, masks[b]) for b in range(B))
-        want = -d * (d + 1) / 2 * float(np.log(2.0))
-        if args.tally > 0:  # untimed: tilings over args.tally further batches (fresh sample indices)
-            t_good, t_err = 0, []
-            for i in range(args.tally):
-                step(args.steps + args.warmup + i)
-                mk, lv = mask.cpu().numpy(), ll.cpu().numpy()
-                t_good += sum(W.is_aztec_tiling(d, mk[b]) for b in range(B))
-                t_err += [float(x) for x in np.abs(lv - want)]
-            line["tally"] = {"samples": args.tally * B, "perfect_tilings": t_good,
-                             "loglik_error_max": max(t_err), "loglik_error_median": float(np.median(t_err)),
-                             "b0": (rank * 1000 + args.steps + args.warmup) * B}
         flops = 8.0 * n ** 3 / 3.0 * B * args.steps * world
-        line.update(value=round(flops / (ms / 1e3) / 1e9, 2), ms_per_step=round(ms / args.steps, 3), scaling="weak",
-                    dtype="c64", samples_per_s=round(B * args.steps * world / (ms / 1e3), 4),
+        variants = {}
+        # exact fp32 (FP32 SIMT updates: the paper's single-precision sampler) and the default 3xTF32
+        # tensor-core updates (products to ~2^-21 relative, fp32 accumulation)
+        for name, flags in (("exact_fp32_simt", dpp.DPP_FLAG_FP32_SIMT), ("tensor_3xtf32", 0)):
+            opts = dpp.make_opts(nb=64, lookahead=1, batch_chunk=1, flags=flags)
+            work = torch.empty(dpp.dpp_workspace_bytes(op, B, n, opts), dtype=torch.uint8, device="cuda")
+
+            def step(i):
+                dpp.dpp_sample_lu_c_batched(B, n, Kc, n, 0, SEED, (rank * 1000 + i) * B, mask, ll, None, opts, work)
+            ms, clocks = _timed(step, args.steps, args.warmup, world, dist)
+            masks = mask.cpu().numpy()
+            good = sum(W.is_aztec_tiling(d, masks[b]) for b in range(B))
+            v = {"value": round(flops / (ms / 1e3) / 1e9, 2), "ms_per_step": round(ms / args.steps, 3),
+                 "samples_per_s": round(B * args.steps * world / (ms / 1e3), 4),
+                 "perfect_tilings_last_step": f"{good}/{B}",
+                 "max_abs_loglik_error_last_step": float(np.max(np.abs(ll.cpu().numpy() - want))),
+                 "pct_fp32_simt_peak": round(100 * flops / (ms / 1e3) / 1e12 / (FP32_SIMT_PEAK_TFLOPS * world), 2),
+                 "clocks": clocks}
+            if args.tally > 0 and flags:  # untimed, exact fp32: tilings over args.tally further batches
+                t_good, t_err = 0, []
+                for i in range(args.tally):
+                    step(args.steps + args.warmup + i)
+                    mk, lv = mask.cpu().numpy(), ll.cpu().numpy()
+                    t_good += sum(W.is_aztec_tiling(d, mk[b]) for b in range(B))
+                    t_err += [float(x) for x in np.abs(lv - want)]
+                v["tally"] = {"samples": args.tally * B, "perfect_tilings": t_good,
+                              "loglik_error_max": max(t_err), "loglik_error_median": float(np.median(t_err)),
+                              "b0": (rank * 1000 + args.steps + args.warmup) * B}
+            variants[name] = v
+            del work
+            torch.cuda.empty_cache()
+        main = variants["tensor_3xtf32"]
+        line.update(value=main["value"], ms_per_step=main["ms_per_step"], scaling="weak", dtype="c64",
+                    samples_per_s=main["samples_per_s"],
                     config={"workload": f"single-precision (complex64) LU sampler, order-{d} Aztec diamond (n={n}), "
-                                        f"balanced-gauge Kenyon kernel, {B} samples per GPU per step",
-                            "n": n, "nb": 64, "global_batch": B * world, "seq_len": None, "parallelism": f"dp{world}"},
-                    perfect_tilings_last_step=f"{good}/{B}",
-                    max_abs_loglik_error_last_step=float(np.max(np.abs(ll.cpu().numpy() - want))),
-                    pct_fp32_simt_peak=round(100 * flops / (ms / 1e3) / 1e12 / (FP32_SIMT_PEAK_TFLOPS * world), 2),
-                    clocks=clocks)
+                                        f"balanced-gauge Kenyon kernel, {B} samples per GPU per step; value: the "
+                                        f"default 3xTF32 tensor-core updates", "n": n, "nb": 64,
+                            "global_batch": B * world, "seq_len": None, "parallelism": f"dp{world}"},
+                    perfect_tilings_last_step=main["perfect_tilings_last_step"],
+                    max_abs_loglik_error_last_step=main["max_abs_loglik_error_last_step"],
+                    pct_fp32_simt_peak=main["pct_fp32_simt_peak"], clocks=main["clocks"], variants=variants)
     elif args.workload == "elementary":
         # Listing 2: rank-k projection of order n = 5000 (the paper's elementary
         # sampler figure: ranks 10..500), a batch of independent samples per GPU per step

@@ -380,6 +380,14 @@ int dpp_profile_end(dpp_profile_t* out);
  * i < max_records; *count (nullable) = the number of launches recorded. */
 int dpp_profile_end_records(dpp_profile_t* out, double* records, int64_t max_records, int64_t* count);
 
+/* Diagnostics (the roofline probe of the dominant kernel): ONE launch of the real trailing-update
+ * kernel, C -= W L^T on the lower triangle of an m x m region with K-deep operands (W, L: m x K
+ * column-major, leading dimension ldo; C: ldc), alone and persistent on every SM, timed with CUDA
+ * events on `stream` (synchronises it); *ms = its duration.  The operands are arbitrary data: this
+ * measures the kernel, it samples nothing.  Listing 3 line 586. */
+int dpp_probe_update_d(int64_t m, int32_t K, const double* W, const double* L, int64_t ldo, double* C,
+                       int64_t ldc, float* ms, dpp_stream_t stream);
+
 const char* dpp_strerror(int code);
 const char* dpp_version(void);
 

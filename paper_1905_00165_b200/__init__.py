@@ -95,6 +95,7 @@ _sig("dpp_profile_begin", ctypes.c_int, [])
 _sig("dpp_profile_begin_stages", ctypes.c_int, [ctypes.c_uint])
 _sig("dpp_profile_end", ctypes.c_int, [ctypes.POINTER(dpp_profile_t)])
 _sig("dpp_profile_end_records", ctypes.c_int, [ctypes.POINTER(dpp_profile_t), _P, _I64, ctypes.POINTER(_I64)])
+_sig("dpp_probe_update_d", ctypes.c_int, [_I64, ctypes.c_int32, _P, _P, _I64, _P, _I64, ctypes.POINTER(ctypes.c_float), _P])
 _sig("dpp_strerror", ctypes.c_char_p, [ctypes.c_int])
 _sig("dpp_version", ctypes.c_char_p, [])
 
@@ -108,7 +109,7 @@ EXPORTS = ["dpp_workspace_bytes", "dpp_sample_herm_d", "dpp_sample_herm_z", "dpp
            "dpp_sample_herm_d_host", "dpp_sample_herm_z_host", "dpp_sample_lu_z_host",
            "dpp_philox_uniforms", "dpp_comm_init", "dpp_comm_init_local", "dpp_comm_destroy", "dpp_bcc_local_cols",
            "dpp_dist_workspace_bytes", "dpp_dist_message_bytes", "dpp_sample_herm_d_dist", "dpp_sample_herm_z_dist",
-           "dpp_sample_herm_d_dist_local", "dpp_sample_herm_z_dist_local", "dpp_profile_begin", "dpp_profile_begin_stages", "dpp_profile_end", "dpp_profile_end_records",
+           "dpp_sample_herm_d_dist_local", "dpp_sample_herm_z_dist_local", "dpp_profile_begin", "dpp_profile_begin_stages", "dpp_profile_end", "dpp_profile_end_records", "dpp_probe_update_d",
            "dpp_strerror", "dpp_version"]
 
 
@@ -380,6 +381,13 @@ def dpp_profile_end_records(max_records: int = 1 << 16):
     rows = [(STAGES[int(buf[4 * i])], float(buf[4 * i + 1]), float(buf[4 * i + 2]), float(buf[4 * i + 3]))
             for i in range(n)]
     return agg, rows
+
+
+def dpp_probe_update_d(m, K, W, L, ldo, C, ldc, stream=None) -> float:
+    """One isolated launch of the real trailing-update kernel (C -= W L^T, lower triangle); its ms."""
+    ms = ctypes.c_float(0.0)
+    _check(_lib.dpp_probe_update_d(m, K, _ptr(W), _ptr(L), ldo, _ptr(C), ldc, ctypes.byref(ms), _stream(stream)))
+    return float(ms.value)
 
 
 def dpp_version() -> str:

@@ -111,13 +111,13 @@ WsLayout layout(Kind kind, int64_t chunk, int64_t n, const Opts& o, bool copies,
   if (kind_herm(kind)) off = align_up(off + 2 * (size_t)chunk * nb * 8);
   L.ut_off = off;
   off = align_up(off + 2 * (size_t)std::max(o.group, 2) * chunk * (size_t)L.strideU * es);
-  // real single precision, one sample: the 3xTF32 tensor-core updates' packed operands, one region
+  // single precision, one sample: the 3xTF32 tensor-core updates' packed operands, one region
   // per stream (the lookahead and the trailing updates run concurrently)
   L.tcs_off = off;
   L.tcs_bytes = 0;
-  if (kind == HERM_S && chunk == 1 && !o.fp32_simt && n > 0) {
+  if ((kind == HERM_S || kind == LU_C) && chunk == 1 && !o.fp32_simt && n > 0) {
     const int kmax = std::max(o.group, 1) * nb;
-    L.tcs_bytes = align_up(tc32_scratch_bytes((int)n, (int)n, kmax));
+    L.tcs_bytes = align_up(tc32_scratch_bytes((int)n, (int)n, kmax, kind == LU_C));
     off = align_up(off + 2 * L.tcs_bytes);
   }
   L.k_off = off;
@@ -701,6 +701,34 @@ BATCHED(dpp_sample_lu_c_batched, LU_C, dpp_complex64_t, false, true)
 int dpp_philox_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, double* u, dpp_stream_t stream) {
   if (count < 0 || (count > 0 && !u)) return DPP_EINVAL;
   return launch_uniforms(seed, j0, b, count, u, (cudaStream_t)stream) == cudaSuccess ? DPP_OK : DPP_ECUDA;
+}
+
+int dpp_probe_update_d(int64_t m, int32_t K, const double* W, const double* L, int64_t ldo, double* C, int64_t ldc,
+                       float* ms, dpp_stream_t stream) {
+  if (m <= 0 || K <= 0 || !W || !L || !C || !ms || ldo < m || ldc < m) return DPP_EINVAL;
+  int rc = check_device();
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  UpdateArgs u{};
+  u.Aop = W; u.lda = ldo; u.Bop = L; u.ldb = ldo; u.mask = 1;
+  u.C = C; u.ldc = ldc;
+  u.a_rows = (int)m; u.b_rows = (int)m; u.K = K; u.batch = 1;
+  u.vec = (ldo % 2 == 0 && ldc % 2 == 0 && reinterpret_cast<uintptr_t>(W) % 16 == 0 &&
+           reinterpret_cast<uintptr_t>(L) % 16 == 0 && reinterpret_cast<uintptr_t>(C) % 16 == 0) ? 1 : 0;
+  u.row0 = 0; u.col0 = 0; u.rows = (int)m; u.cols = (int)m; u.tri = 1;
+  u.grid_limit = device_sms();  // persistent over every SM, as the trailing update with nothing beside it
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+  const cudaError_t le = launch_update(HERM_D, u, st);
+  CK(cudaEventRecord(e1, st));
+  CK(cudaEventSynchronize(e1));
+  CK(le);
+  CK(cudaEventElapsedTime(ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return DPP_OK;
 }
 
 int dpp_profile_begin_stages(unsigned stage_mask) {

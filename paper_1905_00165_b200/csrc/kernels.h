@@ -94,8 +94,8 @@ struct UpdateArgs {
 cudaError_t launch_diag(Kind kind, int nb, const DiagArgs& a, cudaStream_t s);
 cudaError_t launch_update(Kind kind, UpdateArgs a, cudaStream_t s);
 cudaError_t launch_update_simt(Kind kind, UpdateArgs a, cudaStream_t s);  // single precision
-cudaError_t launch_update_tc32(UpdateArgs a, cudaStream_t s);  // real single precision, 3xTF32 tcgen05
-size_t tc32_scratch_bytes(int rows, int cols, int K);
+cudaError_t launch_update_tc32(UpdateArgs a, cudaStream_t s, bool cplx);  // single precision, 3xTF32 tcgen05
+size_t tc32_scratch_bytes(int rows, int cols, int K, bool cplx);
 // dst(j, k) = src(k, j) for k < rows, j < cols (elements of es = 8 or 16 bytes), `batch` matrices at
 // the given strides: the LU row panel A12 / U12 (jb x m2, N-major as a GEMM operand) <-> its K-major
 // transpose.

@@ -291,10 +291,11 @@ cudaError_t launch_update(Kind kind, UpdateArgs a, cudaStream_t s) {
 }
 
 static cudaError_t launch_update_core(Kind kind, UpdateArgs a, cudaStream_t s, bool ws) {
-  // real single precision: tcgen05 3xTF32 for aligned operands (update_tc32.cu), else FP32 SIMT
-  if (kind == HERM_S && a.vec && !a.generic && !a.fp32_simt && !a.dscale && !a.conj && !a.bnmajor && a.batch == 1 &&
-      a.bcc_P == 0 && a.tcs && a.tcs_bytes >= (int64_t)tc32_scratch_bytes(a.rows, a.cols, a.K))
-    return launch_update_tc32(a, s);
+  // single precision: tcgen05 3xTF32 for aligned operands of one sample (update_tc32.cu), else FP32 SIMT
+  if ((kind == HERM_S || (kind == LU_C && !a.mask)) && a.vec && !a.generic && !a.fp32_simt && !a.dscale && !a.conj &&
+      !a.bnmajor && a.batch == 1 && a.bcc_P == 0 && a.tcs &&
+      a.tcs_bytes >= (int64_t)tc32_scratch_bytes(a.rows, a.cols, a.K, kind == LU_C))
+    return launch_update_tc32(a, s, kind == LU_C);
   if (kind == HERM_S || kind == LU_C) return launch_update_simt(kind, a, s);
   const bool scale = a.dscale != nullptr;
 #define DPP_GO(CP, BN_, MK, SC, CJ)                                         \

@@ -30,6 +30,8 @@
 // spared the pack, produced no output for kind::tf32 in tools/tc32_test.cu.)
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "update_common.cuh"
@@ -101,14 +103,33 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, float* v) {
 
 // pack: rows [0, rows) x k [0, K) of X (element (r, k) at r + k ld) into images
 // dst[((t * nch + c) * 2 + part) * TC_PART bytes] for row tile t, k chunk c; zeros beyond.
-__global__ void __launch_bounds__(256) tc32_pack_kernel(const float* X, int64_t ld, int rows, int K, int nch,
+// Complex (complex64 X, C -= A B^T without conjugation) through the real embedding
+//   [Re C; Im C] -= [A2; A3] B2^T,  k' = 2 k + e:  A2(i, 2k) = Re A, A2(i, 2k+1) = -Im A,
+//   A3(i, 2k) = Im A, A3(i, 2k+1) = Re A,  B2(j, 2k) = Re B, B2(j, 2k+1) = Im B
+// -- an A image holds 64 complex rows (A2 above A3), a B image 128 complex rows; K' = 2 K.
+template <bool CPLX, bool AOP>
+__global__ void __launch_bounds__(256) tc32_pack_kernel(const void* Xv, int64_t ld, int rows, int K, int nch,
                                                         unsigned char* dst) {
   __shared__ __align__(16) float img[2][TC_BM * TC_KC];
   const int t = blockIdx.x, c = blockIdx.y, tid = threadIdx.x;
+  constexpr int ROWS = (CPLX && AOP) ? TC_BM / 2 : TC_BM;  // operand rows per image
   for (int e = tid; e < TC_BM * TC_KC; e += 256) {
     const int r = e % TC_BM, k = e / TC_BM;  // consecutive threads: consecutive rows of one column
-    const int gr = t * TC_BM + r, gk = c * TC_KC + k;
-    const float x = (gr < rows && gk < K) ? X[gr + (int64_t)gk * ld] : 0.f;
+    float x;
+    if constexpr (!CPLX) {
+      const float* X = reinterpret_cast<const float*>(Xv);
+      const int gr = t * TC_BM + r, gk = c * TC_KC + k;
+      x = (gr < rows && gk < K) ? X[gr + (int64_t)gk * ld] : 0.f;
+    } else {
+      const float2* X = reinterpret_cast<const float2*>(Xv);
+      const int i = AOP ? (r & (ROWS - 1)) : r, blk = AOP ? (r / ROWS) : 0;
+      const int gr = t * ROWS + i, gk2 = c * TC_KC + k, gk = gk2 >> 1, ee = gk2 & 1;
+      float2 z = make_float2(0.f, 0.f);
+      if (gr < rows && gk < K) z = X[gr + (int64_t)gk * ld];
+      if (!AOP) x = ee ? z.y : z.x;                 // B2
+      else if (blk == 0) x = ee ? -z.y : z.x;       // A2
+      else x = ee ? z.x : z.y;                      // A3
+    }
     const float hi = tf32_rn(x);
     const uint32_t o = tc_koff(r, k) >> 2;
     img[0][o] = hi;
@@ -122,9 +143,10 @@ __global__ void __launch_bounds__(256) tc32_pack_kernel(const float* X, int64_t 
 
 }  // namespace
 
-template <bool MASK>
+template <bool MASK, bool CPLX>
 __global__ void __launch_bounds__(TC_NT, 1) update_tc32_kernel(const UpdateArgs a, const unsigned char* pa,
                                                                 const unsigned char* pb) {
+  constexpr int TBM = CPLX ? TC_BM / 2 : TC_BM;  // C rows per tile (complex: 64, re and im stacked)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[TC_STAGES], empty[TC_STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_s;
@@ -134,7 +156,7 @@ __global__ void __launch_bounds__(TC_NT, 1) update_tc32_kernel(const UpdateArgs 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tiles_per_sample = a.tri ? a.tiles_m * (a.tiles_m + 1) / 2 : a.tiles_m * a.tiles_n;
   const int ntiles = tiles_per_sample * a.batch;
-  const int nch = (a.K + TC_KC - 1) / TC_KC;
+  const int nch = ((CPLX ? 2 : 1) * a.K + TC_KC - 1) / TC_KC;
 
   if (tid == 0) {
     for (int i = 0; i < TC_STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
@@ -158,9 +180,9 @@ __global__ void __launch_bounds__(TC_NT, 1) update_tc32_kernel(const UpdateArgs 
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const TileInfo ti = tile_info<TC_BM, TC_BN>(a, t, tiles_per_sample, MASK);
+        const TileInfo ti = tile_info<TBM, TC_BN>(a, t, tiles_per_sample, MASK);
         if (!ti.valid) continue;
-        const int tr = (ti.grow0 - a.row0) / TC_BM, tc = (ti.gcol0 - a.col0) / TC_BN;
+        const int tr = (ti.grow0 - a.row0) / TBM, tc = (ti.gcol0 - a.col0) / TC_BN;
         for (int kc = 0; kc < nch; ++kc) {
           mbar_wait(&empty[stage], phase ^ 1);
           unsigned char* st = ring + (size_t)stage * TC_STAGE;
@@ -178,7 +200,7 @@ __global__ void __launch_bounds__(TC_NT, 1) update_tc32_kernel(const UpdateArgs 
     int stage = 0, ab = 0;
     uint32_t phase = 0, aphase = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const TileInfo ti = tile_info<TC_BM, TC_BN>(a, t, tiles_per_sample, MASK);
+      const TileInfo ti = tile_info<TBM, TC_BN>(a, t, tiles_per_sample, MASK);
       if (!ti.valid) continue;
       mbar_wait(&tempty[ab], aphase ^ 1);  // the epilogue has drained this accumulator
       tc_fence_after();
@@ -214,18 +236,22 @@ __global__ void __launch_bounds__(TC_NT, 1) update_tc32_kernel(const UpdateArgs 
     int ab = 0;
     uint32_t aphase = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const TileInfo ti = tile_info<TC_BM, TC_BN>(a, t, tiles_per_sample, MASK);
+      const TileInfo ti = tile_info<TBM, TC_BN>(a, t, tiles_per_sample, MASK);
       if (!ti.valid) continue;
-      float* Cg = reinterpret_cast<float*>(a.C) + (int64_t)ti.s * a.strideC;
-      const int r = 32 * q + lane;
+      // TMEM lane R = 32 q + lane: real row R, or complex row R mod 64, component R / 64
+      const int R = 32 * q + lane;
+      const int r = CPLX ? (R & (TBM - 1)) : R;
       const int grow = ti.grow0 + r;
       const int cb = 64 * h;
-      float* p0 = Cg + grow + (int64_t)(ti.gcol0 + cb - ti.cshift) * a.ldc;
+      constexpr int ES = CPLX ? 2 : 1;  // floats per element
+      float* p0 = reinterpret_cast<float*>(a.C) +
+                  ES * ((int64_t)ti.s * a.strideC + grow + (int64_t)(ti.gcol0 + cb - ti.cshift) * a.ldc) +
+                  (CPLX ? R / TBM : 0);
       const bool row_in = r < ti.nrows;
       float cv[64];
 #pragma unroll
       for (int j = 0; j < 64; ++j)
-        cv[j] = (row_in && cb + j < ti.ncols && (!MASK || grow >= ti.gcol0 + cb + j)) ? p0[(int64_t)j * a.ldc] : 0.f;
+        cv[j] = (row_in && cb + j < ti.ncols && (!MASK || grow >= ti.gcol0 + cb + j)) ? p0[(int64_t)j * ES * a.ldc] : 0.f;
       mbar_wait(&tfull[ab], aphase);
       tc_fence_after();
 #pragma unroll
@@ -236,7 +262,8 @@ __global__ void __launch_bounds__(TC_NT, 1) update_tc32_kernel(const UpdateArgs 
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int c = cb + 32 * half + j;
-            if (c < ti.ncols && (!MASK || grow >= ti.gcol0 + c)) p0[(int64_t)(32 * half + j) * a.ldc] = cv[32 * half + j] - v[j];
+            if (c < ti.ncols && (!MASK || grow >= ti.gcol0 + c))
+              p0[(int64_t)(32 * half + j) * ES * a.ldc] = cv[32 * half + j] - v[j];
           }
         }
       }
@@ -254,30 +281,30 @@ __global__ void __launch_bounds__(TC_NT, 1) update_tc32_kernel(const UpdateArgs 
   }
 }
 
-// Scratch bytes the packed operands of an update need.
-size_t tc32_scratch_bytes(int rows, int cols, int K) {
-  const size_t nch = (size_t)(K + TC_KC - 1) / TC_KC;
-  const size_t tm = (size_t)(rows + TC_BM - 1) / TC_BM, tn = (size_t)(cols + TC_BN - 1) / TC_BN;
+// Scratch bytes the packed operands of an update need (complex: 64-row A images, K' = 2 K).
+size_t tc32_scratch_bytes(int rows, int cols, int K, bool cplx) {
+  const size_t nch = (size_t)((cplx ? 2 : 1) * K + TC_KC - 1) / TC_KC;
+  const int bm = cplx ? TC_BM / 2 : TC_BM;
+  const size_t tm = (size_t)(rows + bm - 1) / bm, tn = (size_t)(cols + TC_BN - 1) / TC_BN;
   return (tm + tn) * nch * 2 * TC_PART;
 }
 
-// Real single-precision updates on the tensor cores (3xTF32); a.tcs must hold tc32_scratch_bytes of
-// scratch for the packed operands.  One sample per launch (a.batch == 1); no block-cyclic mode.
-cudaError_t launch_update_tc32(UpdateArgs a, cudaStream_t s) {
-  if (a.rows <= 0 || a.cols <= 0 || a.K <= 0) return cudaSuccess;
-  if (a.conj || a.bnmajor || a.dscale || a.batch != 1 || a.bcc_P) return cudaErrorInvalidValue;
-  const size_t need = tc32_scratch_bytes(a.rows, a.cols, a.K);
-  if (!a.tcs || a.tcs_bytes < (int64_t)need) return cudaErrorInvalidValue;
-  a.tiles_m = (a.rows + TC_BM - 1) / TC_BM;
+template <bool CPLX>
+static cudaError_t launch_tc32_t(UpdateArgs a, cudaStream_t s) {
+  constexpr int TBM = CPLX ? TC_BM / 2 : TC_BM;
+  using E = typename std::conditional<CPLX, float2, float>::type;
+  a.tiles_m = (a.rows + TBM - 1) / TBM;
   a.tiles_n = (a.cols + TC_BN - 1) / TC_BN;
-  const int nch = (a.K + TC_KC - 1) / TC_KC;
+  const int nch = ((CPLX ? 2 : 1) * a.K + TC_KC - 1) / TC_KC;
   unsigned char* pa = reinterpret_cast<unsigned char*>(a.tcs);
   unsigned char* pb = pa + (size_t)a.tiles_m * nch * 2 * TC_PART;
   // the operand rows of the region: A rows [row0, row0 + rows), B rows [col0, col0 + cols)
-  const float* Ar = reinterpret_cast<const float*>(a.Aop) + a.row0;
-  const float* Br = reinterpret_cast<const float*>(a.Bop) + a.col0;
-  tc32_pack_kernel<<<dim3(a.tiles_m, nch), 256, 0, s>>>(Ar, a.lda, min(a.rows, a.a_rows - a.row0), a.K, nch, pa);
-  tc32_pack_kernel<<<dim3(a.tiles_n, nch), 256, 0, s>>>(Br, a.ldb, min(a.cols, a.b_rows - a.col0), a.K, nch, pb);
+  const E* Ar = reinterpret_cast<const E*>(a.Aop) + a.row0;
+  const E* Br = reinterpret_cast<const E*>(a.Bop) + a.col0;
+  tc32_pack_kernel<CPLX, true><<<dim3(a.tiles_m, nch), 256, 0, s>>>(Ar, a.lda, min(a.rows, a.a_rows - a.row0), a.K,
+                                                                    nch, pa);
+  tc32_pack_kernel<CPLX, false><<<dim3(a.tiles_n, nch), 256, 0, s>>>(Br, a.ldb, min(a.cols, a.b_rows - a.col0), a.K,
+                                                                     nch, pb);
   const long long per = a.tri ? (long long)a.tiles_m * (a.tiles_m + 1) / 2 : (long long)a.tiles_m * a.tiles_n;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -287,15 +314,25 @@ cudaError_t launch_update_tc32(UpdateArgs a, cudaStream_t s) {
   const size_t smem = (size_t)TC_STAGES * TC_STAGE + 1024;
   cudaError_t e;
   if (a.mask) {
-    e = cudaFuncSetAttribute(update_tc32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(update_tc32_kernel<true, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    update_tc32_kernel<true><<<(unsigned)g, TC_NT, smem, s>>>(a, pa, pb);
+    update_tc32_kernel<true, CPLX><<<(unsigned)g, TC_NT, smem, s>>>(a, pa, pb);
   } else {
-    e = cudaFuncSetAttribute(update_tc32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(update_tc32_kernel<false, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    update_tc32_kernel<false><<<(unsigned)g, TC_NT, smem, s>>>(a, pa, pb);
+    update_tc32_kernel<false, CPLX><<<(unsigned)g, TC_NT, smem, s>>>(a, pa, pb);
   }
   return cudaGetLastError();
+}
+
+// Single-precision updates on the tensor cores (3xTF32): real (HERM_S) or complex64 (LU_C, no
+// conjugation, no mask); a.tcs must hold tc32_scratch_bytes of scratch for the packed operands.  One
+// sample per launch (a.batch == 1); no block-cyclic mode.
+cudaError_t launch_update_tc32(UpdateArgs a, cudaStream_t s, bool cplx) {
+  if (a.rows <= 0 || a.cols <= 0 || a.K <= 0) return cudaSuccess;
+  if (a.conj || a.bnmajor || a.dscale || a.batch != 1 || a.bcc_P || (cplx && a.mask)) return cudaErrorInvalidValue;
+  if (!a.tcs || a.tcs_bytes < (int64_t)tc32_scratch_bytes(a.rows, a.cols, a.K, cplx)) return cudaErrorInvalidValue;
+  return cplx ? launch_tc32_t<true>(a, s) : launch_tc32_t<false>(a, s);
 }
 
 }  // namespace dpp

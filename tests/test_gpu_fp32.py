@@ -34,7 +34,8 @@ def _kernel(kind, n, seed):
     ("herm_s", 1000, 64, 1, 0), ("herm_s", 2125, 0, 1, 0), ("herm_s", 2125, 256, 1, 0),
     # the FP32 SIMT updates (DPP_FLAG_FP32_SIMT) instead of the default 3xTF32 tensor-core updates
     ("herm_s", 300, 0, 1, 2), ("herm_s", 2125, 0, 1, 2), ("herm_s", 1000, 64, 0, 2),
-    ("lu_c", 130, 0, 1, 0), ("lu_c", 600, 0, 1, 0), ("lu_c", 600, 32, 0, 0)])
+    ("lu_c", 130, 0, 1, 0), ("lu_c", 600, 0, 1, 0), ("lu_c", 600, 32, 0, 0), ("lu_c", 1100, 0, 1, 0),
+    ("lu_c", 600, 0, 1, 2), ("lu_c", 1100, 128, 1, 2)])
 def test_fp32_matches_fp32_oracle(oracle_mod, kind, n, nb, la, flags):
     K = _kernel(kind, n, n + 3)
     fn = oracle_mod.sample_herm_s if kind == "herm_s" else oracle_mod.sample_lu_c

@@ -44,17 +44,23 @@ def test_tensor_core_and_async_copy_in_sass(libpath):
     assert "DMMA.8x8x4" in out
     assert "UBLKCP" in out and "SYNCS" in out
     assert "LDGSTS" in out
+    # the fp32 updates on the 5th-generation tensor cores: tcgen05.mma (UTCHMMA), tcgen05.ld (LDTM)
+    assert "UTCHMMA" in out and "LDTM" in out
 
 
 def test_host_helpers():
     import paper_1905_00165_b200 as dpp
     assert dpp.dpp_version().startswith("dpp-b200")
-    # in-place calls need the per-sample state, the tile operators, D1 and two panel buffers
-    # (W21 = L21 D1, or U12^T for LU, in two pair buffers of two panels: ldk x nb each) -- no n x n buffer
+    # in-place calls need the per-sample state, the tile operators, D1 and the panel buffers
+    # (W21 = L21 D1, or U12^T for LU, in two group buffers of G = 3 panels: ldk x nb each) -- no n x n
+    # buffer
     ws = dpp.dpp_workspace_bytes(dpp.DPP_OP_HERM_D, 1, 16384)
-    assert 4 * 16384 * 128 * 8 < ws < 4 * 16384 * 128 * 8 + 400_000
+    assert 6 * 16384 * 128 * 8 < ws < 6 * 16384 * 128 * 8 + 400_000
     ws = dpp.dpp_workspace_bytes(dpp.DPP_OP_LU_Z, 1, 1000)
-    assert 4 * 1008 * 64 * 16 + 2 * 64 * 64 * 16 < ws < 4 * 1008 * 64 * 16 + 400_000
+    assert 6 * 1008 * 64 * 16 + 2 * 64 * 64 * 16 < ws < 6 * 1008 * 64 * 16 + 400_000
+    # the fp32 sampler's tensor-core updates add two scratch regions for their packed operands
+    assert dpp.dpp_workspace_bytes(dpp.DPP_OP_HERM_S, 1, 4096) > dpp.dpp_workspace_bytes(
+        dpp.DPP_OP_HERM_S, 1, 4096, dpp.make_opts(flags=dpp.DPP_FLAG_FP32_SIMT))
     assert dpp.dpp_workspace_bytes(dpp.DPP_OP_HERM_D | dpp.DPP_OP_BATCHED, 4, 100) >= 4 * 112 * 100 * 8
     assert dpp.dpp_workspace_bytes(dpp.DPP_OP_HERM_D, 1, 10, dpp.make_opts(nb=48)) == 0
     for n, nb, P in [(1000, 128, 3), (16384, 128, 8), (65536, 128, 8), (100, 128, 4), (0, 128, 2)]:

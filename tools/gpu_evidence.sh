@@ -13,3 +13,6 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-dist --streams 1"
 timeout 900 ncu --set full --clock-control none --import-source on --warp-sampling-interval 0 --cache-control none -k regex:"diag_rl_kernel" -s 40 -c 1 -o gpurun_out/prof_diag $CMD > gpurun_out/ncu_diag.log 2>&1
 tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log
+python tools/timeline.py > gpurun_out/timeline.json 2> gpurun_out/timeline.err
+timeout 600 python bench.py --workload aztec_c --steps 3 --warmup 2 > gpurun_out/bench_aztec_c.json 2>/dev/null
+timeout 600 python bench.py --workload crossover > gpurun_out/bench_crossover.json 2>/dev/null

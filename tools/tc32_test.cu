@@ -34,9 +34,9 @@ int main(int argc, char** argv) {
   dpp::UpdateArgs u{};
   u.Aop = dA; u.lda = M; u.Bop = dB; u.ldb = N; u.C = dC; u.ldc = M;
   u.a_rows = M; u.b_rows = N; u.K = K; u.rows = M; u.cols = N; u.batch = 1; u.vec = 1;
-  u.tcs_bytes = (int64_t)dpp::tc32_scratch_bytes(M, N, K);
+  u.tcs_bytes = (int64_t)dpp::tc32_scratch_bytes(M, N, K, false);
   cudaMalloc(&u.tcs, (size_t)u.tcs_bytes);
-  cudaError_t e = dpp::launch_update_tc32(u, 0);
+  cudaError_t e = dpp::launch_update_tc32(u, 0, false);
   cudaError_t e2 = cudaDeviceSynchronize();
   printf("launch %s sync %s\n", cudaGetErrorString(e), cudaGetErrorString(e2));
   std::vector<float> G(C.size());
