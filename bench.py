@@ -722,7 +722,7 @@ def extra_workload(args):
                     dtype="f64", samples_per_s=round(B * args.steps * world / (ms / 1e3), 2),
                     config={"workload": f"BASELINE configs[1]: UST of the 40x40 grid (n=3120, rank 1599), {B} "
                                         f"independent samples per GPU per step", "n": n, "global_batch": B * world,
-                            "nb": args.nb, "group": args.group or 2, "batch_chunk": min(B, args.batch_chunk),
+                            "nb": args.nb, "group": args.group or 3, "batch_chunk": min(B, args.batch_chunk),
                             "lookahead": args.lookahead, "seq_len": None,
                             "parallelism": f"dp{world} (independent samples)"},
                     all_samples_are_spanning_trees_with_1599_edges=ok,

@@ -76,10 +76,14 @@ typedef struct CUstream_st* dpp_stream_t; /* == cudaStream_t */
 #define DPP_FLAG_GENERIC_UPDATE 1u /* every update / panel GEMM on the cp.async fallback kernel
                                       (diagnostics: it is otherwise used only for operands that are
                                       not 16-byte aligned); same results up to rounding */
-#define DPP_FLAG_FP32_SIMT 2u      /* dpp_sample_herm_s*: the updates on the FP32 SIMT pipe (every
+#define DPP_FLAG_FP32_SIMT 2u      /* dpp_sample_herm_s / dpp_sample_lu_c: the updates on the FP32 SIMT pipe (every
                                       product and sum an fp32 operation) instead of the default
                                       3xTF32 split on the tcgen05 tensor cores (each product to
                                       ~2^-21 relative, fp32 accumulation) */
+#define DPP_FLAG_NO_SPLIT_CHAIN 4u /* schedule only (results bit-identical): keep the ungrouped
+                                      steps' panel and lookahead updates whole on the chain stream
+                                      instead of splitting off the next diagonal tile (see DESIGN §6,
+                                      "Split chain"); for measurements and tests */
 typedef struct {
   int32_t nb;            /* block size: 32, 64, 128 or 256 (0 = default: 128 real, 64 complex).
                             Blocks wider than the kind's tile (128 real, 64 complex) are factored
@@ -145,8 +149,11 @@ int dpp_sample_lu_z(int64_t n, dpp_complex_t* K, int64_t ld, uint64_t seed, uint
 /* ---- single precision (the paper's single-precision
  * runs) ------------------------------------------------
  * Same arguments, layout and semantics as dpp_sample_herm_d / dpp_sample_lu_z
- * with float / complex64 matrices, factored in fp32 (FP32 SIMT pipe: sm_100a
- * has no exact-fp32 tensor-core MMA).  Reading R19: the decision compares the
+ * with float / complex64 matrices, factored in fp32: the diagonal tiles on the
+ * FP32 SIMT pipe, the update GEMMs of unbatched calls on the tcgen05 tensor
+ * cores as a 3xTF32 split (complex64: through the real embedding) unless
+ * opts->flags has DPP_FLAG_FP32_SIMT (sm_100a has no exact-fp32 tensor-core
+ * MMA; batched calls always use the SIMT kernel).  Reading R19: the decision compares the
  * fp64 uniform with the fp32 pivot promoted to fp64; loglik is accumulated in
  * fp64 from the fp32 pivots.  K must be 4- (herm_s) / 8-byte (lu_c) aligned. */
 int dpp_sample_herm_s(int64_t n, float* K, int64_t ld, uint64_t seed, uint8_t* mask,

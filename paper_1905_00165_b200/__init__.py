@@ -38,6 +38,7 @@ class dpp_opts_t(ctypes.Structure):
 
 DPP_FLAG_GENERIC_UPDATE = 1
 DPP_FLAG_FP32_SIMT = 2
+DPP_FLAG_NO_SPLIT_CHAIN = 4
 
 
 class dpp_info_t(ctypes.Structure):

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libdpp_b200.so")
-SOURCES = ["diag.cu", "diag_rl.cu", "update.cu", "update_ws.cu", "update_simt.cu", "update_tc32.cu", "elementary.cu", "lensemble.cu", "driver.cu", "dist.cu"]
+SOURCES = ["diag.cu", "diag_rl.cu", "update.cu", "update_ws.cu", "update_simt.cu", "update_tc32.cu", "next_tile.cu", "elementary.cu", "lensemble.cu", "driver.cu", "dist.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -201,6 +201,7 @@ int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* const* K_local, int64_
   if (!comm || n < 0 || ld_local < std::max<int64_t>(n, 1)) return DPP_EINVAL;
   const int P = comm->nranks;
   const int nctx = comm->local ? P : 1;
+  NvtxRange call_range("dpp dist %s n=%lld P=%d", kind == HERM_D ? "herm_d" : "herm_z", (long long)n, P);
   for (int i = 0; i < nctx; ++i)
     if (!loglik[i] || (n > 0 && (!mask[i] || !K_local[i]))) return DPP_EINVAL;
   const int nb = dist_nb(kind, opts);
@@ -373,6 +374,7 @@ int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* const* K_local, int64_
 
   if (!la) {
     for (int64_t k = 0; k < nblk; ++k) {
+      NvtxRange step_range("dist step %lld", (long long)k);
       if (RankCtx* oc = owner_ctx(k)) {
         if ((rc = wait_receivers(*oc))) return rc;
         if ((rc = factor_block(*oc, k, st))) return rc;
@@ -389,6 +391,7 @@ int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* const* K_local, int64_
     for (int64_t k = 0; k < nblk; ++k) {
       const int64_t m2 = m2_of(k);
       if (m2 <= 0) break;
+      NvtxRange step_range("dist step %lld", (long long)k);
       const int64_t kn = k + 1;  // the lookahead block
       // phase 1 (every rank's S1): message buffer kn&1 was last read by the trailing update of
       // step k-1; the owner of kn updates block column kn with step k's panel and factors it

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -42,6 +43,7 @@ struct Opts {
   int64_t group_min_rows;  // -1: defaults; else group only while more than this many rows remain
   bool generic;          // DPP_FLAG_GENERIC_UPDATE
   bool fp32_simt;        // DPP_FLAG_FP32_SIMT
+  bool no_split;         // DPP_FLAG_NO_SPLIT_CHAIN
 };
 
 // opts->nb larger than the kind's tile (256 real; 128 or 256 complex) is the blocked algorithm with
@@ -58,6 +60,7 @@ int resolve_opts(Kind kind, const dpp_opts_t* o, Opts* r) {
   r->batch_chunk = o ? o->batch_chunk : 0;
   r->generic = o && (o->flags & DPP_FLAG_GENERIC_UPDATE);
   r->fp32_simt = o && (o->flags & DPP_FLAG_FP32_SIMT);
+  r->no_split = o && (o->flags & DPP_FLAG_NO_SPLIT_CHAIN);
   if (nb != 32 && nb != 64 && nb != 128 && nb != 256) return DPP_EINVAL;
   if (o && (o->group < 0 || o->group > 8)) return DPP_EINVAL;
   // G = 3 by default (round 2: C4 31.2 vs 30.8 TF/s with G = 2, UST 2675 vs 2643 samples/s,
@@ -134,8 +137,8 @@ WsLayout layout(Kind kind, int64_t chunk, int64_t n, const Opts& o, bool copies,
 
 // ---------------------------------------------------------------- stream pair per device
 struct DeviceStreams {
-  cudaStream_t s1 = nullptr, s2 = nullptr;
-  cudaEvent_t ev_start, ev_panel, ev_rest, ev_done1, ev_done2;
+  cudaStream_t s1 = nullptr, s2 = nullptr, s3 = nullptr;  // chain, trailing, split-off chain work
+  cudaEvent_t ev_start, ev_panel, ev_rest, ev_done1, ev_done2, ev_diag, ev_p0, ev_p1, ev_lr, ev_done3;
   std::recursive_mutex mu;
   bool init = false;
 };
@@ -167,7 +170,9 @@ int get_streams(DeviceStreams** out, cudaStream_t caller = nullptr) {
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return DPP_ECUDA;
     if (cudaStreamCreateWithPriority(&d.s1, cudaStreamNonBlocking, hi) != cudaSuccess) return DPP_ECUDA;
     if (cudaStreamCreateWithPriority(&d.s2, cudaStreamNonBlocking, lo) != cudaSuccess) return DPP_ECUDA;
-    for (cudaEvent_t* e : {&d.ev_start, &d.ev_panel, &d.ev_rest, &d.ev_done1, &d.ev_done2})
+    if (cudaStreamCreateWithPriority(&d.s3, cudaStreamNonBlocking, hi) != cudaSuccess) return DPP_ECUDA;
+    for (cudaEvent_t* e : {&d.ev_start, &d.ev_panel, &d.ev_rest, &d.ev_done1, &d.ev_done2, &d.ev_diag, &d.ev_p0,
+                           &d.ev_p1, &d.ev_lr, &d.ev_done3})
       if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return DPP_ECUDA;
     d.init = true;
   }
@@ -244,7 +249,11 @@ int device_sms() {
 // otherwise.  (Round 2: the (a) term had counted one column at K = nb whatever g -- a 4x
 // underestimate at the paired steps, which starved the next pair's chain of SMs: a timeline of one
 // C4 sample showed the trailing kernel idle 5.3 ms, mostly at those steps.)
-int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile, bool herm, int g = 1) {
+//
+// Split-chain steps (see run_blocked): the chain stream s1 carries only the diag tile, P0 and LT
+// (one tile each), s3 the one-wave launches P1 and LR beside the next diag tile, (b) the rest.
+// With the period T = max(chain, (b)'s tiles on SMs - R, P1 + LR on R - 1 SMs).
+int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile, bool herm, int g = 1, bool split = false) {
   const double side = (double)((m2 + tile - 1) / tile), side_b = (double)((m2 - jn + tile - 1) / tile);
   const double lu = herm ? 1.0 : 2.0;
   const double tb = (herm ? side_b * (side_b + 1) / 2 : side_b * side_b) * batch;  // (b) tiles
@@ -267,6 +276,17 @@ int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile, bool herm, int
   }
   int best = 8;
   double best_t = 1e300;
+  if (split) {
+    const double rest = side - 1.0;  // P1 / LR row tiles
+    for (int R = 4; R <= sms / 2; R += 2) {
+      const double t1 = diag_tiles + 1.0;
+      const double t2 = tb / (sms - R);
+      const double t3 = 2.0 * std::ceil(rest / (R - 1));
+      const double t = std::max(t1, std::max(t2, t3));
+      if (t < best_t - 1e-9) { best_t = t; best = R; }
+    }
+    return best;
+  }
   for (int R = 4; R <= sms / 2; R += 2) {
     const double t1 = g * diag_tiles + chain / R;
     const double t2 = g * tb / (sms - R);
@@ -311,17 +331,20 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
                 dpp_info_t* info, char* work, const WsLayout& L, cudaStream_t caller, bool map = false) {
   void* state = work + L.state_off;
   if (n == 0) { CK(launch_zero_state(state, loglik, info, batch, caller)); return DPP_OK; }
+  static const char* const kname[] = {"herm_d", "herm_z", "lu_z", "herm_s", "lu_c"};
+  NvtxRange call_range("dpp %s n=%lld batch=%d", kname[kind], (long long)n, batch);
   DeviceStreams* ds = nullptr;
   int rc = get_streams(&ds, caller);
   if (rc) return rc;
   std::lock_guard<std::recursive_mutex> lk(ds->mu);
   const int nb = o.nb;
   const bool la = o.lookahead > 0;
-  cudaStream_t s1 = la ? ds->s1 : caller, s2 = la ? ds->s2 : caller;
+  cudaStream_t s1 = la ? ds->s1 : caller, s2 = la ? ds->s2 : caller, s3 = la ? ds->s3 : caller;
   if (la) {
     CK(cudaEventRecord(ds->ev_start, caller));
     CK(cudaStreamWaitEvent(s1, ds->ev_start, 0));
     CK(cudaStreamWaitEvent(s2, ds->ev_start, 0));
+    CK(cudaStreamWaitEvent(s3, ds->ev_start, 0));
   }
   const size_t es = esize(kind);
   const bool herm = kind_herm(kind);
@@ -344,6 +367,8 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
   bool have_rest = false;
   int gpos = -1;            // position of the previous step in its group (-1: none)
   bool prev_glast = false;  // the previous step was the last of a group
+  bool lr_pending = false;  // the previous step's lookahead rows below its diagonal tile run on s3
+  bool used_s3 = false;
   const int sms = device_sms();
   // Head block: when nb does not divide n, the FIRST block takes the remainder (n mod nb) so that
   // every trailing region is a whole number of tiles (a ragged last block would leave a partly
@@ -360,6 +385,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
   for (int64_t j0 = 0; j0 < n; j0 += blk(j0), ++step) {
     const int jb = (int)blk(j0);
     const int64_t j1 = j0 + jb, m2 = n - j1;
+    NvtxRange step_range("step %d j0=%lld", step, (long long)j0);
     double* dvec = herm ? reinterpret_cast<double*>(work + L.d_off) + (size_t)(step & 1) * batch * nb : nullptr;
     // LU: U12^T (m2 x jb, ld = ldk, K-major GEMM operand); Hermitian: W21 = L21 D1 (same shape);
     // double-buffered like D1
@@ -385,6 +411,18 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       }
     }
     const bool glast = gp == G - 1, gnonlast = gp >= 0 && !glast;
+    // Split chain (ungrouped Hermitian steps of one fp64 sample): the only work the next diag tile
+    // waits for is the panel's first row tile P0 (the rows of the next block) and the lookahead
+    // update LT of the next diagonal tile; they stay on the chain stream s1, while the panel's other
+    // rows P1 and the lookahead update of the rows below the next tile LR run on s3 beside the next
+    // diag tile.  Same tiles, same arithmetic as the unsplit launches: bit-identical results.
+    // Only near the end (m2 <= 3072: the steps whose chain is the bound; above it the one-wave P1 /
+    // LR launches cost the trailing update more SMs than the chain saves -- measured on C4).
+    const bool split = la && !o.no_split && batch == 1 && herm && kind != HERM_S && gp < 0 && m2 > nb &&
+                       m2 <= 3072;
+    const int64_t jsp = std::min<int64_t>(nb, m2);  // rows of P0 / LT (= the ungrouped jn)
+    // real 128-blocks: P0 and LT as ONE single-CTA launch (next_tile.cu)
+    const bool fuse = split && kind == HERM_D && nb == 128 && jb == 128 && vec && !o.generic;
     char* const PH = WP + (size_t)(gp >= 0 ? gp * (strideU + nb) : (step % G) * strideU) * es;  // my slot
     char* const WG = WP + (size_t)(gp > 0 ? gp * nb : 0) * es;  // the stacked operand of panels 0..gp
     const int64_t jg0 = gp > 0 ? j0 - (int64_t)gp * nb : j0;  // the group's first column
@@ -404,10 +442,14 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       CK(launch_diag(kind, nb, d, s1));
     }
     if (m2 <= 0) break;
+    if (split) CK(cudaEventRecord(ds->ev_diag, s1));
+    // the panel reads this block column below the diagonal tile: the previous step's LR (s3)
+    if (lr_pending) { CK(cudaStreamWaitEvent(s1, ds->ev_lr, 0)); lr_pending = false; }
     // ---- stage 2: panel GEMMs with the tile operators (in place)
     {
       const double fl = (herm ? 1.0 : 2.0) * (double)m2 * jb * jb * cplx_mult(kind) * batch;  // TRSM count
-      ProfScope ps(1, fl, s1);
+      // (split: P1's share is bracketed on s3, P0's with the fused launch when there is one)
+      ProfScope ps(1, split ? (fuse ? 0.0 : fl * jsp / m2) : fl, s1);
       UpdateArgs p = base_update(kind, batch, vec);
       p.Aop = Ab + (size_t)(j1 + j0 * ld) * es; p.lda = ld; p.strideA = strideA;   // A21
       p.Bop = Bm; p.ldb = nb; p.strideB = L.strideM;
@@ -420,7 +462,21 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
         p.wout = grouping ? PH : UT; p.ldw = L.ldk; p.strideWo = grouping ? strideW : strideU;
         p.wscale = dvec; p.wsstride = nb;
       }
-      CK(upd(p, s1));
+      if (split) {
+        UpdateArgs p0 = p, p1 = p;
+        if (!fuse) {
+          p0.rows = (int)jsp;
+          CK(upd(p0, s1));
+          CK(cudaEventRecord(ds->ev_p0, s1));
+        }
+        CK(cudaStreamWaitEvent(s3, ds->ev_diag, 0));
+        p1.row0 = (int)jsp; p1.rows = (int)(m2 - jsp);
+        { ProfScope ps1(1, fl * (m2 - jsp) / m2, s3); CK(upd(p1, s3)); }
+        CK(cudaEventRecord(ds->ev_p1, s3));
+        used_s3 = true;
+      } else {
+        CK(upd(p, s1));
+      }
       if (!herm) {
         // U12 = L11^-1 A12 = A12 - Am A12 (Am = I - L11^-1), computed transposed so that every
         // operand is K-major:  U12^T = A12^T - A12^T Am^T  in the U12^T buffer, then copied back.
@@ -477,7 +533,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       CK(upd(u, s1));
       continue;
     }
-    CK(cudaEventRecord(ds->ev_panel, s1));
+    if (!split) CK(cudaEventRecord(ds->ev_panel, s1));
     if (copyback) {
       CK(cudaStreamWaitEvent(s2, ds->ev_panel, 0));
       ProfScope pa(4, 0.0, s2);
@@ -489,7 +545,33 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     // group's lookahead update and is not part of the previous trailing update)
     if (have_rest && !(gnonlast && (gp > 0 || prev_glast))) CK(cudaStreamWaitEvent(s1, ds->ev_rest, 0));
     prev_glast = glast;
-    {
+    if (split) {
+      // LT: the next diagonal tile (chain, s1); LR: the rows below it (s3, after P0 and P1)
+      UpdateArgs lt = u, lr = u;
+      lt.row0 = 0; lt.col0 = 0; lt.rows = (int)jsp; lt.cols = (int)jsp; lt.tri = 0;
+      if (fuse) {
+        NextTileArgs nt{};
+        nt.A21 = reinterpret_cast<double*>(Ab + (size_t)(j1 + j0 * ld) * es); nt.ld = ld;
+        nt.Bm = reinterpret_cast<const double*>(Bm); nt.ldm = nb; nt.d = dvec;
+        nt.W21 = reinterpret_cast<double*>(grouping ? PH : UT); nt.ldw = L.ldk;
+        nt.C = reinterpret_cast<double*>(Ab + (size_t)(j1 + j1 * ld) * es);
+        ProfScope ps(2, region_flops(kind, 0, 0, jsp, jsp, u.K) + (double)jsp * jb * jb, s1);
+        CK(launch_next_tile(nt, s1));
+        CK(cudaEventRecord(ds->ev_p0, s1));
+      } else {
+        ProfScope ps(2, region_flops(kind, 0, 0, jsp, jsp, u.K), s1);
+        CK(upd(lt, s1));
+      }
+      CK(cudaStreamWaitEvent(s3, ds->ev_p0, 0));
+      if (have_rest) CK(cudaStreamWaitEvent(s3, ds->ev_rest, 0));
+      lr.row0 = (int)jsp; lr.col0 = 0; lr.rows = (int)(m2 - jsp); lr.cols = (int)jsp; lr.tri = 0;
+      {
+        ProfScope ps(2, region_flops(kind, jsp, 0, m2 - jsp, jsp, u.K), s3);
+        CK(upd(lr, s3));
+      }
+      CK(cudaEventRecord(ds->ev_lr, s3));
+      lr_pending = true;
+    } else {
       UpdateArgs ua = u;
       ua.row0 = 0; ua.col0 = 0; ua.rows = (int)m2; ua.cols = jn; ua.tri = 0;
       double fl = region_flops(kind, 0, 0, m2, jn, ua.K);
@@ -505,12 +587,17 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     // (b) the rest [jn, m2)^2 on S2, persistently on the SMs the lookahead chain leaves free
     gpos = gp;  // a non-last position: the group's last step applies this step's trailing update
     if (m2 > jn && !gnonlast) {
-      CK(cudaStreamWaitEvent(s2, ds->ev_panel, 0));
+      if (split) {
+        CK(cudaStreamWaitEvent(s2, ds->ev_p0, 0));
+        CK(cudaStreamWaitEvent(s2, ds->ev_p1, 0));
+      } else {
+        CK(cudaStreamWaitEvent(s2, ds->ev_panel, 0));
+      }
       UpdateArgs ub = u;
       ub.row0 = jn; ub.col0 = jn; ub.rows = (int)(m2 - jn); ub.cols = (int)(m2 - jn);
       ub.tri = herm;
       if (vec)
-        ub.grid_limit = sms - reserve_sms(m2, jn, sms, batch, kind_cplx(kind) ? 64 : 128, herm, glast ? G : 1);
+        ub.grid_limit = sms - reserve_sms(m2, jn, sms, batch, kind_cplx(kind) ? 64 : 128, herm, glast ? G : 1, split);
       {
         ProfScope ps(3, region_flops(kind, jn, jn, m2 - jn, m2 - jn, ub.K) * batch, s2);
         CK(upd(ub, s2));
@@ -524,6 +611,10 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     CK(cudaEventRecord(ds->ev_done2, s2));
     CK(cudaStreamWaitEvent(caller, ds->ev_done1, 0));
     CK(cudaStreamWaitEvent(caller, ds->ev_done2, 0));
+    if (used_s3) {
+      CK(cudaEventRecord(ds->ev_done3, s3));
+      CK(cudaStreamWaitEvent(caller, ds->ev_done3, 0));
+    }
   }
   return DPP_OK;
 }

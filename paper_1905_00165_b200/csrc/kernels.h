@@ -3,8 +3,27 @@
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
+
+#include <cstdio>
 
 namespace dpp {
+
+// NVTX range (host side; a no-op unless a tool such as ncu --nvtx or nsys is attached): one per
+// sampler call and one per block step, so a timeline or an ncu --nvtx-include filter can tell the
+// steps' launches apart.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  template <class... T>
+  NvtxRange(const char* fmt, T... args) {
+    char b[96];
+    snprintf(b, sizeof b, fmt, args...);
+    nvtxRangePushA(b);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 enum Kind { HERM_D = 0, HERM_Z = 1, LU_Z = 2, HERM_S = 3, LU_C = 4 };  // _S/_C: single precision
 inline bool kind_herm(Kind k) { return k == HERM_D || k == HERM_Z || k == HERM_S; }
@@ -110,5 +129,18 @@ cudaError_t launch_copy_matrix(size_t es, const void* src, int64_t lds, int64_t 
                                int64_t strideD, int n, int batch, bool lower, cudaStream_t s);
 cudaError_t launch_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, double* u, cudaStream_t s);
 cudaError_t launch_zero_state(void* state, double* loglik, void* info, int batch, cudaStream_t s);
+
+// Split-chain step, real fp64, nb = 128 (next_tile.cu): the panel's first row tile P0
+// (L21_0 = A21_0 - A21_0 Bm^T in place, W21_0 = L21_0 D1 into its slot) and the lookahead update of
+// the next diagonal tile LT (lower triangle of C -= W21_0 L21_0^T), one CTA; bit-identical to the
+// two update-kernel launches it replaces.  16-byte aligned A21, Bm, ld, ldm.
+struct NextTileArgs {
+  double* A21; int64_t ld;       // 128 x 128 block (rows j1.., block column j0), in place
+  const double* Bm; int64_t ldm;  // the diag tile's panel operator (K-major)
+  const double* d;                // D1 (128)
+  double* W21; int64_t ldw;       // W21_0 destination (rows 0..127 of the panel slot)
+  double* C;                      // the next diagonal tile (ld)
+};
+cudaError_t launch_next_tile(const NextTileArgs& a, cudaStream_t s);
 
 }  // namespace dpp

@@ -226,6 +226,20 @@ def test_blocking_and_lookahead_invariance():
             assert np.max(np.abs(np.tril(F - ref[2]))) <= 1e-9
 
 
+@pytest.mark.parametrize("kind,n,nb", [("herm_d", 2125, 128), ("herm_d", 1130, 64), ("herm_z", 1111, 64),
+                                         ("herm_z", 700, 32)])
+def test_split_chain_bitwise(kind, n, nb):
+    """The split chain (P0 / LT on the chain stream, P1 / LR on a third stream) computes the same
+    tiles with the same arithmetic as the whole panel and lookahead launches: bit-identical mask,
+    loglik and factor, in place and batched (where it is off)."""
+    K = _kernel(kind, n, seed=n + 3)
+    a, Fa, _ = _gpu_single(kind, K, 8, dpp.make_opts(nb=nb))
+    b, Fb, _ = _gpu_single(kind, K, 8, dpp.make_opts(nb=nb, flags=dpp.DPP_FLAG_NO_SPLIT_CHAIN))
+    assert np.array_equal(a.mask.cpu().numpy(), b.mask.cpu().numpy())
+    assert float(a.loglik) == float(b.loglik)
+    assert np.array_equal(Fa, Fb)
+
+
 def test_determinism_bitwise():
     K = _kernel("herm_d", 700, seed=13)
     a, Fa, _ = _gpu_single("herm_d", K, 4)
@@ -254,6 +268,7 @@ def test_large_parity_2048(oracle_mod):
 # (256 real; 128 complex), which runs as grouped 128- (64-) wide sub-blocks.
 OPT_CASES = {
     "generic": dict(flags=1),
+    "no_split_chain": dict(flags=4),
     "unpaired": dict(group=1),
     "pair_all_sizes": dict(group=2, group_min_rows=-1),
     "group3": dict(group=3, group_min_rows=-1),

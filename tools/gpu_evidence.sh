@@ -16,3 +16,8 @@ tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log
 python tools/timeline.py > gpurun_out/timeline.json 2> gpurun_out/timeline.err
 timeout 600 python bench.py --workload aztec_c --steps 3 --warmup 2 > gpurun_out/bench_aztec_c.json 2>/dev/null
 timeout 600 python bench.py --workload crossover > gpurun_out/bench_crossover.json 2>/dev/null
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
+HCMD="python bench.py --workload herm_s --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_herm_s.csv $HCMD > gpurun_out/ncu_launch_hs.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --cache-control none --kernel-name-base demangled -k regex:"update_tc32_kernel" -s 40 -c 1 -o gpurun_out/prof_tc32 $HCMD > gpurun_out/ncu_tc32.log 2>&1
+echo done
