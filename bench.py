@@ -164,6 +164,7 @@ def main():
     ap.add_argument("--lookahead", type=int, default=1, help="ust: 0 = single stream")
     ap.add_argument("--nb", type=int, default=128, help="ust / herm_s: block size")
     ap.add_argument("--group", type=int, default=0, help="c4 / ust: dpp_opts_t.group (0 = library default)")
+    ap.add_argument("--flags", type=int, default=0, help="c4 / ust: extra dpp_opts_t.flags bits")
     ap.add_argument("--no-dist", action="store_true", help="c4: skip the configs[4] block-cyclic sub-record")
     ap.add_argument("--dist-n", type=int, default=65536, help="c4: n of the block-cyclic sub-record")
     ap.add_argument("--dist-steps", type=int, default=2, help="c4: timed samples of the block-cyclic sub-record")
@@ -207,7 +208,7 @@ def main():
 
     Kc = W.haar_kernel_torch(n, seed=KSEED, spectrum="beta")  # column-major storage (symmetric)
     torch.cuda.synchronize()
-    opts = dpp.make_opts(nb=NB, lookahead=1, group=args.group)
+    opts = dpp.make_opts(nb=NB, lookahead=1, group=args.group, flags=args.flags)
     op = dpp.DPP_OP_HERM_D | dpp.DPP_OP_BATCHED
     # consecutive steps rotate over three caller streams with three workspaces (--streams 3): the
     # library gives each caller stream its own internal stream pair, so one sample's copy and first
@@ -697,7 +698,7 @@ def extra_workload(args):
         Kc = torch.from_numpy(np.ascontiguousarray(K.T)).cuda()
         B = args.batch
         opts = dpp.make_opts(nb=args.nb, lookahead=args.lookahead, batch_chunk=min(B, args.batch_chunk),
-                             group=args.group)
+                             group=args.group, flags=args.flags)
         op = dpp.DPP_OP_HERM_D | dpp.DPP_OP_BATCHED
         NSU = args.ust_streams  # consecutive steps rotate over this many streams (batches in flight)
         works = [torch.empty(dpp.dpp_workspace_bytes(op, B, n, opts), dtype=torch.uint8, device="cuda")

@@ -71,6 +71,15 @@ template <> struct BlockAcc16<double> {
         for (int j = 0; j < 2; ++j) dmma884(c[i][j][0], c[i][j][1], a[i], b[j]);
     }
   }
+  // block -> C (the layout store() writes)
+  __device__ __forceinline__ void load(const double* C, int lane, int ldc = BLK_LD) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) c[i][j][e] = C[i * 8 + (lane >> 2) + (j * 8 + 2 * (lane & 3) + e) * ldc];
+  }
   // C -> block (neg: store -C)
   __device__ __forceinline__ void store(double* C, int lane, bool neg, int ldc = BLK_LD) const {
 #pragma unroll
