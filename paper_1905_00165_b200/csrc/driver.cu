@@ -27,6 +27,20 @@
 
 using namespace dpp;
 
+// schedule constants (compile-time; measured values, DESIGN.md §6 "Schedules tried")
+#ifndef DPP_DIAG_TILES
+#define DPP_DIAG_TILES 2.5        // one sample's diag tile in update-tile times (K = nb)
+#endif
+#ifndef DPP_DIAG_TILES_BATCH
+#define DPP_DIAG_TILES_BATCH 5.0  // the same in the batched cost model
+#endif
+#ifndef DPP_GROUP_MIN_ROWS
+#define DPP_GROUP_MIN_ROWS 6144   // 128-wide Hermitian blocks: no grouping at or below this many rows
+#endif
+#ifndef DPP_SPLIT_ROWS
+#define DPP_SPLIT_ROWS 3072       // split chain at or below this many trailing rows
+#endif
+
 namespace {
 
 constexpr size_t ALIGN = 256;
@@ -260,7 +274,7 @@ int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile, bool herm, int
   double diag_tiles, chain;
   if (batch == 1 && tile == 128) {
     // the diag tile in update-tile times (~49 us vs ~20-30 us per tile at K = nb)
-    diag_tiles = 2.5;
+    diag_tiles = DPP_DIAG_TILES;
     const double cols_a = (double)((jn + tile - 1) / tile);
     const double ta = lu * side * cols_a * g;                 // (a) now
     const double tp = lu * side_b;                            // one panel GEMM (K = nb)
@@ -271,7 +285,7 @@ int reserve_sms(int64_t m2, int jn, int sms, int batch, int tile, bool herm, int
     // with the chain's GEMMs) and the 64-wide complex tiles: the round-1 model, tuned on the UST
     // batch and the complex workloads (the corrected terms above cost 10 % on the UST batch and
     // 1.5-2.6 % on complex samples with three in flight; on one real C4 sample they save 1 ms)
-    diag_tiles = 5.0;
+    diag_tiles = DPP_DIAG_TILES_BATCH;
     chain = lu * side * batch + g * lu * side_b * batch;
   }
   int best = 8;
@@ -322,7 +336,7 @@ int64_t group_threshold(const Opts& o, bool herm, int batch) {
   if (o.group_min_rows >= 0) return o.group_min_rows;
   if (batch >= 8) return 0;
   if (!herm) return 8192;
-  return o.nb >= 128 ? 6144 : 0;
+  return o.nb >= 128 ? DPP_GROUP_MIN_ROWS : 0;
 }
 
 // Factors `batch` matrices A + s*strideA (in place), samples b0 + s.
@@ -378,7 +392,10 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
   // blocking does not change the sample.
   const int64_t rem = n % nb;
   const int64_t head = (n > nb && rem && rem % (int64_t)(16 / es) == 0) ? rem : 0;
-  const int gbase = head ? 1 : 0;  // groups are aligned after the head block
+  // With grouping the head block is position 0 of group 0 (its trailing update deferred like any
+  // non-last position: a separate K = head pass over the whole trailing matrix is HBM-bound -- the
+  // UST batch, n = 3120, spent 28 ms of a 381 ms step in it).  Position gp of a group starts at
+  // column offset goff(gp) from the group's first column (the head shifts group 0's later blocks).
   const int G = o.group;
   const int64_t gthr = group_threshold(o, herm, batch);
   auto blk = [&](int64_t j) -> int64_t { return (head && j == 0) ? head : std::min<int64_t>(nb, n - j); };
@@ -394,8 +411,10 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     // grouping: steps (G g .. G g + G-1) share the group buffer (g & 1) of G panels per sample
     const bool grouping = la && G > 1 && nb == (int)std::min<int64_t>(nb, n);
     const int64_t strideW = (int64_t)std::max(G, 2) * strideU;
-    const int gstep = step - gbase;  // (-1 for the head block: group buffer 1, unused by group 0)
-    char* WP = work + L.ut_off + (size_t)((gstep < 0 ? 1 : gstep / G) & 1) * batch * strideW * es;
+    const int gstep = step;
+    char* WP = work + L.ut_off + (size_t)((gstep / G) & 1) * batch * strideW * es;
+    const int64_t w0 = (head && gstep < G) ? head : nb;  // width of the group's position 0
+    auto goff = [&](int g) -> int64_t { return g == 0 ? 0 : w0 + (int64_t)(g - 1) * nb; };
     // group roles: a group starts at a step that is a multiple of G when all its G blocks are full
     // width, its last step has a trailing region of its own, and the trailing updates still dominate
     // (near the end the chain is the bound, and a group's G-wide lookahead update lengthens it).
@@ -419,13 +438,15 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     // Only near the end (m2 <= 3072: the steps whose chain is the bound; above it the one-wave P1 /
     // LR launches cost the trailing update more SMs than the chain saves -- measured on C4).
     const bool split = la && !o.no_split && batch == 1 && herm && kind != HERM_S && gp < 0 && m2 > nb &&
-                       m2 <= 3072;
+                       m2 <= DPP_SPLIT_ROWS;
     const int64_t jsp = std::min<int64_t>(nb, m2);  // rows of P0 / LT (= the ungrouped jn)
     // real 128-blocks: P0 and LT as ONE single-CTA launch (next_tile.cu)
     const bool fuse = split && kind == HERM_D && nb == 128 && jb == 128 && vec && !o.generic;
-    char* const PH = WP + (size_t)(gp >= 0 ? gp * (strideU + nb) : (step % G) * strideU) * es;  // my slot
+    // my slot: its columns at goff(gp) of the group buffer, shifted down by gp nb rows so that row
+    // r of the stacked operand is the same matrix row in every slot
+    char* const PH = WP + (size_t)(gp >= 0 ? goff(gp) * L.ldk + (int64_t)gp * nb : (step % G) * strideU) * es;
     char* const WG = WP + (size_t)(gp > 0 ? gp * nb : 0) * es;  // the stacked operand of panels 0..gp
-    const int64_t jg0 = gp > 0 ? j0 - (int64_t)gp * nb : j0;  // the group's first column
+    const int64_t jg0 = gp > 0 ? j0 - goff(gp) : j0;  // the group's first column
     bool copyback = false;  // LU: the U12^T -> A12 copy deferred to the trailing stream
     const char* cb_src = nullptr;
     char* cb_dst = nullptr;
@@ -523,7 +544,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       u.Bop = UT; u.ldb = L.ldk; u.strideB = strideU;  // U12^T (j, k), K-major
     }
     u.C = Ab + (size_t)(j1 + j1 * ld) * es; u.ldc = ld; u.strideC = strideA;
-    u.a_rows = (int)m2; u.b_rows = (int)m2; u.K = (gp > 0 ? gp * nb : 0) + jb;
+    u.a_rows = (int)m2; u.b_rows = (int)m2; u.K = (int)((gp > 0 ? goff(gp) : 0) + jb);
     // width of the lookahead region: the next block -- or, at the last step of a group, the next
     // group's G blocks, so the next group's whole diag/panel chain runs under this group's update
     const int jn = (int)std::min<int64_t>(glast ? (int64_t)G * nb : nb, m2);
