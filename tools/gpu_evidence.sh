@@ -21,7 +21,7 @@ nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -DDIAG_OLD -I includ
 CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-dist --streams 1"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on --warp-sampling-interval 0 --cache-control none -k regex:"diag_rl_kernel" -s 40 -c 1 -o gpurun_out/prof_diag $CMD > gpurun_out/ncu_diag.log 2>&1
-timeout 900 ncu --set full --clock-control none --cache-control none -k regex:"update_ws_kernel<0, 0, 0" -s 30 -c 3 -o gpurun_out/prof_panel $CMD > gpurun_out/ncu_panel.log 2>&1
+timeout 900 ncu --set full --clock-control none --cache-control none --kernel-name-base demangled -k regex:'update_ws_kernel<.bool.0, .bool.0, .bool.0' -s 30 -c 3 -o gpurun_out/prof_panel $CMD > gpurun_out/ncu_panel.log 2>&1
 HCMD="python bench.py --workload herm_s --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 timeout 900 ncu --set full --clock-control none --import-source on --cache-control none --kernel-name-base demangled -k regex:"update_tc32_kernel" -s 40 -c 1 -o gpurun_out/prof_tc32 $HCMD > gpurun_out/ncu_tc32.log 2>&1
 echo done
