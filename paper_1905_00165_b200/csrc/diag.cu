@@ -361,11 +361,12 @@ static cudaError_t launch_diag_t(const DiagArgs& a, cudaStream_t s) {
   return launch_diag_nt<T, HERM, NB, 256>(a, s);
 }
 
-cudaError_t launch_diag_rl(int nb, const DiagArgs& a, cudaStream_t s);
+cudaError_t launch_diag_rl(int nb, const DiagArgs& a, cudaStream_t s, bool fp32);
 
 cudaError_t launch_diag(Kind kind, int nb, const DiagArgs& a, cudaStream_t s) {
   // real symmetric 64- and 128-tiles: the blocked kernel of diag_rl.cu (warp sub-panels + DMMA)
-  if (kind == HERM_D && (nb == 64 || nb == 128)) return launch_diag_rl(nb, a, s);
+  if (kind == HERM_D && (nb == 64 || nb == 128)) return launch_diag_rl(nb, a, s, false);
+  if (kind == HERM_S && (nb == 64 || nb == 128)) return launch_diag_rl(nb, a, s, true);
   switch (kind) {
     case HERM_D:
       if (nb <= 32) return launch_diag_t<double, true, 32>(a, s);

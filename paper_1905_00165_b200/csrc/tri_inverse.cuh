@@ -144,15 +144,21 @@ template <typename T> struct BlockAccSimt {
   }
   __device__ __forceinline__ void mma(const T* A, const T* B, int lane, int lda = BLK_LD, int ldb = BLK_LD) {
 #pragma unroll 4
-    for (int k = 0; k < 16; ++k)
+    for (int k = 0; k < 16; ++k) {
+      T a[2], b[2][2];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const T a = A[i * 8 + (lane >> 2) + k * lda];
+      for (int i = 0; i < 2; ++i) a[i] = A[i * 8 + (lane >> 2) + k * lda];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) b[j][e] = B[k + (j * 8 + 2 * (lane & 3) + e) * ldb];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) c[i][j][e] = madd(c[i][j][e], a, B[k + (j * 8 + 2 * (lane & 3) + e) * ldb]);
-      }
+          for (int e = 0; e < 2; ++e) c[i][j][e] = madd(c[i][j][e], a[i], b[j][e]);
+    }
   }
   __device__ __forceinline__ void store(T* C, int lane, bool ng, int ldc = BLK_LD) const {
 #pragma unroll
@@ -162,6 +168,14 @@ template <typename T> struct BlockAccSimt {
 #pragma unroll
         for (int e = 0; e < 2; ++e)
           C[i * 8 + (lane >> 2) + (j * 8 + 2 * (lane & 3) + e) * ldc] = ng ? neg(c[i][j][e]) : c[i][j][e];
+  }
+  __device__ __forceinline__ void load(const T* C, int lane, int ldc = BLK_LD) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) c[i][j][e] = C[i * 8 + (lane >> 2) + (j * 8 + 2 * (lane & 3) + e) * ldc];
   }
 };
 template <> struct BlockAcc16<float> : BlockAccSimt<float> {};

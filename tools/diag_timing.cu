@@ -21,7 +21,10 @@ __device__ long long g_stamps[8][64];
 #include "kernels.h"
 #include "../paper_1905_00165_b200/csrc/diag_rl.cu"
 #ifdef DIAG_OLD
-#include "_old_diag_rl.cu"  // the previous kernel (a saved copy): bitwise A/B of every output
+#ifndef OLD_FILE
+#define OLD_FILE "_old_diag_rl.cu"
+#endif
+#include OLD_FILE  // the previous kernel (a saved copy): bitwise A/B of every output
 #endif
 
 template <class F>
@@ -88,7 +91,7 @@ int main(int argc, char** argv) {
     cudaMemcpy(m.data(), mask, m.size(), cudaMemcpyDeviceToHost);
     return std::make_pair(o, m);
   };
-  const float t_new = time_launch([&] { return dpp::launch_diag_rl(nb, d, 0); }, dA, dA0, bytes, reps);
+  const float t_new = time_launch([&] { return dpp::launch_diag_rl(nb, d, 0, false); }, dA, dA0, bytes, reps);
   auto out_new = outputs();
   long long st[8][64];
   cudaMemcpyFromSymbol(st, g_stamps, sizeof st);
