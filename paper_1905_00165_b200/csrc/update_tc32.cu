@@ -108,10 +108,9 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, float* v) {
 //   A3(i, 2k) = Im A, A3(i, 2k+1) = Re A,  B2(j, 2k) = Re B, B2(j, 2k+1) = Im B
 // -- an A image holds 64 complex rows (A2 above A3), a B image 128 complex rows; K' = 2 K.
 template <bool CPLX, bool AOP>
-__global__ void __launch_bounds__(256) tc32_pack_kernel(const void* Xv, int64_t ld, int rows, int K, int nch,
-                                                        unsigned char* dst) {
-  __shared__ __align__(16) float img[2][TC_BM * TC_KC];
-  const int t = blockIdx.x, c = blockIdx.y, tid = threadIdx.x;
+__device__ __forceinline__ void tc32_pack_tile(const void* Xv, int64_t ld, int rows, int K, int nch,
+                                               unsigned char* dst, int t, int c, float (*img)[TC_BM * TC_KC]) {
+  const int tid = threadIdx.x;
   constexpr int ROWS = (CPLX && AOP) ? TC_BM / 2 : TC_BM;  // operand rows per image
   for (int e = tid; e < TC_BM * TC_KC; e += 256) {
     const int r = e % TC_BM, k = e / TC_BM;  // consecutive threads: consecutive rows of one column
@@ -139,6 +138,19 @@ __global__ void __launch_bounds__(256) tc32_pack_kernel(const void* Xv, int64_t 
   float4* out = reinterpret_cast<float4*>(dst + ((size_t)t * nch + c) * 2 * TC_PART);
   const float4* in = reinterpret_cast<const float4*>(&img[0][0]);
   for (int e = tid; e < 2 * TC_BM * TC_KC / 4; e += 256) out[e] = in[e];
+}
+
+// Both operands of an update in one launch: CTAs x < tiles_a pack A's row tiles, the others B's
+// (two launches on the sampler's chain cost a launch each per update; the chain of the fp32
+// sampler is its bound).
+template <bool CPLX>
+__global__ void __launch_bounds__(256) tc32_pack_kernel(const void* Av, int64_t lda, int arows, const void* Bv,
+                                                        int64_t ldb, int brows, int K, int nch, int tiles_a,
+                                                        unsigned char* pa, unsigned char* pb) {
+  __shared__ __align__(16) float img[2][TC_BM * TC_KC];
+  const int t = blockIdx.x, c = blockIdx.y;
+  if (t < tiles_a) tc32_pack_tile<CPLX, true>(Av, lda, arows, K, nch, pa, t, c, img);
+  else tc32_pack_tile<CPLX, false>(Bv, ldb, brows, K, nch, pb, t - tiles_a, c, img);
 }
 
 }  // namespace
@@ -301,10 +313,8 @@ static cudaError_t launch_tc32_t(UpdateArgs a, cudaStream_t s) {
   // the operand rows of the region: A rows [row0, row0 + rows), B rows [col0, col0 + cols)
   const E* Ar = reinterpret_cast<const E*>(a.Aop) + a.row0;
   const E* Br = reinterpret_cast<const E*>(a.Bop) + a.col0;
-  tc32_pack_kernel<CPLX, true><<<dim3(a.tiles_m, nch), 256, 0, s>>>(Ar, a.lda, min(a.rows, a.a_rows - a.row0), a.K,
-                                                                    nch, pa);
-  tc32_pack_kernel<CPLX, false><<<dim3(a.tiles_n, nch), 256, 0, s>>>(Br, a.ldb, min(a.cols, a.b_rows - a.col0), a.K,
-                                                                     nch, pb);
+  tc32_pack_kernel<CPLX><<<dim3(a.tiles_m + a.tiles_n, nch), 256, 0, s>>>(
+      Ar, a.lda, min(a.rows, a.a_rows - a.row0), Br, a.ldb, min(a.cols, a.b_rows - a.col0), a.K, nch, a.tiles_m, pa, pb);
   const long long per = a.tri ? (long long)a.tiles_m * (a.tiles_m + 1) / 2 : (long long)a.tiles_m * a.tiles_n;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
