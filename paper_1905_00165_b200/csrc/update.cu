@@ -274,9 +274,12 @@ static cudaError_t launch_update_core(Kind kind, UpdateArgs a, cudaStream_t s, b
 cudaError_t launch_update(Kind kind, UpdateArgs a, cudaStream_t s) {
   if (a.rows <= 0 || a.cols <= 0 || a.K <= 0) return cudaSuccess;
   const bool ws = a.vec && !a.generic && kind != HERM_S && kind != LU_C;
-  // the second output W: fused into the warp-specialized panel kernel (no mask, Hermitian), else a
-  // column-scaling pass over the updated region
-  const bool fuse = a.wout && ws && !a.mask && a.bcc_P == 0 && (kind == HERM_D || kind == HERM_Z);
+  // the second output W: fused into the warp-specialized panel kernel (no mask, Hermitian) or the
+  // 3xTF32 kernel's epilogue (real single precision), else a column-scaling pass over the region
+  const bool tc32 = kind == HERM_S && a.vec && !a.generic && !a.fp32_simt && !a.dscale && !a.conj && !a.bnmajor &&
+                    a.batch == 1 && a.bcc_P == 0 && a.tcs &&
+                    a.tcs_bytes >= (int64_t)tc32_scratch_bytes(a.rows, a.cols, a.K, false);
+  const bool fuse = a.wout && !a.mask && a.bcc_P == 0 && ((ws && (kind == HERM_D || kind == HERM_Z)) || tc32);
   UpdateArgs k = a;
   if (!fuse) k.wout = nullptr;
   cudaError_t e = launch_update_core(kind, k, s, ws);

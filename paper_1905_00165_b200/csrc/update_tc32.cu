@@ -260,6 +260,15 @@ __global__ void __launch_bounds__(TC_NT, 1) update_tc32_kernel(const UpdateArgs 
                   ES * ((int64_t)ti.s * a.strideC + grow + (int64_t)(ti.gcol0 + cb - ti.cshift) * a.ldc) +
                   (CPLX ? R / TBM : 0);
       const bool row_in = r < ti.nrows;
+      // second output W = C_new diag(wscale) (the Hermitian panel's W21 = L21 D1), real unmasked only
+      float* w0 = nullptr;
+      const double* ws = nullptr;
+      if constexpr (!CPLX && !MASK) {
+        if (a.wout) {
+          w0 = reinterpret_cast<float*>(a.wout) + (int64_t)ti.s * a.strideWo + grow + (int64_t)(ti.gcol0 + cb) * a.ldw;
+          ws = a.wscale + (int64_t)ti.s * a.wsstride + ti.gcol0 + cb;
+        }
+      }
       float cv[64];
 #pragma unroll
       for (int j = 0; j < 64; ++j)
@@ -274,8 +283,11 @@ __global__ void __launch_bounds__(TC_NT, 1) update_tc32_kernel(const UpdateArgs 
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int c = cb + 32 * half + j;
-            if (c < ti.ncols && (!MASK || grow >= ti.gcol0 + c))
-              p0[(int64_t)(32 * half + j) * ES * a.ldc] = cv[32 * half + j] - v[j];
+            if (c < ti.ncols && (!MASK || grow >= ti.gcol0 + c)) {
+              const float nv = cv[32 * half + j] - v[j];
+              p0[(int64_t)(32 * half + j) * ES * a.ldc] = nv;
+              if (!CPLX && !MASK && w0) w0[(int64_t)(32 * half + j) * a.ldw] = scal(nv, __ldg(ws + 32 * half + j));
+            }
           }
         }
       }
