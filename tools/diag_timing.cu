@@ -53,6 +53,7 @@ int main(int argc, char** argv) {
   const int batch = argc > 1 ? atoi(argv[1]) : 1, reps = argc > 2 ? atoi(argv[2]) : 50;
   const int nb = argc > 3 ? atoi(argv[3]) : 128, ld = argc > 4 ? atoi(argv[4]) : nb, n = nb;
   const int forced = argc > 5 ? atoi(argv[5]) : 0;
+  const bool fp32 = argc > 6 && atoi(argv[6]) != 0;  // the single-precision instantiation (no A/B)
   // A = 0.5 I + 0.3/sqrt(n) * symmetric noise: pivots in (0, 1), roughly half kept
   std::vector<double> A((size_t)ld * n * batch, 0.0);
   srand(7);
@@ -73,7 +74,12 @@ int main(int argc, char** argv) {
   cudaMalloc(&Bm, (size_t)nb * nb * 8 * batch); cudaMalloc(&dvec, (size_t)nb * 8 * batch);
   cudaMalloc(&ll, 8 * batch); cudaMalloc(&mask, (size_t)n * batch); cudaMalloc(&state, 64 * (size_t)batch);
   cudaMalloc(&dF, F.size());
-  cudaMemcpy(dA0, A.data(), bytes, cudaMemcpyHostToDevice);
+  if (fp32) {  // the tile in fp32, in the first half of the buffers
+    std::vector<float> Af(A.begin(), A.end());
+    cudaMemcpy(dA0, Af.data(), Af.size() * 4, cudaMemcpyHostToDevice);
+  } else {
+    cudaMemcpy(dA0, A.data(), bytes, cudaMemcpyHostToDevice);
+  }
   cudaMemcpy(dF, F.data(), F.size(), cudaMemcpyHostToDevice);
   dpp::DiagArgs d{};
   d.A = dA; d.ld = ld; d.strideA = (int64_t)ld * n; d.n = n + 1;  // n + 1: not the last tile (ops formed)
@@ -91,12 +97,13 @@ int main(int argc, char** argv) {
     cudaMemcpy(m.data(), mask, m.size(), cudaMemcpyDeviceToHost);
     return std::make_pair(o, m);
   };
-  const float t_new = time_launch([&] { return dpp::launch_diag_rl(nb, d, 0, false); }, dA, dA0, bytes, reps);
+  const float t_new = time_launch([&] { return dpp::launch_diag_rl(nb, d, 0, fp32); }, dA, dA0, bytes, reps);
   auto out_new = outputs();
   long long st[8][64];
   cudaMemcpyFromSymbol(st, g_stamps, sizeof st);
   printf("{\"batch\": %d, \"nb\": %d, \"ld\": %d, \"forced\": %d, \"us_new\": %.2f", batch, nb, ld, forced, 1000 * t_new);
 #ifdef DIAG_OLD
+  if (!fp32) {
   const float t_old = time_launch([&] { return dpp_old::launch_diag_rl(nb, d, 0); }, dA, dA0, bytes, reps);
   auto out_old = outputs();
   size_t ndiff = 0;
@@ -105,6 +112,7 @@ int main(int argc, char** argv) {
   const bool mask_eq = out_new.second == out_old.second;
   printf(", \"us_old\": %.2f, \"words_differing_from_old\": %zu, \"mask_equal\": %s", 1000 * t_old, ndiff,
          mask_eq ? "true" : "false");
+  }
 #endif
   printf("}\n");
   if (batch > 1) return 0;
