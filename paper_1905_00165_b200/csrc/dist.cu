@@ -46,6 +46,13 @@ using namespace dpp;
 namespace {
 
 constexpr size_t ALIGN = 256;
+
+#ifndef DPP_DIST_PAIR_ROWS
+#define DPP_DIST_PAIR_ROWS 6144    // real: pairs while the pair's second step keeps more trailing rows
+#endif
+#ifndef DPP_DIST_PAIR_ROWS_Z
+#define DPP_DIST_PAIR_ROWS_Z 2048  // complex
+#endif
 inline size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
@@ -101,7 +108,7 @@ inline int64_t msg_pitch(int64_t m2) { return std::max<int64_t>(round_up(m2, 16)
 // work = [state][panel operator Bm: nb x nb][D1: nb][message buffer 0][message buffer 1]
 //        [W21 = L21 D1 of message 0][of message 1] (the pre-scaled A operand of the update)
 struct DistWs {
-  size_t state_off, bm_off, d_off, msg_off[2], w_off[2], total;
+  size_t state_off, bm_off, d_off, msg_off[2], w_off[2], gw_off[2], gl_off[2], total;
 };
 DistWs dist_ws(int64_t n, int nb, size_t es) {
   DistWs w;
@@ -118,6 +125,16 @@ DistWs dist_ws(int64_t n, int nb, size_t es) {
   for (int b = 0; b < 2; ++b) {
     w.w_off[b] = off;
     off = align_up(off + (size_t)ldw * nb * es);
+  }
+  // paired steps (see run_dist): the stacked operands of a pair's K = 2 nb update, double-buffered
+  // by pair -- W = [W21_a | W21_a+1] and (messages, P > 1) L = [L21_a | L21_a+1]
+  for (int b = 0; b < 2; ++b) {
+    w.gw_off[b] = off;
+    off = align_up(off + (size_t)ldw * 2 * nb * es);
+  }
+  for (int b = 0; b < 2; ++b) {
+    w.gl_off[b] = off;
+    off = align_up(off + (size_t)ldw * 2 * nb * es);
   }
   w.total = off;
   return w;
@@ -262,6 +279,34 @@ int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* const* K_local, int64_
     if (self_only) return {c.K + (size_t)(k * nb + jb_of(k) + (k / P) * nb * ld_local) * es, ld_local};
     return {msg_of(c, k) + M.w_off, msg_pitch(m2_of(k))};
   };
+  // Paired steps (the distributed form of the single-GPU driver's grouped updates, G = 2): the
+  // trailing update of an even step a is deferred and applied with step a+1's as ONE K = 2 nb pass
+  // over the stacked operands W = [W21_a | W21_a+1], L = [L21_a | L21_a+1] (the two slots of a
+  // pair buffer, slot 1 shifted down by nb rows so that row r of the stacked operand is the same
+  // matrix row in both); step a+1's lookahead covers the next pair's two block columns, so the
+  // next pair's first step runs beside the pair's update.  Pairs form from the start while the
+  // pair's second step keeps more than pair_rows trailing rows (near the end the chain bounds).
+  // (dpp_opts_t: group = 1 turns pairs off; group_min_rows > 0 sets the threshold, < 0 pairs at
+  // every size -- the tests' way to reach the paired schedule at small n)
+  const int64_t gmr = opts ? opts->group_min_rows : 0;
+  const int64_t pair_rows = std::max<int64_t>(
+      2 * nb, gmr < 0 ? 0 : gmr > 0 ? gmr : (kind == HERM_D ? DPP_DIST_PAIR_ROWS : DPP_DIST_PAIR_ROWS_Z));
+  const bool pairs = !(opts && opts->group == 1);
+  auto pos_of = [&](int64_t k) -> int {  // position of step k in its pair, -1: unpaired
+    if (!la || !pairs) return -1;
+    const int64_t a = k & ~(int64_t)1;
+    if (a + 1 >= nblk || jb_of(a + 1) != nb || m2_of(a + 1) <= pair_rows) return -1;
+    return (int)(k - a);
+  };
+  const int64_t ldg = msg_pitch(n);
+  auto gw_slot = [&](const RankCtx& c, int64_t k) {  // W21 of paired step k in its pair's W buffer
+    const int64_t p = k & 1;
+    return c.w + W.gw_off[(k >> 1) & 1] + (size_t)(p * nb * ldg + p * nb) * es;
+  };
+  auto gl_slot = [&](const RankCtx& c, int64_t k) {  // L21 of paired step k (messages only)
+    const int64_t p = k & 1;
+    return c.w + W.gl_off[(k >> 1) & 1] + (size_t)(p * nb * ldg + p * nb) * es;
+  };
   // owner(k): stage 1 + stage 2 of block k, packed into message k (stream s)
   auto factor_block = [&](RankCtx& c, int64_t k, cudaStream_t s) -> int {
     const int64_t j0 = k * nb;
@@ -312,8 +357,16 @@ int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* const* K_local, int64_
     }
     if (m2 > 0) {
       auto l = l21_of(c, k);
-      CK(launch_scale_cols(kind, l.first, l.second, 0, c.w + W.w_off[k & 1], msg_pitch(m2), 0,
-                           reinterpret_cast<const double*>(msg + M.d_off), 0, (int)m2, jb, 1, s));
+      const double* d1 = reinterpret_cast<const double*>(msg + M.d_off);
+      if (pos_of(k) >= 0) {
+        CK(launch_scale_cols(kind, l.first, l.second, 0, gw_slot(c, k), ldg, 0, d1, 0, (int)m2, jb, 1, s));
+        if (!self_only)
+          CK(cudaMemcpy2DAsync(gl_slot(c, k), (size_t)ldg * es, l.first, (size_t)l.second * es, (size_t)m2 * es,
+                               (size_t)jb, cudaMemcpyDeviceToDevice, s));
+      } else {
+        CK(launch_scale_cols(kind, l.first, l.second, 0, c.w + W.w_off[k & 1], msg_pitch(m2), 0, d1, 0, (int)m2,
+                             jb, 1, s));
+      }
     }
     return DPP_OK;
   };
@@ -355,12 +408,29 @@ int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* const* K_local, int64_
     if (m2 <= 0 || q_lo >= q_hi) return DPP_OK;
     auto l = l21_of(c, k);
     UpdateArgs u{};
-    u.Aop = c.w + W.w_off[k & 1]; u.lda = msg_pitch(m2);  // W21 = L21 D1
-    u.Bop = l.first; u.ldb = l.second; u.mask = 1;         // L21 (conjugated on load for complex)
+    const int pk = pos_of(k);
+    int K = jb;
+    if (pk == 1) {
+      // the pair (k-1, k): K = 2 nb over the stacked operands from row j1 of step k (slot 0 shifted)
+      u.Aop = c.w + W.gw_off[(k >> 1) & 1] + (size_t)nb * es; u.lda = ldg;
+      if (self_only) {  // one rank: blocks k-1 and k are adjacent local columns
+        u.Bop = c.K + (size_t)(j1 + (k - 1) * nb * ld_local) * es; u.ldb = ld_local;
+      } else {
+        u.Bop = c.w + W.gl_off[(k >> 1) & 1] + (size_t)nb * es; u.ldb = ldg;
+      }
+      K = 2 * nb;
+    } else if (pk == 0) {
+      u.Aop = gw_slot(c, k); u.lda = ldg;                  // W21 of step k alone
+      u.Bop = l.first; u.ldb = l.second;
+    } else {
+      u.Aop = c.w + W.w_off[k & 1]; u.lda = msg_pitch(m2);  // W21 = L21 D1
+      u.Bop = l.first; u.ldb = l.second;                    // L21 (conjugated on load for complex)
+    }
+    u.mask = 1;
     u.conj = kind == HERM_Z;
     u.C = c.K + (size_t)j1 * es;  // local column 0, A22 row 0
     u.ldc = ld_local;
-    u.a_rows = (int)m2; u.b_rows = (int)m2; u.K = jb; u.batch = 1; u.vec = vec ? 1 : 0;
+    u.a_rows = (int)m2; u.b_rows = (int)m2; u.K = K; u.batch = 1; u.vec = vec ? 1 : 0;
     u.row0 = 0; u.rows = (int)m2; u.col0 = 0; u.cols = (int)m2; u.tri = 0;
     u.bcc_P = P; u.bcc_r = c.r; u.bcc_nb = nb; u.bcc_q0 = (int)q_lo; u.bcc_j1 = j1;
     u.tiles_n = (int)(q_hi - q_lo);
@@ -393,23 +463,33 @@ int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* const* K_local, int64_
       if (m2 <= 0) break;
       NvtxRange step_range("dist step %lld", (long long)k);
       const int64_t kn = k + 1;  // the lookahead block
+      const int pk = pos_of(k);
       // phase 1 (every rank's S1): message buffer kn&1 was last read by the trailing update of
-      // step k-1; the owner of kn updates block column kn with step k's panel and factors it
+      // step k-1; the owner of kn updates block column kn with step k's panel and factors it.  The
+      // first step of a pair needs no wait: its lookahead block was covered by the previous pair's
+      // lookahead update and is not part of that pair's trailing update (which reads pair buffers
+      // only); the second step of a pair also brings block kn+1 up to date for the next pair.
       for (auto& c : R) {
-        if (k > 0) CK(cudaStreamWaitEvent(c.s1, c.rs->ev_rest, 0));
+        if (k > 0 && !(pk == 0 && pos_of(k - 1) == 1)) CK(cudaStreamWaitEvent(c.s1, c.rs->ev_rest, 0));
         if (c.r == (int)(kn % P)) {
-          if ((rc = update(c, k, kn / P, 1, 0, c.s1))) return rc;  // block column kn with step k's panel
+          if ((rc = update(c, k, kn / P, 1, 0, c.s1))) return rc;  // block column kn with step k's panel(s)
           if ((rc = wait_receivers(c))) return rc;
           if ((rc = factor_block(c, kn, c.s1))) return rc;
         }
+        if (pk == 1 && kn + 1 < nblk && c.r == (int)((kn + 1) % P))
+          if ((rc = update(c, k, (kn + 1) / P, 1, 0, c.s1))) return rc;  // block column kn+1, the pair
       }
       // phase 2: the exchange of message kn
       if ((rc = exchange(kn, true))) return rc;
       // phase 3 (S2): the rest of step k's trailing update (message k: ev_msg of the last step)
       for (auto& c : R) {
+        if (pk == 0) {  // deferred to the pair's second step
+          CK(cudaEventRecord(c.rs->ev_msg, c.s1));  // message kn (exchange issued above)
+          continue;
+        }
         const bool own_next = c.r == (int)(kn % P);
         CK(cudaStreamWaitEvent(c.s2, c.rs->ev_msg, 0));
-        const int64_t q_lo = own_next ? kn / P + 1 : first_after(c, k);
+        const int64_t q_lo = pk == 1 ? first_after(c, kn + 1) : own_next ? kn / P + 1 : first_after(c, k);
         int reserve = 0;
         if (!comm->local) {
           if (own_next) {

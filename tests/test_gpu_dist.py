@@ -21,8 +21,15 @@ if not torch.cuda.is_available():
 import paper_1905_00165_b200 as dpp  # noqa: E402
 from paper_1905_00165_b200 import dist as D  # noqa: E402
 
+# la = 2: lookahead with paired steps at every size (dpp_opts_t.group_min_rows < 0; by default pairs
+# form only while more than 6144 / 2048 trailing rows remain, beyond these sizes)
 CASES = [("herm_d", n, la) for n in (1, 128, 300, 1000, 2049) for la in (1, 0)] + \
-        [("herm_z", n, la) for n in (1, 64, 200, 777) for la in (1, 0)]
+        [("herm_z", n, la) for n in (1, 64, 200, 777) for la in (1, 0)] + \
+        [("herm_d", 1000, 2), ("herm_d", 2049, 2), ("herm_d", 640, 2), ("herm_z", 777, 2), ("herm_z", 450, 2)]
+
+
+def _dist_opts(la):
+    return dpp.make_opts(lookahead=1, group_min_rows=-1) if la == 2 else dpp.make_opts(lookahead=la)
 
 
 @pytest.mark.parametrize("kind,n,la", CASES)
@@ -39,7 +46,7 @@ def test_dist_world1_matches_oracle(oracle_mod, kind, n, la):
         ll = torch.empty((), dtype=torch.float64, device="cuda")
         info = torch.empty(32, dtype=torch.uint8, device="cuda")
         op = dpp.DPP_OP_HERM_Z if cplx else dpp.DPP_OP_HERM_D
-        opts = dpp.make_opts(lookahead=la)
+        opts = _dist_opts(la)
         work = torch.empty(dpp.dpp_dist_workspace_bytes(op, n, 1, opts), dtype=torch.uint8, device="cuda")
         fn = dpp.dpp_sample_herm_z_dist if cplx else dpp.dpp_sample_herm_d_dist
         fn(comm, n, loc, loc.shape[1], 5, mask, ll, info, opts, work)
@@ -101,8 +108,8 @@ def test_dist_full_size_bench_configuration(oracle_mod, kind, n):
     check_decisions(mask.cpu().numpy(), d.cpu().numpy(), 0, 0, oracle_mod)
 
 
-LOCAL_CASES = [("herm_d", n, P, la) for n, P in ((1000, 2), (2049, 3), (1300, 4), (129, 2)) for la in (1, 0)] + \
-              [("herm_z", n, P, la) for n, P in ((777, 2), (640, 3), (450, 4)) for la in (1, 0)]
+LOCAL_CASES = [("herm_d", n, P, la) for n, P in ((1000, 2), (2049, 3), (1300, 4), (129, 2)) for la in (1, 0, 2)] + \
+              [("herm_z", n, P, la) for n, P in ((777, 2), (640, 3), (450, 4)) for la in (1, 0, 2)]
 
 
 @pytest.mark.parametrize("kind,n,P,la", LOCAL_CASES)
@@ -116,7 +123,7 @@ def test_dist_virtual_ranks_match_oracle(oracle_mod, kind, n, P, la):
     o = (oracle_mod.sample_herm_z if cplx else oracle_mod.sample_herm_d)(K, 7, 0)
     Kc = torch.from_numpy(np.ascontiguousarray(K.T)).cuda()
     locs = [D.to_local(Kc, n, nb, P, r) for r in range(P)]
-    res = D.sample_local(locs, n, 7, complex_=cplx, opts=dpp.make_opts(lookahead=la))
+    res = D.sample_local(locs, n, 7, complex_=cplx, opts=_dist_opts(la))
     for r in range(P):
         compare_masks(res["masks"][r].cpu().numpy(), o)
     infos = dpp.Sample(res["masks"], res["loglik"], res["info"]).info_dicts()
@@ -129,16 +136,19 @@ def test_dist_virtual_ranks_match_oracle(oracle_mod, kind, n, P, la):
             assert abs(infos[r]["min_abs_pivot"] - o.min_abs_pivot) <= 1e-9 * np.max(np.abs(K))
 
 
-def test_dist_virtual_ranks_bitwise_vs_one_rank():
+@pytest.mark.parametrize("paired", [False, True])
+def test_dist_virtual_ranks_bitwise_vs_one_rank(paired):
     """The decomposition does not change the arithmetic of any element: P = 1, 2, 4 give bit-identical
-    masks, logliks and factors (each trailing element sees the same sequence of K = nb updates)."""
+    masks, logliks and factors (each trailing element sees the same sequence of K = nb updates, or of
+    K = 2 nb updates of the paired steps: the same stacked operands whether L21 is read in place or
+    from the messages)."""
     n, nb = 1500, 128
     K = W.haar_kernel(n, seed=41)
     Kc = torch.from_numpy(np.ascontiguousarray(K.T)).cuda()
     ref = None
     for P in (1, 2, 4):
         locs = [D.to_local(Kc, n, nb, P, r) for r in range(P)]
-        res = D.sample_local(locs, n, 3)
+        res = D.sample_local(locs, n, 3, opts=_dist_opts(2) if paired else None)
         F = D.from_local(locs, n, nb, P, Kc)
         cur = (res["masks"][0].clone(), res["loglik"][0].clone(), torch.tril(F))
         if ref is None:
