@@ -47,11 +47,14 @@ namespace {
 
 constexpr size_t ALIGN = 256;
 
-#ifndef DPP_DIST_PAIR_ROWS
-#define DPP_DIST_PAIR_ROWS 6144    // real: pairs while the pair's second step keeps more trailing rows
+#ifndef DPP_DIST_GROUP
+#define DPP_DIST_GROUP 3           // default G of the grouped block steps
 #endif
-#ifndef DPP_DIST_PAIR_ROWS_Z
-#define DPP_DIST_PAIR_ROWS_Z 2048  // complex
+#ifndef DPP_DIST_GROUP_ROWS
+#define DPP_DIST_GROUP_ROWS 6144    // real: groups while the group's last step keeps more trailing rows
+#endif
+#ifndef DPP_DIST_GROUP_ROWS_Z
+#define DPP_DIST_GROUP_ROWS_Z 2048  // complex
 #endif
 inline size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
@@ -110,7 +113,7 @@ inline int64_t msg_pitch(int64_t m2) { return std::max<int64_t>(round_up(m2, 16)
 struct DistWs {
   size_t state_off, bm_off, d_off, msg_off[2], w_off[2], gw_off[2], gl_off[2], total;
 };
-DistWs dist_ws(int64_t n, int nb, size_t es) {
+DistWs dist_ws(int64_t n, int nb, size_t es, int G) {
   DistWs w;
   const int64_t ldw = msg_pitch(n);  // the largest pitch (step 0 has m2 < n)
   MsgLayout m = msg_layout(nb);
@@ -126,15 +129,16 @@ DistWs dist_ws(int64_t n, int nb, size_t es) {
     w.w_off[b] = off;
     off = align_up(off + (size_t)ldw * nb * es);
   }
-  // paired steps (see run_dist): the stacked operands of a pair's K = 2 nb update, double-buffered
-  // by pair -- W = [W21_a | W21_a+1] and (messages, P > 1) L = [L21_a | L21_a+1]
+  // grouped steps (see run_dist): the stacked operands of a group's K = G nb update, double-buffered
+  // by group -- W = [W21_a | .. | W21_a+G-1] and (messages, P > 1) L = [L21_a | .. | L21_a+G-1]
+  const int g = std::max(G, 1);
   for (int b = 0; b < 2; ++b) {
     w.gw_off[b] = off;
-    off = align_up(off + (size_t)ldw * 2 * nb * es);
+    off = align_up(off + (G > 1 ? (size_t)ldw * g * nb * es : 0));
   }
   for (int b = 0; b < 2; ++b) {
     w.gl_off[b] = off;
-    off = align_up(off + (size_t)ldw * 2 * nb * es);
+    off = align_up(off + (G > 1 ? (size_t)ldw * g * nb * es : 0));
   }
   w.total = off;
   return w;
@@ -174,6 +178,13 @@ int dist_nb(Kind kind, const dpp_opts_t* opts) {
   const int def = kind == HERM_D ? 128 : 64;  // = the update kernel's tile width (bcc mode needs BN == nb)
   const int nb = (opts && opts->nb) ? opts->nb : def;
   return nb == def ? nb : -1;
+}
+
+// G: the trailing updates of G consecutive block steps applied as one K = G nb pass (dpp_opts_t.group:
+// 0 = default 3, 1 = off, up to 4); -1 if out of range
+int dist_group(const dpp_opts_t* opts) {
+  const int g = (opts && opts->group) ? opts->group : DPP_DIST_GROUP;
+  return (g >= 1 && g <= 4) ? g : -1;
 }
 
 int device_sms() {
@@ -230,7 +241,9 @@ int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* const* K_local, int64_
   const double range_tol = (opts && opts->range_tol > 0) ? opts->range_tol : 1e-8;
   const uint8_t* forced = opts ? opts->forced : nullptr;
   const bool la = !opts || opts->lookahead != 0;
-  const DistWs W = dist_ws(n, nb, es);
+  const int G = dist_group(opts);
+  if (G < 0) return DPP_EINVAL;
+  const DistWs W = dist_ws(n, nb, es, G);
   for (int i = 0; i < nctx; ++i)
     if (!work[i] || work_bytes < W.total || reinterpret_cast<uintptr_t>(work[i]) % ALIGN) return DPP_EWORKSPACE;
   if (n == 0) {
@@ -279,33 +292,34 @@ int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* const* K_local, int64_
     if (self_only) return {c.K + (size_t)(k * nb + jb_of(k) + (k / P) * nb * ld_local) * es, ld_local};
     return {msg_of(c, k) + M.w_off, msg_pitch(m2_of(k))};
   };
-  // Paired steps (the distributed form of the single-GPU driver's grouped updates, G = 2): the
-  // trailing update of an even step a is deferred and applied with step a+1's as ONE K = 2 nb pass
-  // over the stacked operands W = [W21_a | W21_a+1], L = [L21_a | L21_a+1] (the two slots of a
-  // pair buffer, slot 1 shifted down by nb rows so that row r of the stacked operand is the same
-  // matrix row in both); step a+1's lookahead covers the next pair's two block columns, so the
-  // next pair's first step runs beside the pair's update.  Pairs form from the start while the
-  // pair's second step keeps more than pair_rows trailing rows (near the end the chain bounds).
-  // (dpp_opts_t: group = 1 turns pairs off; group_min_rows > 0 sets the threshold, < 0 pairs at
-  // every size -- the tests' way to reach the paired schedule at small n)
+  // Grouped steps (the distributed form of the single-GPU driver's grouped updates, G = 3 by
+  // default): the trailing updates of steps a .. a+G-1 are deferred to the group's last step and
+  // applied as ONE K = G nb pass over the stacked operands W = [W21_a | .. | W21_a+G-1],
+  // L = [L21_a | .. | L21_a+G-1] (the slots of a group buffer, slot p shifted down by p nb rows so
+  // that row r of the stacked operand is the same matrix row in every slot); step a+p's lookahead
+  // update of block a+p+1 takes the panels a .. a+p (K = (p+1) nb), and the group's last step
+  // updates the next group's G block columns, so the next group's steps run beside the group's
+  // trailing update.  Groups form from the start while the group's last step keeps more than
+  // group_rows trailing rows (near the end the chain bounds).
+  // (dpp_opts_t: group = 1 turns groups off; group_min_rows > 0 sets the threshold, < 0 groups at
+  // every size -- the tests' way to reach the grouped schedule at small n)
   const int64_t gmr = opts ? opts->group_min_rows : 0;
-  const int64_t pair_rows = std::max<int64_t>(
-      2 * nb, gmr < 0 ? 0 : gmr > 0 ? gmr : (kind == HERM_D ? DPP_DIST_PAIR_ROWS : DPP_DIST_PAIR_ROWS_Z));
-  const bool pairs = !(opts && opts->group == 1);
-  auto pos_of = [&](int64_t k) -> int {  // position of step k in its pair, -1: unpaired
-    if (!la || !pairs) return -1;
-    const int64_t a = k & ~(int64_t)1;
-    if (a + 1 >= nblk || jb_of(a + 1) != nb || m2_of(a + 1) <= pair_rows) return -1;
+  const int64_t group_rows = std::max<int64_t>(
+      (int64_t)G * nb, gmr < 0 ? 0 : gmr > 0 ? gmr : (kind == HERM_D ? DPP_DIST_GROUP_ROWS : DPP_DIST_GROUP_ROWS_Z));
+  auto pos_of = [&](int64_t k) -> int {  // position of step k in its group, -1: ungrouped
+    if (!la || G < 2) return -1;
+    const int64_t a = k / G * G;
+    if (a + G - 1 >= nblk || jb_of(a + G - 1) != nb || m2_of(a + G - 1) <= group_rows) return -1;
     return (int)(k - a);
   };
   const int64_t ldg = msg_pitch(n);
-  auto gw_slot = [&](const RankCtx& c, int64_t k) {  // W21 of paired step k in its pair's W buffer
-    const int64_t p = k & 1;
-    return c.w + W.gw_off[(k >> 1) & 1] + (size_t)(p * nb * ldg + p * nb) * es;
+  auto gw_slot = [&](const RankCtx& c, int64_t k) {  // W21 of grouped step k in its group's W buffer
+    const int64_t p = k % G;
+    return c.w + W.gw_off[(k / G) & 1] + (size_t)(p * nb * ldg + p * nb) * es;
   };
-  auto gl_slot = [&](const RankCtx& c, int64_t k) {  // L21 of paired step k (messages only)
-    const int64_t p = k & 1;
-    return c.w + W.gl_off[(k >> 1) & 1] + (size_t)(p * nb * ldg + p * nb) * es;
+  auto gl_slot = [&](const RankCtx& c, int64_t k) {  // L21 of grouped step k (messages only)
+    const int64_t p = k % G;
+    return c.w + W.gl_off[(k / G) & 1] + (size_t)(p * nb * ldg + p * nb) * es;
   };
   // owner(k): stage 1 + stage 2 of block k, packed into message k (stream s)
   auto factor_block = [&](RankCtx& c, int64_t k, cudaStream_t s) -> int {
@@ -410,15 +424,16 @@ int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* const* K_local, int64_
     UpdateArgs u{};
     const int pk = pos_of(k);
     int K = jb;
-    if (pk == 1) {
-      // the pair (k-1, k): K = 2 nb over the stacked operands from row j1 of step k (slot 0 shifted)
-      u.Aop = c.w + W.gw_off[(k >> 1) & 1] + (size_t)nb * es; u.lda = ldg;
-      if (self_only) {  // one rank: blocks k-1 and k are adjacent local columns
-        u.Bop = c.K + (size_t)(j1 + (k - 1) * nb * ld_local) * es; u.ldb = ld_local;
+    if (pk >= 1) {
+      // the group's steps k-pk .. k: K = (pk+1) nb over the stacked operands from row j1 of step k
+      // (the slots' common row: slot 0 shifted by pk nb rows)
+      u.Aop = c.w + W.gw_off[(k / G) & 1] + (size_t)pk * nb * es; u.lda = ldg;
+      if (self_only) {  // one rank: the group's blocks are adjacent local columns
+        u.Bop = c.K + (size_t)(j1 + (k - pk) * nb * ld_local) * es; u.ldb = ld_local;
       } else {
-        u.Bop = c.w + W.gl_off[(k >> 1) & 1] + (size_t)nb * es; u.ldb = ldg;
+        u.Bop = c.w + W.gl_off[(k / G) & 1] + (size_t)pk * nb * es; u.ldb = ldg;
       }
-      K = 2 * nb;
+      K = (pk + 1) * nb;
     } else if (pk == 0) {
       u.Aop = gw_slot(c, k); u.lda = ldg;                  // W21 of step k alone
       u.Bop = l.first; u.ldb = l.second;
@@ -465,31 +480,35 @@ int run_dist(Kind kind, dpp_comm_t comm, int64_t n, void* const* K_local, int64_
       const int64_t kn = k + 1;  // the lookahead block
       const int pk = pos_of(k);
       // phase 1 (every rank's S1): message buffer kn&1 was last read by the trailing update of
-      // step k-1; the owner of kn updates block column kn with step k's panel and factors it.  The
-      // first step of a pair needs no wait: its lookahead block was covered by the previous pair's
-      // lookahead update and is not part of that pair's trailing update (which reads pair buffers
-      // only); the second step of a pair also brings block kn+1 up to date for the next pair.
+      // step k-1; the owner of kn updates block column kn with step k's panel(s) and factors it.
+      // A group's non-last steps need no wait: their lookahead blocks were covered by the previous
+      // group's lookahead update and are not part of its trailing update (which reads group
+      // buffers only); a group's last step also brings the next group's other blocks up to date.
+      const bool glast = pk == G - 1;
       for (auto& c : R) {
-        if (k > 0 && !(pk == 0 && pos_of(k - 1) == 1)) CK(cudaStreamWaitEvent(c.s1, c.rs->ev_rest, 0));
+        if (k > 0 && !(pk >= 0 && !glast && (pk > 0 || pos_of(k - 1) == G - 1)))
+          CK(cudaStreamWaitEvent(c.s1, c.rs->ev_rest, 0));
         if (c.r == (int)(kn % P)) {
           if ((rc = update(c, k, kn / P, 1, 0, c.s1))) return rc;  // block column kn with step k's panel(s)
           if ((rc = wait_receivers(c))) return rc;
           if ((rc = factor_block(c, kn, c.s1))) return rc;
         }
-        if (pk == 1 && kn + 1 < nblk && c.r == (int)((kn + 1) % P))
-          if ((rc = update(c, k, (kn + 1) / P, 1, 0, c.s1))) return rc;  // block column kn+1, the pair
+        if (glast)
+          for (int64_t b = kn + 1; b < kn + G && b < nblk; ++b)
+            if (c.r == (int)(b % P))
+              if ((rc = update(c, k, b / P, 1, 0, c.s1))) return rc;  // the next group's block columns
       }
       // phase 2: the exchange of message kn
       if ((rc = exchange(kn, true))) return rc;
       // phase 3 (S2): the rest of step k's trailing update (message k: ev_msg of the last step)
       for (auto& c : R) {
-        if (pk == 0) {  // deferred to the pair's second step
+        if (pk >= 0 && !glast) {  // deferred to the group's last step
           CK(cudaEventRecord(c.rs->ev_msg, c.s1));  // message kn (exchange issued above)
           continue;
         }
         const bool own_next = c.r == (int)(kn % P);
         CK(cudaStreamWaitEvent(c.s2, c.rs->ev_msg, 0));
-        const int64_t q_lo = pk == 1 ? first_after(c, kn + 1) : own_next ? kn / P + 1 : first_after(c, k);
+        const int64_t q_lo = glast ? first_after(c, k + G) : own_next ? kn / P + 1 : first_after(c, k);
         int reserve = 0;
         if (!comm->local) {
           if (own_next) {
@@ -618,7 +637,9 @@ size_t dpp_dist_workspace_bytes(int op, int64_t n, int nranks, const dpp_opts_t*
   const Kind kind = k == DPP_OP_HERM_D ? HERM_D : HERM_Z;
   const int nb = dist_nb(kind, opts);
   if (nb < 0) return 0;
-  return dist_ws(n, nb, kind == HERM_D ? 8 : 16).total;
+  const int G = dist_group(opts);
+  if (G < 0) return 0;
+  return dist_ws(n, nb, kind == HERM_D ? 8 : 16, G).total;
 }
 
 int64_t dpp_dist_message_bytes(int op, int64_t n, int nranks, int64_t k) {

@@ -21,11 +21,12 @@ if not torch.cuda.is_available():
 import paper_1905_00165_b200 as dpp  # noqa: E402
 from paper_1905_00165_b200 import dist as D  # noqa: E402
 
-# la = 2: lookahead with paired steps at every size (dpp_opts_t.group_min_rows < 0; by default pairs
-# form only while more than 6144 / 2048 trailing rows remain, beyond these sizes)
+# la = 2: lookahead with grouped steps (G = 3) at every size (dpp_opts_t.group_min_rows < 0; by
+# default groups form only while more than 6144 / 2048 trailing rows remain, beyond these sizes)
 CASES = [("herm_d", n, la) for n in (1, 128, 300, 1000, 2049) for la in (1, 0)] + \
         [("herm_z", n, la) for n in (1, 64, 200, 777) for la in (1, 0)] + \
-        [("herm_d", 1000, 2), ("herm_d", 2049, 2), ("herm_d", 640, 2), ("herm_z", 777, 2), ("herm_z", 450, 2)]
+        [("herm_d", 1000, 2), ("herm_d", 2049, 2), ("herm_d", 640, 2), ("herm_d", 1300, 2), ("herm_z", 777, 2),
+         ("herm_z", 450, 2), ("herm_z", 1000, 2)]
 
 
 def _dist_opts(la):
@@ -136,7 +137,7 @@ def test_dist_virtual_ranks_match_oracle(oracle_mod, kind, n, P, la):
             assert abs(infos[r]["min_abs_pivot"] - o.min_abs_pivot) <= 1e-9 * np.max(np.abs(K))
 
 
-@pytest.mark.parametrize("paired", [False, True])
+@pytest.mark.parametrize("paired", [False, True, 2])
 def test_dist_virtual_ranks_bitwise_vs_one_rank(paired):
     """The decomposition does not change the arithmetic of any element: P = 1, 2, 4 give bit-identical
     masks, logliks and factors (each trailing element sees the same sequence of K = nb updates, or of
@@ -148,7 +149,8 @@ def test_dist_virtual_ranks_bitwise_vs_one_rank(paired):
     ref = None
     for P in (1, 2, 4):
         locs = [D.to_local(Kc, n, nb, P, r) for r in range(P)]
-        res = D.sample_local(locs, n, 3, opts=_dist_opts(2) if paired else None)
+        opts = (dpp.make_opts(group=2, group_min_rows=-1) if paired == 2 else _dist_opts(2)) if paired else None
+        res = D.sample_local(locs, n, 3, opts=opts)
         F = D.from_local(locs, n, nb, P, Kc)
         cur = (res["masks"][0].clone(), res["loglik"][0].clone(), torch.tril(F))
         if ref is None:
