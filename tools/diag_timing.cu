@@ -12,7 +12,7 @@
 #include <utility>
 #include <vector>
 
-__device__ long long g_stamps[8][64];
+__device__ long long g_stamps[16][64];
 #define DIAG_STAMP(slot)                                                                          \
   do {                                                                                            \
     if (blockIdx.y == 0 && (threadIdx.x & 31) == 0) g_stamps[threadIdx.x >> 5][(slot)] = clock64(); \
@@ -99,7 +99,7 @@ int main(int argc, char** argv) {
   };
   const float t_new = time_launch([&] { return dpp::launch_diag_rl(nb, d, 0, fp32); }, dA, dA0, bytes, reps);
   auto out_new = outputs();
-  long long st[8][64];
+  long long st[16][64];
   cudaMemcpyFromSymbol(st, g_stamps, sizeof st);
   printf("{\"batch\": %d, \"nb\": %d, \"ld\": %d, \"forced\": %d, \"us_new\": %.2f", batch, nb, ld, forced, 1000 * t_new);
 #ifdef DIAG_OLD
@@ -116,28 +116,29 @@ int main(int argc, char** argv) {
 #endif
   printf("}\n");
   if (batch > 1) return 0;
+  const int NW = dpp::RL_NWARP;
   const long long t0 = st[0][30];
   printf("# clocks from kernel entry (warp 0); slots: 0 copies issued, 1 tile loaded, per sub-panel P: 2+3P S1 done, "
          "3+3P after barrier, 4+3P S2/S3 done; 28 end\n");
   for (int P = 0; P < nb / 16; ++P) {
     const long long start = P == 0 ? st[0][1] : st[0][4 + 3 * (P - 1)];
     long long oth = 0;
-    for (int w = 1; w < 8; ++w) {
+    for (int w = 1; w < NW; ++w) {
       const long long t = st[w][2 + 3 * P] - start;
       oth = t > oth ? t : oth;
     }
     long long upd = 0, s2 = 0;
-    for (int w = 1; w < 8; ++w) {
+    for (int w = 1; w < NW; ++w) {
       const long long t = st[w][40 + P] - start;
       upd = t > upd ? t : upd;
     }
-    for (int w = 0; w < 8; ++w) {
+    for (int w = 0; w < NW; ++w) {
       const long long t = st[w][48 + P] - st[0][3 + 3 * P];
       s2 = t > s2 ? t : s2;
     }
     if (P >= 1) {
       printf("   workers (from phase start): ");
-      for (int w = 1; w < 8; ++w)
+      for (int w = 1; w < NW; ++w)
         printf(" w%d: updates %5lld end %5lld |", w, st[w][40 + P] - start, st[w][2 + 3 * P] - start);
       printf("\n");
     }
@@ -146,9 +147,9 @@ int main(int argc, char** argv) {
            st[0][4 + 3 * P] - st[0][32 + P], st[0][4 + 3 * P] - start);
   }
   long long endmax = 0;
-  for (int w = 0; w < 8; ++w) endmax = st[w][28] - t0 > endmax ? st[w][28] - t0 : endmax;
+  for (int w = 0; w < NW; ++w) endmax = st[w][28] - t0 > endmax ? st[w][28] - t0 : endmax;
   printf("load %lld  end stage %lld (per warp:", st[0][1] - t0, endmax - (st[0][4 + 3 * (nb / 16 - 1)] - t0));
-  for (int w = 0; w < 8; ++w) printf(" %lld", st[w][28] - st[0][4 + 3 * (nb / 16 - 1)]);
+  for (int w = 0; w < NW; ++w) printf(" %lld", st[w][28] - st[0][4 + 3 * (nb / 16 - 1)]);
   printf(")  total %lld cycles\n", endmax);
   return 0;
 }
