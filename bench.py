@@ -596,7 +596,8 @@ def dist_record(args, world, rank, dist):
         flops = n ** 3 / 3.0
         msg = sum(D.message_bytes(n, nb, k) for k in range((n + nb - 1) // nb)) if world > 1 else 0
         rec = {"workload": f"BASELINE configs[4]: real K n={n}, lam~U(0,1), ONE sample factored 1D block-column-"
-                           f"cyclic over {world} GPU(s), nb={nb}, depth-1 lookahead, NCCL broadcast per block step "
+                           f"cyclic over {world} GPU(s), nb={nb}, depth-1 lookahead, trailing updates of G = 3 block steps "
+                           f"grouped, NCCL broadcast per block step "
                            f"({'none at one rank' if world == 1 else 'live rows only'})",
                "n": n, "ranks": world, "scaling": "strong", "ms_per_sample": round(ms, 2),
                "value": round(flops / (ms / 1e3) / 1e9, 2), "unit": UNIT,
@@ -1056,7 +1057,8 @@ def extra_workload(args):
                     config={"workload": f"BASELINE configs[4]: dense {'complex Hermitian' if cplx else 'real-symmetric'} "
                                         f"K=Q diag(lam) Q^H, lam~U(0,1), n={n}, ONE sample per step factored 1D "
                                         f"block-column-cyclic over {world} GPU(s) (NCCL broadcast of each panel, "
-                                        f"depth-1 lookahead); step includes restoring the local columns",
+                                        f"depth-1 lookahead, trailing updates of G = 3 block steps grouped); step includes restoring the "
+                                        f"local columns",
                             "n": n, "nb": nb, "global_batch": 1, "seq_len": None, "parallelism": f"bcc{world}"},
                     restore_copy_ms_per_step=round(copy_ms / args.steps, 3),
                     value_excluding_restore=round(flops / ((ms - copy_ms) / 1e3) / 1e9, 2),
