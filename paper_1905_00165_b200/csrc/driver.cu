@@ -342,7 +342,8 @@ int64_t group_threshold(const Opts& o, bool herm, int batch) {
 // Factors `batch` matrices A + s*strideA (in place), samples b0 + s.
 int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_t strideA, int batch,
                 uint64_t seed, uint64_t b0, uint8_t* mask, const uint8_t* forced, double* loglik,
-                dpp_info_t* info, char* work, const WsLayout& L, cudaStream_t caller, bool map = false) {
+                dpp_info_t* info, char* work, const WsLayout& L, cudaStream_t caller, bool map = false,
+                const void* dsrc = nullptr, int64_t dld = 0, int64_t dstride = 0) {
   void* state = work + L.state_off;
   if (n == 0) { CK(launch_zero_state(state, loglik, info, batch, caller)); return DPP_OK; }
   static const char* const kname[] = {"herm_d", "herm_z", "lu_z", "herm_s", "lu_c"};
@@ -377,6 +378,33 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
   };
   void* Bm = work + L.bm_off;
   void* Am = work + L.am_off;
+  // Deferred copy (dsrc != null: the batched entry points with a device kernel K at dsrc, leading
+  // dimension dld, stride dstride): instead of copying K's lower triangle into the workspace before
+  // the factorization, columns [0, copied) are valid in the workspace and the first update launch
+  // touching a block column range at `copied` reads its C values from K itself (UpdateArgs::csrc)
+  // and writes the workspace -- the lookahead updates of the first block columns and the first
+  // trailing update (the rest of the matrix), so only the first block column is ever copied.  Any
+  // other first touch copies the columns it needs beforehand (ensure_cols).  Hermitian
+  // warp-specialized path only (its updates never write above the diagonal; the sampler reads only
+  // the lower triangle).
+  int64_t copied = dsrc ? 0 : n;
+  auto ensure_cols = [&](int64_t c1, cudaStream_t s) -> int {
+    if (c1 <= copied) return DPP_OK;
+    ProfScope pa(4, 0.0, s);
+    CK(launch_copy_matrix(esize(kind), dsrc, dld, dstride, A, ld, strideA, (int)n, batch, true, s, (int)copied,
+                          (int)c1));
+    copied = c1;
+    return DPP_OK;
+  };
+  // a launch whose C region starts at column c0 (and row c0) and ends at column c1: read from K if
+  // nothing in [c0, c1) has been touched yet
+  auto defer_to = [&](UpdateArgs& ua, int64_t c0, int64_t c1) {
+    if (copied != c0 || !vec || o.generic) return false;
+    ua.csrc = reinterpret_cast<const char*>(dsrc) + (size_t)(c0 + c0 * dld) * esize(kind);
+    ua.ldcs = dld; ua.strideCs = dstride;
+    copied = c1;
+    return true;
+  };
   int step = 0;
   bool have_rest = false;
   int gpos = -1;            // position of the previous step in its group (-1: none)
@@ -457,6 +485,9 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     d.mask = mask; d.forced = forced; d.state = state; d.loglik = loglik; d.info = info;
     d.tie_tol = o.tie_tol; d.range_tol = o.range_tol; d.batch = batch; d.map = map ? 1 : 0;
     d.need_ops = m2 > 0; d.Bm = Bm; d.Am = Am; d.dvec = dvec; d.ldm = nb; d.strideM = L.strideM;
+    // the diag tile and the panel read block column j0; a split step's LT / LR (s3, ordered after P0
+    // only) also the next block's columns, copied here ahead of everything the step launches
+    if ((rc = ensure_cols(split ? j1 + jsp : j1, s1))) return rc;
     {
       const double fl = (herm ? 1.0 : 2.0) * jb * (double)jb * jb / 3.0 * cplx_mult(kind) * batch;
       ProfScope ps(0, fl, s1);
@@ -550,6 +581,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     const int jn = (int)std::min<int64_t>(glast ? (int64_t)G * nb : nb, m2);
     if (!la) {
       u.row0 = 0; u.col0 = 0; u.rows = (int)m2; u.cols = (int)m2; u.tri = herm;
+      if (!defer_to(u, j1, n) && (rc = ensure_cols(n, s1))) return rc;
       ProfScope ps(3, region_flops(kind, 0, 0, m2, m2, jb) * batch, s1);
       CK(upd(u, s1));
       continue;
@@ -595,6 +627,7 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
     } else {
       UpdateArgs ua = u;
       ua.row0 = 0; ua.col0 = 0; ua.rows = (int)m2; ua.cols = jn; ua.tri = 0;
+      if (!defer_to(ua, j1, j1 + jn) && (rc = ensure_cols(j1 + jn, s1))) return rc;
       double fl = region_flops(kind, 0, 0, m2, jn, ua.K);
       if (!herm && m2 > jn) fl += region_flops(kind, 0, jn, jn, m2 - jn, jb);
       ProfScope ps(2, fl * batch, s1);
@@ -617,6 +650,11 @@ int run_blocked(Kind kind, const Opts& o, int64_t n, void* A, int64_t ld, int64_
       UpdateArgs ub = u;
       ub.row0 = jn; ub.col0 = jn; ub.rows = (int)(m2 - jn); ub.cols = (int)(m2 - jn);
       ub.tri = herm;
+      if (defer_to(ub, j1 + jn, n)) {
+        ub.csrc = reinterpret_cast<const char*>(ub.csrc) - (size_t)(jn + jn * dld) * esize(kind);  // origin at u.C's
+      } else if ((rc = ensure_cols(n, s2))) {
+        return rc;
+      }
       if (vec)
         ub.grid_limit = sms - reserve_sms(m2, jn, sms, batch, kind_cplx(kind) ? 64 : 128, herm, glast ? G : 1, split);
       {
@@ -687,6 +725,12 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
   // one 2-D DMA copy per 128-column block of rows [c, n) -- about half the bytes of the full
   // matrix (this halves the host->device time of the _host entry points).
   const bool lower = kind_herm(kind);
+  // device kernels of the fp64 Hermitian samplers: the copy into the workspace is deferred into the
+  // first updates (run_blocked), which read K directly -- needs the lookahead schedule, the
+  // warp-specialized update kernel and 16-byte aligned K columns
+  const bool defer = !host && n > 0 && (kind == HERM_D || kind == HERM_Z) && o.lookahead > 0 && !o.generic &&
+                     reinterpret_cast<uintptr_t>(K) % 16 == 0 && ((size_t)ld * es) % 16 == 0 &&
+                     ((size_t)strideK * es) % 16 == 0 && ((size_t)L.ldk * es) % 16 == 0;
   auto h2d = [&](char* dst, const char* src) -> int {
     if (!lower) {
       CK(cudaMemcpy2DAsync(dst, (size_t)L.ldk * es, src, (size_t)ld * es, (size_t)n * es, (size_t)n, ck, st));
@@ -714,7 +758,7 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
         for (int s = 0; s < cb; ++s)
           if ((rc = h2d(Kc + (size_t)s * L.strideK * es,
                         reinterpret_cast<const char*>(K) + (size_t)(strideK * (c0 + s)) * es))) return rc;
-      } else {
+      } else if (!defer) {
         ProfScope pa(4, 0.0, st);
         CK(launch_copy_matrix(es, reinterpret_cast<const char*>(K) + (size_t)(strideK * c0) * es, ld,
                               strideK, Kc, L.ldk, L.strideK, (int)n, cb, lower, st));
@@ -724,7 +768,9 @@ int sample_batched(Kind kind, int64_t batch, int64_t n, const void* K, int64_t l
     double* llk = host ? reinterpret_cast<double*>(w + L.ll_off) : loglik + c0;
     dpp_info_t* ifo = host ? (info ? reinterpret_cast<dpp_info_t*>(w + L.info_off) : nullptr) : (info ? info + c0 : nullptr);
     const uint8_t* fz = o.forced ? o.forced + c0 * n : nullptr;
-    rc = run_blocked(kind, o, n, Kc, L.ldk, L.strideK, cb, seed, b0 + (uint64_t)c0, mk, fz, llk, ifo, w, L, st);
+    rc = run_blocked(kind, o, n, Kc, L.ldk, L.strideK, cb, seed, b0 + (uint64_t)c0, mk, fz, llk, ifo, w, L, st,
+                     false, defer ? reinterpret_cast<const char*>(K) + (size_t)(strideK * c0) * es : nullptr, ld,
+                     strideK);
     if (rc) return rc;
     if (host) {
       if (n > 0) CK(cudaMemcpyAsync(mask + c0 * n, mk, (size_t)cb * n, cudaMemcpyDeviceToHost, st));

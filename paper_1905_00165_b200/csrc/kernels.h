@@ -108,6 +108,12 @@ struct UpdateArgs {
   int64_t ldw, strideWo;
   const double* wscale;
   int64_t wsstride;
+  // optional source of the C values READ (element (i, j) at i + j*ldcs, stride strideCs per sample;
+  // results are still written to C): a region's first update reads the caller's kernel directly
+  // instead of a workspace copy made beforehand (driver.cu, deferred copy).  Warp-specialized fast
+  // kernel only: launch_update rejects it for the others.
+  const void* csrc;
+  int64_t ldcs, strideCs;
 };
 
 cudaError_t launch_diag(Kind kind, int nb, const DiagArgs& a, cudaStream_t s);
@@ -124,9 +130,11 @@ cudaError_t launch_transpose(size_t es, const void* src, int64_t lds, int64_t st
 cudaError_t launch_scale_cols(Kind kind, const void* L, int64_t ldl, int64_t strideL, void* W, int64_t ldw,
                               int64_t strideW, const double* d, int64_t strideD, int rows, int cols, int batch,
                               cudaStream_t s);
-// dst <- src for `batch` n x n column-major matrices of es-byte elements (lower: rows >= column only)
+// dst <- src for columns [c0, c1) (c1 < 0: n) of `batch` n x n column-major matrices of es-byte
+// elements (lower: rows >= column only)
 cudaError_t launch_copy_matrix(size_t es, const void* src, int64_t lds, int64_t strideS, void* dst, int64_t ldd,
-                               int64_t strideD, int n, int batch, bool lower, cudaStream_t s);
+                               int64_t strideD, int n, int batch, bool lower, cudaStream_t s, int c0 = 0,
+                               int c1 = -1);
 cudaError_t launch_uniforms(uint64_t seed, uint64_t j0, uint64_t b, int64_t count, double* u, cudaStream_t s);
 cudaError_t launch_zero_state(void* state, double* loglik, void* info, int batch, cudaStream_t s);
 

@@ -209,23 +209,66 @@ cudaError_t launch_scale_cols(Kind kind, const void* L, int64_t ldl, int64_t str
   return cudaGetLastError();
 }
 
-// dst <- src for `batch` n x n column-major matrices; lower = true copies only rows >= column (the
-// part a Hermitian sampler reads).  One CTA per (column, sample).
-template <typename T>
+// dst <- src for columns [c0, c1) of `batch` n x n column-major matrices; lower = true copies only
+// rows >= column (the part a Hermitian sampler reads).  Persistent warps walk (sample, column)
+// items; each warp moves one column with four 16-byte loads in flight per lane (the one-CTA-per-
+// column kernel it replaces wrote the UST batch's 40 GB at 3.6 TB/s).  V = 16-byte vectors when
+// both sides are 16-byte aligned (ld, stride, base), else one element per access.
+template <typename T, bool V>
 __global__ void __launch_bounds__(256) copy_matrix_kernel(const T* src, int64_t lds, int64_t strideS, T* dst,
-                                                          int64_t ldd, int64_t strideD, int n, bool lower) {
-  const int64_t j = blockIdx.x, s = blockIdx.y;
-  const T* a = src + s * strideS + j * lds;
-  T* b = dst + s * strideD + j * ldd;
-  for (int i = (lower ? (int)j : 0) + threadIdx.x; i < n; i += 256) b[i] = a[i];
+                                                          int64_t ldd, int64_t strideD, int n, int c0, int ncols,
+                                                          int batch, bool lower) {
+  constexpr int E = V ? 16 / (int)sizeof(T) : 1;  // elements per access
+  const int lane = threadIdx.x & 31;
+  const int64_t items = (int64_t)ncols * batch;
+  for (int64_t it = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); it < items; it += (int64_t)gridDim.x * 8) {
+    const int64_t s = it / ncols;
+    const int j = c0 + (int)(it % ncols);
+    const T* a = src + s * strideS + (int64_t)j * lds;
+    T* b = dst + s * strideD + (int64_t)j * ldd;
+    int i0 = lower ? j : 0;
+    if (V) {  // scalar head up to the first 16-byte boundary (same offset on both sides)
+      const int head = min(n - i0, (int)((E - (i0 % E)) % E));
+      if (lane < head) b[i0 + lane] = a[i0 + lane];
+      i0 += head;
+      const int nv = (n - i0) / E;
+      const uint4* av = reinterpret_cast<const uint4*>(a + i0);
+      uint4* bv = reinterpret_cast<uint4*>(b + i0);
+      int v = lane;
+      for (; v + 96 < nv; v += 128) {
+        const uint4 x0 = av[v], x1 = av[v + 32], x2 = av[v + 64], x3 = av[v + 96];
+        bv[v] = x0; bv[v + 32] = x1; bv[v + 64] = x2; bv[v + 96] = x3;
+      }
+      for (; v < nv; v += 32) bv[v] = av[v];
+      for (int i = i0 + nv * E + lane; i < n; i += 32) b[i] = a[i];
+    } else {
+      for (int i = i0 + lane; i < n; i += 32) b[i] = a[i];
+    }
+  }
 }
 
 cudaError_t launch_copy_matrix(size_t es, const void* src, int64_t lds, int64_t strideS, void* dst, int64_t ldd,
-                               int64_t strideD, int n, int batch, bool lower, cudaStream_t s) {
-  if (n <= 0 || batch <= 0) return cudaSuccess;
-  dim3 grid(n, batch);
-#define DPP_CP(T) copy_matrix_kernel<T><<<grid, 256, 0, s>>>(reinterpret_cast<const T*>(src), lds, strideS, \
-      reinterpret_cast<T*>(dst), ldd, strideD, n, lower)
+                               int64_t strideD, int n, int batch, bool lower, cudaStream_t s, int c0, int c1) {
+  if (c1 < 0 || c1 > n) c1 = n;
+  if (n <= 0 || batch <= 0 || c0 >= c1) return cudaSuccess;
+  const int ncols = c1 - c0;
+  const bool v = reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0 &&
+                 (lds * (int64_t)es) % 16 == 0 && (ldd * (int64_t)es) % 16 == 0 &&
+                 (strideS * (int64_t)es) % 16 == 0 && (strideD * (int64_t)es) % 16 == 0;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t items = (int64_t)ncols * batch;
+  const int64_t grid = std::min<int64_t>((items + 7) / 8, (int64_t)sms * 8);
+#define DPP_CP(T)                                                                                             \
+  do {                                                                                                        \
+    if (v)                                                                                                    \
+      copy_matrix_kernel<T, true><<<(unsigned)grid, 256, 0, s>>>(reinterpret_cast<const T*>(src), lds, strideS, \
+          reinterpret_cast<T*>(dst), ldd, strideD, n, c0, ncols, batch, lower);                               \
+    else                                                                                                      \
+      copy_matrix_kernel<T, false><<<(unsigned)grid, 256, 0, s>>>(reinterpret_cast<const T*>(src), lds, strideS, \
+          reinterpret_cast<T*>(dst), ldd, strideD, n, c0, ncols, batch, lower);                               \
+  } while (0)
   if (es == 4) DPP_CP(float);
   else if (es == 8) DPP_CP(double);
   else DPP_CP(double2);
@@ -274,6 +317,10 @@ static cudaError_t launch_update_core(Kind kind, UpdateArgs a, cudaStream_t s, b
 cudaError_t launch_update(Kind kind, UpdateArgs a, cudaStream_t s) {
   if (a.rows <= 0 || a.cols <= 0 || a.K <= 0) return cudaSuccess;
   const bool ws = a.vec && !a.generic && kind != HERM_S && kind != LU_C;
+  // a separate C source is read only by the warp-specialized kernel (16-byte aligned, no bcc)
+  if (a.csrc && (!ws || a.bcc_P > 0 || reinterpret_cast<uintptr_t>(a.csrc) % 16 || (a.ldcs * kind_esize(kind)) % 16 ||
+                 (a.strideCs * kind_esize(kind)) % 16))
+    return cudaErrorInvalidValue;
   // the second output W: fused into the warp-specialized panel kernel (no mask, Hermitian) or the
   // 3xTF32 kernel's epilogue (real single precision), else a column-scaling pass over the region
   const bool tc32 = kind == HERM_S && a.vec && !a.generic && !a.fp32_simt && !a.dscale && !a.conj && !a.bnmajor &&

@@ -357,3 +357,37 @@ def test_host_equals_device_path(oracle_mod, n):
     m = 600
     o = oracle_mod.sample_herm_d(Kc[:m, :m].cpu().numpy().T.copy(), 4, 0)
     compare_masks(mh[0].numpy()[:m], o)
+
+
+@pytest.mark.parametrize("kind,n,kw", [("herm_d", 1130, {}), ("herm_d", 2125, dict(group_min_rows=-1)),
+                                       ("herm_d", 700, dict(group=1)), ("herm_z", 555, {}),
+                                       ("herm_z", 555, dict(group_min_rows=-1))])
+def test_deferred_copy_bitwise(kind, n, kw):
+    """The batched entry points on a device kernel defer the workspace copy into the first updates
+    (they read K itself); the sample is bit for bit the in-place call's (which factors the caller's
+    copy), for a shared kernel, a strided batch of distinct kernels, and an odd leading dimension
+    (no deferral: K's columns are not 16-byte aligned).  K stays unmodified."""
+    opts = dpp.make_opts(**kw)
+    Ks = [_kernel(kind, n, seed=n + i) for i in range(3)]
+    ref = []
+    for i, K in enumerate(Ks):
+        Kc = to_device(K, kind)
+        si = dpp.sample(kind, Kc, 11, opts=opts)
+        torch.cuda.synchronize()
+        ref.append((si.mask.clone(), si.loglik.clone(), si.info.clone()))
+    for ld in (n, n + 1):
+        Kd = to_device(Ks[0], kind, ld)
+        K0 = Kd.clone()
+        sb = dpp.sample_batched(kind, Kd, 2, seed=11, b0=0, opts=opts)
+        torch.cuda.synchronize()
+        assert torch.equal(Kd, K0), "batched call wrote its read-only K"
+        assert torch.equal(sb.mask[0], ref[0][0]) and float(sb.loglik[0]) == float(ref[0][1]), (kind, ld)
+        assert torch.equal(sb.info[0], ref[0][2]), (kind, ld)
+    Kst = torch.stack([to_device(K, kind) for K in Ks])  # strided batch: sample b of kernel b
+    for b in range(3):
+        sb = dpp.sample_batched(kind, Kst[b:b + 1], 1, seed=11, b0=0, opts=opts)
+        torch.cuda.synchronize()
+        assert torch.equal(sb.mask[0], ref[b][0]) and float(sb.loglik[0]) == float(ref[b][1]), (kind, b)
+    sb = dpp.sample_batched(kind, Kst, 3, seed=11, b0=0, opts=opts)
+    torch.cuda.synchronize()
+    assert torch.equal(sb.mask[0], ref[0][0]) and float(sb.loglik[0]) == float(ref[0][1])
