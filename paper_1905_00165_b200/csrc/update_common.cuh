@@ -70,23 +70,6 @@ struct MmaAcc {
         if (CPLX) im[CPLX ? i : 0][CPLX ? j : 0][0] = im[CPLX ? i : 0][CPLX ? j : 0][1] = 0.0;
       }
   }
-  // Cs(r, c) -= acc with fragment j at tile columns col[j] .. col[j] + 7 (real, no mask)
-  template <int TM, int LDC>
-  __device__ __forceinline__ void subtract_into_cols(double* Cs, int wm, const int (&col)[NI], int lane,
-                                                     const TileInfo& ti) const {
-#pragma unroll
-    for (int i = 0; i < MI; ++i) {
-      const int r = wm * TM + i * 8 + (lane >> 2);
-#pragma unroll
-      for (int j = 0; j < NI; ++j) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int c = col[j] + 2 * (lane & 3) + e;
-          if (r < ti.nrows && c < ti.ncols) Cs[c * LDC + r] -= re[i][j][e];
-        }
-      }
-    }
-  }
   // Cs(r, c) -= acc for the elements this lane owns; MASK keeps the strict upper triangle intact
   template <bool MASK, int TM, int TN, int LDC>
   __device__ __forceinline__ void subtract_into(typename Elem<CPLX>::T* Cs, int wm, int wn, int lane,

@@ -53,37 +53,6 @@ struct WsLayoutT {
   static constexpr int NT = (NCONS + 2) * 32;   // + operand producer warp + C-tile warp
 };
 
-// Real unmasked launches (the stage-2 panel GEMMs, whose operator B is triangular: op(B)(j, k) = 0
-// for k > j) give each consumer warp its NI 8-column fragments SNAKED over the tile instead of TN
-// adjacent columns: fragment j of warp column wn covers tile columns j*WN*8 + (j odd ? WN-1-wn : wn)*8.
-// A fragment skips the K-chunks past its last column, and with the snake every warp column does the
-// same number of fragment-chunks (34 of 64 at K = BN = 128), where the contiguous map left warp
-// column 0 idle for 3/4 of the tile while warp column 3 paced the ring through every chunk.
-template <int WN, int NI>
-__device__ __forceinline__ int snake_col(int j, int wn) {
-  return j * WN * 8 + ((j & 1) ? (WN - 1 - wn) : wn) * 8;
-}
-
-// acc += A_chunk B_chunk^T (real, K-major B) for the fragments whose bit is set in `act`
-template <int KC, int MI, int NI, int LDA, int LDBK>
-__device__ __forceinline__ void mma_chunk_cols(MmaAcc<false, MI, NI>& acc, const double* As, const double* Bs,
-                                               int m_off, const int (&col)[NI], unsigned act, int lane) {
-#pragma unroll
-  for (int ks = 0; ks < KC / 4; ++ks) {
-    const int kk = ks * 4 + (lane & 3);
-    double af[MI];
-#pragma unroll
-    for (int i = 0; i < MI; ++i) af[i] = As[kk * LDA + m_off + i * 8 + (lane >> 2)];
-#pragma unroll
-    for (int j = 0; j < NI; ++j) {
-      if (!(act >> j & 1u)) continue;
-      const double bf = Bs[kk * LDBK + col[j] + (lane >> 2)];
-#pragma unroll
-      for (int i = 0; i < MI; ++i) dmma884(acc.re[i][j][0], acc.re[i][j][1], af[i], bf);
-    }
-  }
-}
-
 __device__ __forceinline__ void consumer_sync(int nthreads) {
   asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
 }
@@ -236,10 +205,6 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
 
   // ============================ consumer warps ============================
   const int wm = warp % C::WM, wn = warp / C::WM;
-  constexpr bool SNAKE = !CPLX && !MASK && !SCALE && !BNMAJ;
-  int col[NI];  // first tile column of each 8-column fragment of this warp
-#pragma unroll
-  for (int j = 0; j < NI; ++j) col[j] = SNAKE ? snake_col<C::WN, NI>(j, wn) : wn * TN + j * 8;
   int stage = 0;
   uint32_t phase = 0, cphase = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -253,10 +218,7 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
     const int kc0 = a.ktri ? ti.grow0 / C::KC : 0;
     // triangular B (stage-2 operators): the warp's columns need k <= its last column only; the
     // chunks past it are waited for and released without DMMA (the ring is shared by all warps)
-    int lastcol = 0;  // the warp's last tile column
-#pragma unroll
-    for (int j = 0; j < NI; ++j) lastcol = max(lastcol, col[j] + 7);
-    const int kcend = a.btri ? min(nchunks, (ti.gcol0 + lastcol + 1 + C::KC - 1) / C::KC) : nchunks;
+    const int kcend = a.btri ? min(nchunks, (ti.gcol0 + wn * TN + TN + C::KC - 1) / C::KC) : nchunks;
     if (idle) {
       for (int kc = kc0; kc < nchunks; ++kc) {
         mbar_wait(&full[stage], phase);
@@ -274,20 +236,9 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
           continue;
         }
         const T* As = ring + stage * LY::STAGE_ELEMS;
-        if constexpr (SNAKE) {
-          // fragments whose last column is below this chunk's first k multiply only zeros (btri)
-          unsigned act = (1u << NI) - 1u;
-          if (a.btri) {
-            act = 0u;
-#pragma unroll
-            for (int j = 0; j < NI; ++j) act |= (ti.gcol0 + col[j] + 7 >= kc * C::KC ? 1u : 0u) << j;
-          }
-          mma_chunk_cols<C::KC, MI, NI, LY::LDA, LY::LDBK>(acc, As, As + LY::A_ELEMS, wm * TM, col, act, lane);
-        } else {
-          mma_chunk<CPLX, BNMAJ, SCALE, CONJ, C::KC, MI, NI, LY::LDA, LY::LDBK, LY::LDBN>(
-              acc, As, As + LY::A_ELEMS, reinterpret_cast<const double*>(As + LY::A_ELEMS + LY::B_ELEMS), wm * TM,
-              wn * TN, lane);
-        }
+        mma_chunk<CPLX, BNMAJ, SCALE, CONJ, C::KC, MI, NI, LY::LDA, LY::LDBK, LY::LDBN>(
+            acc, As, As + LY::A_ELEMS, reinterpret_cast<const double*>(As + LY::A_ELEMS + LY::B_ELEMS), wm * TM,
+            wn * TN, lane);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -296,28 +247,18 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
     // ---- epilogue: C -= acc in shared memory; the C warp writes the tile back
     mbar_wait(cfull, cphase);
     cphase ^= 1;
-    if constexpr (SNAKE) {
-      acc.template subtract_into_cols<TM, LY::LDC>(Cs, wm, col, lane, ti);
-    } else {
-      acc.template subtract_into<MASK, TM, TN, LY::LDC>(Cs, wm, wn, lane, ti);
-    }
+    acc.template subtract_into<MASK, TM, TN, LY::LDC>(Cs, wm, wn, lane, ti);
     if constexpr (!MASK) {
       if (a.wout) {
         // second output W = C_new diag(wscale) (the Hermitian panel's W21 = L21 D1): each warp
-        // re-reads the TM x TN part of the updated tile it wrote, one row per lane, coalesced stores
+        // re-reads its own TM x TN part of the updated tile, one row per lane, coalesced stores
         __syncwarp();
         T* Wg = reinterpret_cast<T*>(a.wout) + (int64_t)ti.s * a.strideWo + ti.grow0 + (int64_t)ti.gcol0 * a.ldw;
         const double* d = a.wscale + (int64_t)ti.s * a.wsstride + ti.gcol0;
-#pragma unroll
-        for (int j = 0; j < NI; ++j) {
-#pragma unroll
-          for (int cc = 0; cc < 8; ++cc) {
-            const int c = col[j] + cc;
-            if (c >= ti.ncols) continue;
-            const double dc = __ldg(d + c);
-            for (int r = wm * TM + lane; r < wm * TM + TM && r < ti.nrows; r += 32)
-              Wg[r + (int64_t)c * a.ldw] = scal(Cs[c * LY::LDC + r], dc);
-          }
+        for (int c = wn * TN; c < wn * TN + TN && c < ti.ncols; ++c) {
+          const double dc = __ldg(d + c);
+          for (int r = wm * TM + lane; r < wm * TM + TM && r < ti.nrows; r += 32)
+            Wg[r + (int64_t)c * a.ldw] = scal(Cs[c * LY::LDC + r], dc);
         }
       }
     }
