@@ -245,6 +245,14 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
       }
     }
     // ---- epilogue: C -= acc in shared memory; the C warp writes the tile back
+    // (the W21 scale of this lane's column is loaded first: its latency hides behind the wait and
+    // the subtraction instead of sitting, once per column, inside the store loop below)
+    double dl = 0.0;
+    if constexpr (!MASK) {
+      static_assert(MASK || TN <= 32, "one W21 scale per lane");
+      if (a.wout && lane < TN && wn * TN + lane < ti.ncols)
+        dl = __ldg(a.wscale + (int64_t)ti.s * a.wsstride + ti.gcol0 + wn * TN + lane);
+    }
     mbar_wait(cfull, cphase);
     cphase ^= 1;
     acc.template subtract_into<MASK, TM, TN, LY::LDC>(Cs, wm, wn, lane, ti);
@@ -254,11 +262,13 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
         // re-reads its own TM x TN part of the updated tile, one row per lane, coalesced stores
         __syncwarp();
         T* Wg = reinterpret_cast<T*>(a.wout) + (int64_t)ti.s * a.strideWo + ti.grow0 + (int64_t)ti.gcol0 * a.ldw;
-        const double* d = a.wscale + (int64_t)ti.s * a.wsstride + ti.gcol0;
-        for (int c = wn * TN; c < wn * TN + TN && c < ti.ncols; ++c) {
-          const double dc = __ldg(d + c);
-          for (int r = wm * TM + lane; r < wm * TM + TM && r < ti.nrows; r += 32)
-            Wg[r + (int64_t)c * a.ldw] = scal(Cs[c * LY::LDC + r], dc);
+#pragma unroll 8
+        for (int cc = 0; cc < TN; ++cc) {
+          const int c = wn * TN + cc;
+          const double dc = __shfl_sync(0xffffffffu, dl, cc);
+          if (c < ti.ncols)
+            for (int r = wm * TM + lane; r < wm * TM + TM && r < ti.nrows; r += 32)
+              Wg[r + (int64_t)c * a.ldw] = scal(Cs[c * LY::LDC + r], dc);
         }
       }
     }
