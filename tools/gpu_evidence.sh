@@ -16,7 +16,7 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log
 python tools/timeline.py > gpurun_out/timeline.json 2> gpurun_out/timeline.err
 python tools/timeline.py 3120 0 1024 > gpurun_out/timeline_ust.json 2> gpurun_out/timeline_ust.err
-nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -DDIAG_OLD -I include -I paper_1905_00165_b200/csrc tools/diag_timing.cu -o tools/diag_timing.bin > /dev/null 2>&1
+nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -I include -I paper_1905_00165_b200/csrc tools/diag_timing.cu -o tools/diag_timing.bin > /dev/null 2>&1
 { timeout 60 tools/diag_timing.bin 1 50 128 128 0; for a in "1 20 128 131 0" "1 20 128 130 1" "1 20 64 64 0" "148 10 128 128 0" "1024 5 128 128 0"; do timeout 60 tools/diag_timing.bin $a | head -1; done; } > gpurun_out/diag_timing.txt 2>&1
 CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-dist --streams 1"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
