@@ -102,11 +102,14 @@ struct MmaAcc {
 // One shared-memory K-chunk: acc += A_chunk * op(B_chunk)^T with DMMA.8x8x4.
 //   A: [KC][LDA] (row k holds the BM rows), B: [KC][LDBK] (K-major) or [BN][LDBN] (N-major),
 //   Ds: [KC] per-k scale of B (SCALE), CONJ: conjugate B (Hermitian complex).
+//   tri (real only, warp-uniform): the warp tile sits on the diagonal of a masked Hermitian tile,
+//   so the 8x8 fragments strictly above it (j > i) are never stored and their DMMAs are
+//   predicated off (one predicate, no second copy of the loop).
 // Fragments: a = A[m = lane>>2][k = lane&3], b = B[k = lane&3][n = lane>>2].
 template <bool CPLX, bool BNMAJ, bool SCALE, bool CONJ, int KC, int MI, int NI, int LDA, int LDBK, int LDBN>
 __device__ __forceinline__ void mma_chunk(MmaAcc<CPLX, MI, NI>& acc, const typename Elem<CPLX>::T* As,
                                           const typename Elem<CPLX>::T* Bs, const double* Ds, int m_off, int n_off,
-                                          int lane) {
+                                          int lane, bool tri = false) {
   using T = typename Elem<CPLX>::T;
 #pragma unroll
   for (int ks = 0; ks < KC / 4; ++ks) {
@@ -125,7 +128,8 @@ __device__ __forceinline__ void mma_chunk(MmaAcc<CPLX, MI, NI>& acc, const typen
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < NI; ++j) dmma884(acc.re[i][j][0], acc.re[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < NI; ++j)
+          if (j <= i || !tri) dmma884(acc.re[i][j][0], acc.re[i][j][1], af[i], bf[j]);
     } else {
       // a*b:       re += ar br - ai bi ;  im += ar bi + ai br
       // a*conj(b): re += ar br + ai bi ;  im += ai br - ar bi

@@ -204,7 +204,21 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
   }
 
   // ============================ consumer warps ============================
-  const int wm = warp % C::WM, wn = warp / C::WM;
+  // Warp -> warp tile.  A warp's DMMAs run on its sub-partition's FP64 pipe (SMSP = warp & 3, one
+  // warp saturates it: tools/dmma_tput.cu), so a tile takes as long as its busiest sub-partition.
+  // Real 4 x 4 layout: the plain map wm = warp & 3 would put the four working warps of row 3 of a
+  // masked diagonal tile on one sub-partition (the tile as slow as a full one); this table gives
+  // every sub-partition one warp tile per column with, on a diagonal tile, (below, below, idle, idle)
+  // on two of them and (diag, diag, below, idle) on the other two: 2 / 2.25 warp tiles of DMMAs
+  // instead of 4 (diagonal warp tiles skip their 6 of 16 fragments above the diagonal).
+  int wm = warp % C::WM;
+  const int wn = warp / C::WM;
+  if constexpr (MASK && !CPLX && C::WM == 4 && C::WN == 4) {
+    // wm[s = warp & 3][wn]: s0 {0,1,3,0}, s1 {1,0,2,3}, s2 {2,2,0,1}, s3 {3,3,1,2}; each column a permutation
+    constexpr uint32_t TBL = (0u | 1u << 2 | 3u << 4 | 0u << 6) | (1u | 0u << 2 | 2u << 4 | 3u << 6) << 8 |
+                             (2u | 2u << 2 | 0u << 4 | 1u << 6) << 16 | (3u | 3u << 2 | 1u << 4 | 2u << 6) << 24;
+    wm = (TBL >> (8 * (warp & 3) + 2 * wn)) & 3;
+  }
   int stage = 0;
   uint32_t phase = 0, cphase = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -215,6 +229,7 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
     // a warp tile strictly above the diagonal of a masked diagonal tile writes nothing: it only
     // keeps pace with the ring (waits and releases every stage) and leaves the DMMA pipe to the others
     const bool idle = MASK && ti.diag && ti.gcol0 + wn * TN > ti.grow0 + wm * TM + TM - 1;
+    const bool wdiag = !CPLX && MASK && TM == TN && ti.diag && ti.gcol0 + wn * TN == ti.grow0 + wm * TM;
     const int kc0 = a.ktri ? ti.grow0 / C::KC : 0;
     // triangular B (stage-2 operators): the warp's columns need k <= its last column only; the
     // chunks past it are waited for and released without DMMA (the ring is shared by all warps)
@@ -238,7 +253,7 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
         const T* As = ring + stage * LY::STAGE_ELEMS;
         mma_chunk<CPLX, BNMAJ, SCALE, CONJ, C::KC, MI, NI, LY::LDA, LY::LDBK, LY::LDBN>(
             acc, As, As + LY::A_ELEMS, reinterpret_cast<const double*>(As + LY::A_ELEMS + LY::B_ELEMS), wm * TM,
-            wn * TN, lane);
+            wn * TN, lane, wdiag);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
