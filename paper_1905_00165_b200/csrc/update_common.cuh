@@ -104,7 +104,8 @@ struct MmaAcc {
 //   Ds: [KC] per-k scale of B (SCALE), CONJ: conjugate B (Hermitian complex).
 //   tri (real only, warp-uniform): the warp tile sits on the diagonal of a masked Hermitian tile,
 //   so the 8x8 fragments strictly above it (j > i) are never stored and their DMMAs are
-//   predicated off (one predicate, no second copy of the loop).
+//   predicated off (one predicate, no second copy of the loop; grouping them under one branch per
+//   k-step keeps all A fragments live and spills).
 // Fragments: a = A[m = lane>>2][k = lane&3], b = B[k = lane&3][n = lane>>2].
 template <bool CPLX, bool BNMAJ, bool SCALE, bool CONJ, int KC, int MI, int NI, int LDA, int LDBK, int LDBN>
 __device__ __forceinline__ void mma_chunk(MmaAcc<CPLX, MI, NI>& acc, const typename Elem<CPLX>::T* As,

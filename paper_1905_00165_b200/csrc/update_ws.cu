@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
   }
   int stage = 0;
   uint32_t phase = 0, cphase = 0;
+  bool ready = false;  // the current stage's full barrier was already seen complete
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const TileInfo ti = tile_info<C::BM, C::BN>(a, t, tiles_per_sample, MASK);
     if (!ti.valid) continue;
@@ -236,27 +237,38 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
     const int kcend = a.btri ? min(nchunks, (ti.gcol0 + wn * TN + TN + C::KC - 1) / C::KC) : nchunks;
     if (idle) {
       for (int kc = kc0; kc < nchunks; ++kc) {
-        mbar_wait(&full[stage], phase);
+        if (!ready) mbar_wait(&full[stage], phase);
+        ready = false;
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     } else {
-      for (int kc = kc0; kc < nchunks; ++kc) {
-        mbar_wait(&full[stage], phase);
-        if (kc >= kcend) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[stage]);
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
-          continue;
+      // One copy of the chunk body per ring stage (s is a constant in each): the operand and barrier
+      // addresses are base + immediate, so nothing but the fragment loads sits between a chunk's
+      // wait and its first DMMA; and the NEXT stage's barrier is tested a whole chunk early
+      // (`ready`), so the wait itself leaves the chunk boundary when the producer is ahead.  The four
+      // warps of a sub-partition reach a chunk boundary together (they share one FP64 pipe fairly):
+      // whatever a boundary costs beyond the other warps' three DMMA slots idles the pipe.
+      int kc = kc0;
+      while (kc < nchunks) {
+#pragma unroll
+        for (int s = 0; s < C::STAGES; ++s) {
+          if (s == stage && kc < nchunks) {
+            if (!ready) mbar_wait(&full[s], phase);
+            ready = mbar_test(&full[(s + 1) % C::STAGES], s + 1 == C::STAGES ? phase ^ 1 : phase);
+            if (kc < kcend) {
+              const T* As = ring + s * LY::STAGE_ELEMS;
+              mma_chunk<CPLX, BNMAJ, SCALE, CONJ, C::KC, MI, NI, LY::LDA, LY::LDBK, LY::LDBN>(
+                  acc, As, As + LY::A_ELEMS, reinterpret_cast<const double*>(As + LY::A_ELEMS + LY::B_ELEMS), wm * TM,
+                  wn * TN, lane, wdiag);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            ++kc;
+            if (s + 1 == C::STAGES) { stage = 0; phase ^= 1; } else { stage = s + 1; }
+          }
         }
-        const T* As = ring + stage * LY::STAGE_ELEMS;
-        mma_chunk<CPLX, BNMAJ, SCALE, CONJ, C::KC, MI, NI, LY::LDA, LY::LDBK, LY::LDBN>(
-            acc, As, As + LY::A_ELEMS, reinterpret_cast<const double*>(As + LY::A_ELEMS + LY::B_ELEMS), wm * TM,
-            wn * TN, lane, wdiag);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
-        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
     // ---- epilogue: C -= acc in shared memory; the C warp writes the tile back
@@ -302,6 +314,10 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
   }
 }
 
+#ifndef DPP_WS_TPC
+#define DPP_WS_TPC 8  // tiles per short-lived CTA (tools/gpu_tpc_sweep.sh: UST 2913 / 2929 / 2925 samples/s for 4 / 8 / 16, 2860 for 2; C4 flat)
+#endif
+
 static int num_sms() {
   static int sms[64] = {0};
   int dev = 0;
@@ -322,9 +338,9 @@ cudaError_t launch_update_ws_v(UpdateArgs a, cudaStream_t s) {
   const long long per = a.tri ? (long long)a.tiles_m * (a.tiles_m + 1) / 2 : (long long)a.tiles_m * a.tiles_n;
   const long long total = per * a.batch;
   if (total <= 0) return cudaSuccess;
-  // short-lived CTAs walk <= TPC = 4 tiles each (at least one wave of the SMs), so the high-priority
+  // short-lived CTAs walk <= TPC = 8 tiles each (at least one wave of the SMs), so the high-priority
   // lookahead stream still finds SMs between tiles; persistent launches take the CTAs granted
-  constexpr long long TPC = 4;
+  constexpr long long TPC = DPP_WS_TPC;
   long long g;
   if (a.grid_limit > 0) {
     const long long lim = (long long)a.grid_limit * CPS;
