@@ -21,12 +21,6 @@
 #include "kernels.h"
 #include "update_common.cuh"
 
-#ifndef DPP_WS_DIAG_NOC
-#define DPP_WS_DIAG_NOC 0  // timing diagnostic (tools/gpu_prefetch_ab.sh): drop the C-tile traffic
-#endif
-#ifndef DPP_WS_PREFETCH
-#define DPP_WS_PREFETCH 0  // L2 prefetch of the next tile's operands by the producer warp (experiment)
-#endif
 
 namespace dpp {
 
@@ -103,7 +97,7 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
       if (!have_prev) return;
       mbar_wait(cready, rphase);
       rphase ^= 1;
-      if (!prev.diag && !DPP_WS_DIAG_NOC) {
+      if (!prev.diag) {
         T* Cg = reinterpret_cast<T*>(a.C) + (int64_t)prev.s * a.strideC;
         const int cbulk = CPLX ? prev.nrows : (prev.nrows & ~1);
         if (cbulk > 0)
@@ -134,15 +128,9 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
       }
       fence_proxy_async_smem();  // generic smem accesses before the async-proxy writes
       __syncwarp();
-#if DPP_WS_DIAG_NOC  // timing diagnostic only (wrong results): no C-tile loads or stores
-      if (lane == 0) mbar_arrive(cfull);
-      __syncwarp();
-      if (false)
-#else
       if (lane == 0) mbar_arrive_expect_tx(cfull, (uint32_t)(ti.ncols * cbulk * LY::ES));
       __syncwarp();
       if (cbulk > 0)
-#endif
         for (int c = lane; c < ti.ncols; c += 32)
           bulk_g2s(Cs + c * LY::LDC, Cg + ti.grow0 + (ti.gcol0 + c - ti.cshift) * ldr, (uint32_t)(cbulk * LY::ES),
                    cfull);
@@ -167,27 +155,7 @@ __global__ void __launch_bounds__(WsLayoutT<CPLX, BNMAJ, V>::NT, 1) update_ws_ke
       const int arows = min(C::BM, a.a_rows - ti.grow0);   // operand rows that exist
       const int bcols = min(C::BN, a.b_rows - ti.gcol0);
       const int abulk = CPLX ? arows : (arows & ~1), bbulk = CPLX ? bcols : (bcols & ~1);
-#if DPP_WS_PREFETCH
-      // the NEXT tile's operand segments, chunk by chunk, into L2 while this tile runs: the ring's
-      // own loads (issued <= STAGES chunks ahead) then never wait on DRAM
-      TileInfo tn{};
-      tn.valid = false;
-      if (!BNMAJ && t + (int)gridDim.x < ntiles) tn = tile_info<C::BM, C::BN>(a, t + gridDim.x, tiles_per_sample, MASK);
-      const int pa = tn.valid ? (min(C::BM, a.a_rows - tn.grow0) & ~1) : 0;
-      const int pb = tn.valid ? (min(C::BN, a.b_rows - tn.gcol0) & ~1) : 0;
-      const T* Agn = reinterpret_cast<const T*>(a.Aop) + (int64_t)tn.s * a.strideA + tn.grow0;
-      const T* Bgn = reinterpret_cast<const T*>(a.Bop) + (int64_t)tn.s * a.strideB + tn.gcol0;
-#endif
       for (int kc = a.ktri ? ti.grow0 / C::KC : 0; kc < nchunks; ++kc) {
-#if DPP_WS_PREFETCH
-        if (tn.valid) {
-          const int kk = kc * C::KC + (lane & (C::KC - 1));
-          if (kk < a.K) {
-            if (lane < C::KC && pa > 0) bulk_prefetch_l2(Agn + (int64_t)kk * a.lda, (uint32_t)(pa * LY::ES));
-            else if (lane >= C::KC && lane < 2 * C::KC && pb > 0) bulk_prefetch_l2(Bgn + (int64_t)kk * a.ldb, (uint32_t)(pb * LY::ES));
-          }
-        }
-#endif
         mbar_wait(&empty[stage], phase ^ 1);
         T* As = ring + stage * LY::STAGE_ELEMS;
         T* Bs = As + LY::A_ELEMS;
