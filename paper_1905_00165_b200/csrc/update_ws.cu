@@ -22,11 +22,16 @@
 #include "update_common.cuh"
 
 
+#ifndef DPP_WS_KC
+#define DPP_WS_KC 8       // real kernels: k per ring stage ...
+#define DPP_WS_STAGES 5   // ... and ring stages (tools/gpu_update_ab.sh)
+#endif
+
 namespace dpp {
 
 template <bool CPLX, int V> struct WsCfg;
 template <> struct WsCfg<false, 1> {  // real: 128x128 tile, 16 consumer warps 4 x 4 of 32x32
-  static constexpr int BM = 128, BN = 128, WM = 4, WN = 4, KC = 8, STAGES = 5;
+  static constexpr int BM = 128, BN = 128, WM = 4, WN = 4, KC = DPP_WS_KC, STAGES = DPP_WS_STAGES;
 };
 template <> struct WsCfg<true, 0> {   // complex: 64x64 tile, consumer warps 2 x 4 of 32x16
   static constexpr int BM = 64, BN = 64, WM = 2, WN = 4, KC = 8, STAGES = 4;
