@@ -22,9 +22,18 @@
 #include "update_common.cuh"
 
 
+// Ring geometry (tools/gpu_update_ab.sh).  A chunk boundary (barrier round, first fragment loads) is
+// reached by the four warps of a sub-partition together and idles its FP64 pipe, so FEW LARGE chunks
+// beat a deep ring of small ones: real kernels 2 stages of 16 k (64 DMMAs per warp and chunk) --
+// probe K = 384: 33.8 TF/s against 32.9 for 5 x 8 k and 32.1 for 11 x 4 k; 3 x 12 k the same but
+// K = 128 is not a multiple of 12 (profiles/r02/update_ab.txt).
 #ifndef DPP_WS_KC
-#define DPP_WS_KC 8       // real kernels: k per ring stage ...
-#define DPP_WS_STAGES 5   // ... and ring stages (tools/gpu_update_ab.sh)
+#define DPP_WS_KC 16      // real kernels: k per ring stage ...
+#define DPP_WS_STAGES 2   // ... and ring stages
+#endif
+#ifndef DPP_WS_KCZ
+#define DPP_WS_KCZ 8      // complex kernels
+#define DPP_WS_STAGESZ 4
 #endif
 
 namespace dpp {
@@ -34,7 +43,7 @@ template <> struct WsCfg<false, 1> {  // real: 128x128 tile, 16 consumer warps 4
   static constexpr int BM = 128, BN = 128, WM = 4, WN = 4, KC = DPP_WS_KC, STAGES = DPP_WS_STAGES;
 };
 template <> struct WsCfg<true, 0> {   // complex: 64x64 tile, consumer warps 2 x 4 of 32x16
-  static constexpr int BM = 64, BN = 64, WM = 2, WN = 4, KC = 8, STAGES = 4;
+  static constexpr int BM = 64, BN = 64, WM = 2, WN = 4, KC = DPP_WS_KCZ, STAGES = DPP_WS_STAGESZ;
 };
 
 template <bool CPLX, bool BNMAJ, int V>
