@@ -32,8 +32,8 @@
 #define DPP_WS_STAGES 2   // ... and ring stages
 #endif
 #ifndef DPP_WS_KCZ
-#define DPP_WS_KCZ 8      // complex kernels
-#define DPP_WS_STAGESZ 4
+#define DPP_WS_KCZ 16     // complex kernels (64 x 64 tiles): 4 stages of 16 k -- Aztec d = 80 33.3 -> 34.3 TF/s,
+#define DPP_WS_STAGESZ 4  // n = 32768 block-cyclic 31.1 -> 32.5, n = 8192 Hermitian / LU +2.8 / +2.2 % over 4 x 8 k
 #endif
 
 namespace dpp {
